@@ -1,0 +1,152 @@
+/* f3rg.h -- C ABI of the B200-native F3R hot path (fp64 FGMRES > fp32 FGMRES >
+ * fp16-matrix FGMRES > fp16 Richardson, arXiv 2505.20719).
+ *
+ * This is the drop-in boundary for the reference's solve path. The reference is a
+ * C++ library (/root/reference/proj); its per-vector virtuals
+ * (LinearOperator::multiply/precondition, include/f3r/operator.hpp:19-27) run
+ * ~10^4 times per solve, so the device boundary sits one level up, at the
+ * ComposedSolver (include/f3r/nesting.hpp:55-77): one call solves the whole nest.
+ * Kernel-level entry points replace the reference's BLAS-1/SpMV free functions and
+ * are what the parity tests call. Plain pointers and sizes only; no torch types.
+ *
+ * Precision tags: 0 = binary16, 1 = binary32, 2 = binary64 (reference enum
+ * f3r::Precision, include/f3r/precision.hpp:20).
+ *
+ * Error convention (reference include/f3r/errors.hpp:12-38): every function
+ * returns 0 on success or one of the F3RG_E* codes, matching the exception class
+ * the reference throws; f3rg_last_error() returns the message of the calling
+ * thread's last failure. Non-convergence is NOT an error (reference
+ * src/nesting.cpp:283-306): it is report.converged == 0 plus report.flag.
+ *
+ * Ownership (reference include/f3r/nesting.hpp:51-54): host arrays passed in are
+ * borrowed for the duration of the call only; the library owns every device copy.
+ * A solver handle is not re-entrant (one host thread at a time, Richardson weights
+ * mutate), distinct handles may share one matrix handle and run concurrently.
+ */
+#ifndef F3RG_H
+#define F3RG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  F3RG_OK = 0,
+  F3RG_EDIMENSION = 2,     /* f3r::DimensionError */
+  F3RG_ESOLVER = 3,        /* f3r::SolverError */
+  F3RG_EPARSE = 4,         /* f3r::ParseError */
+  F3RG_EFACTORIZATION = 5, /* f3r::FactorizationError */
+  F3RG_ECUDA = 6,          /* CUDA runtime failure (no reference counterpart) */
+  F3RG_EUNSUPPORTED = 7,   /* valid reference input not implemented on the device */
+  F3RG_EINTERNAL = 9
+};
+
+enum { F3RG_P16 = 0, F3RG_P32 = 1, F3RG_P64 = 2 };
+enum { F3RG_PRECOND_ILU0 = 0, F3RG_PRECOND_IC0 = 1, F3RG_PRECOND_IDENTITY = 2 };
+
+typedef struct f3rg_matrix f3rg_matrix; /* SparseCsr + PrecisionReplicas on the device */
+typedef struct f3rg_solver f3rg_solver; /* ComposedSolver on the device */
+
+/* fp64 CSR in host memory; u32 indices (reference include/f3r/csr.hpp:23-67) */
+typedef struct {
+  uint64_t n;
+  const uint32_t* row_ptr; /* n+1 */
+  const uint32_t* col_idx; /* row_ptr[n] */
+  const double* values;    /* row_ptr[n] */
+} f3rg_csr;
+
+/* reference RunOptions, include/f3r/nesting.hpp:29-38 */
+typedef struct {
+  double tol;
+  int32_t max_outer_restarts;
+  uint64_t max_outer_total;
+  int32_t reset_richardson_on_restart;
+} f3rg_run_options;
+
+/* reference ConvergenceReport, include/f3r/report.hpp:18-30 (fixed-size view; the
+ * variable-length fields are fetched with f3rg_solver_history / _level_iterations /
+ * _omegas) */
+typedef struct {
+  int32_t converged;
+  uint64_t outer_iterations;
+  uint64_t precond_invocations;
+  double final_true_residual;
+  double wall_seconds;
+  uint64_t n_history;
+  uint64_t n_levels;
+  uint64_t n_omegas;
+  char flag[128];
+} f3rg_report;
+
+const char* f3rg_last_error(void);
+const char* f3rg_version(void);
+void f3rg_default_run_options(f3rg_run_options* opts); /* tol 1e-8, 3, 300, 0 */
+
+/* ---- matrices (replaces SparseCsr(...) + make_replicas, src/csr.cpp:40-69,130-136) */
+int f3rg_matrix_create(f3rg_matrix** out, const f3rg_csr* a64);
+void f3rg_matrix_destroy(f3rg_matrix* a);
+uint64_t f3rg_matrix_rows(const f3rg_matrix* a);
+uint64_t f3rg_matrix_nnz(const f3rg_matrix* a);
+/* replica values widened to fp64 into host memory (nnz doubles) */
+int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host);
+
+/* ---- solver spec grammar (replaces parse_solver_spec / SolverSpec::to_string,
+ *      src/solver_spec.cpp:147-212) */
+int f3rg_spec_canonical(const char* spec, char* out, size_t cap);
+
+/* ---- composed solver (replaces build(spec, replicas, M) + ComposedSolver::run,
+ *      src/nesting.cpp:176-352,354-357). precond_kind must be IDENTITY on this
+ *      build (the spec's terminal, like the reference's, only names it). */
+int f3rg_solver_create(f3rg_solver** out, const f3rg_matrix* a, const char* spec, int precond_kind);
+void f3rg_solver_destroy(f3rg_solver* s);
+const char* f3rg_solver_id(const f3rg_solver* s);
+/* b, x: HOST fp64 arrays of length n (x may be NULL); copies happen inside */
+int f3rg_solve(f3rg_solver* s, const double* b_host, double* x_host, const f3rg_run_options* opts,
+               f3rg_report* rep);
+/* b, x: DEVICE fp64 arrays (x may be NULL); stream: cudaStream_t or 0 (own stream) */
+int f3rg_solve_device(f3rg_solver* s, const double* b_dev, double* x_dev, const f3rg_run_options* opts,
+                      f3rg_report* rep, uintptr_t stream);
+/* report vectors of the LAST solve (host memory, up to cap entries) */
+int f3rg_solver_history(const f3rg_solver* s, double* out, uint64_t cap);
+int f3rg_solver_level_iterations(const f3rg_solver* s, uint64_t* out, uint64_t cap);
+int f3rg_solver_omegas(f3rg_solver* s, double* out, uint64_t cap); /* innermost_omegas() */
+/* per-kernel timing of the next solve (CUDA events around each launch; the solve
+ * runs eagerly instead of through the captured graph) */
+int f3rg_solver_set_profile(f3rg_solver* s, int on);
+/* kernel i of the last profiled solve: name, total ms, launches, algorithmic bytes */
+int f3rg_solver_profile_entry(const f3rg_solver* s, uint64_t i, char* name, size_t cap, double* ms,
+                              uint64_t* launches, double* bytes);
+
+/* ---- kernel-level entry points (device pointers, stream = cudaStream_t or 0) ---
+ * Each mirrors one reference free function, same argument meaning. */
+int f3rg_spmv(const f3rg_matrix* a, int prec_a, const void* x, int prec_x, void* y, int prec_y,
+              uintptr_t stream); /* spmv, src/csr.cpp:138-147 */
+int f3rg_dot(const void* x, int prec_x, const void* y, int prec_y, uint64_t n, int floor_prec, double* out_host,
+             uintptr_t stream); /* dot_at_least, src/vector_ops.cpp:154-164 */
+int f3rg_norm2(const void* x, int prec_x, uint64_t n, double* out_host, uintptr_t stream); /* norm2 :166 */
+int f3rg_axpy(double alpha, const void* x, int prec_x, void* y, int prec_y, uint64_t n,
+              uintptr_t stream); /* axpy :114 */
+int f3rg_add_scaled(const void* x, int prec_x, double alpha, const void* y, int prec_y, void* out, int prec_out,
+                    uint64_t n, uintptr_t stream); /* add_scaled :131 */
+int f3rg_copy(const void* x, int prec_x, void* y, int prec_y, uint64_t n, uintptr_t stream); /* copy_into :87 */
+int f3rg_scale(double alpha, void* x, int prec_x, uint64_t n, uintptr_t stream);            /* scale_in_place :104 */
+int f3rg_fill(void* x, int prec_x, uint64_t n, double value, uintptr_t stream);             /* fill :77 */
+
+/* ---- Richardson with persistent state (richardson_apply + RichardsonState,
+ *      src/richardson.cpp:10-54, include/f3r/richardson.hpp:26-46), M = identity */
+typedef struct f3rg_richardson f3rg_richardson;
+int f3rg_richardson_create(f3rg_richardson** out, const f3rg_matrix* a, int prec, int m, uint64_t cycle);
+void f3rg_richardson_destroy(f3rg_richardson* r);
+int f3rg_richardson_set_omegas(f3rg_richardson* r, const double* omegas_host);
+/* omegas[m]; counters[3] = call_count, update_count, degenerate_events */
+int f3rg_richardson_state(f3rg_richardson* r, double* omegas_host, uint64_t* counters_host);
+/* v, z: device vectors at the Richardson precision */
+int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* F3RG_H */

@@ -1,0 +1,599 @@
+"""B200-native F3R hot path (arXiv 2505.20719): nested fp64 FGMRES > fp32 FGMRES >
+fp16-matrix FGMRES > fp16 Richardson with adaptive weight, as hand-written sm_100a
+CUDA behind a C ABI (include/f3rg.h, lib/libf3rg.so).
+
+This module is the Python mirror of the reference's C++ interface for the path
+(/root/reference/proj/include/f3r/*.hpp) -- same names, argument meaning and
+error classes -- so tests read like the reference's own:
+
+    reps = make_replicas(SparseCsr(n, row_ptr, col_idx, values))   # csr.hpp:72-81
+    solver = build_f3r(F3rConfig(), reps, IdentityPrecond(n))       # nesting.hpp:93-95
+    run = solver.run(b, RunOptions(tol=1e-10))                      # nesting.hpp:64
+    run.report.outer_iterations, run.x
+
+Device memory, streams and vectors are torch CUDA tensors (plumbing only); all
+arithmetic runs in libf3rg.so. There is no CPU fallback: importing without the
+built library, or calling without a GPU, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libf3rg.so")
+
+
+# ---------------------------------------------------------------- errors (errors.hpp)
+class F3rError(RuntimeError):
+    """f3r::Error"""
+
+
+class ParseError(F3rError):
+    """f3r::ParseError -- malformed solver spec"""
+
+
+class DimensionError(F3rError):
+    """f3r::DimensionError -- size mismatch / invalid CSR"""
+
+
+class FactorizationError(F3rError):
+    """f3r::FactorizationError"""
+
+
+class SolverError(F3rError):
+    """f3r::SolverError -- structural solver failures (m < 1, precision increase, ...)"""
+
+
+class UnsupportedError(SolverError):
+    """Valid reference input that this device build does not implement (e.g. ILU(0) M)."""
+
+
+class CudaError(F3rError):
+    """CUDA runtime failure (no reference counterpart)."""
+
+
+_ERRS = {2: DimensionError, 3: SolverError, 4: ParseError, 5: FactorizationError, 6: CudaError,
+         7: UnsupportedError, 9: F3rError}
+
+
+# ------------------------------------------------------------------ library loading
+class _Report(C.Structure):
+    _fields_ = [("converged", C.c_int32), ("outer_iterations", C.c_uint64), ("precond_invocations", C.c_uint64),
+                ("final_true_residual", C.c_double), ("wall_seconds", C.c_double), ("n_history", C.c_uint64),
+                ("n_levels", C.c_uint64), ("n_omegas", C.c_uint64), ("flag", C.c_char * 128)]
+
+
+class _Csr(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+
+
+class _RunOpts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_outer_restarts", C.c_int32), ("max_outer_total", C.c_uint64),
+                ("reset_richardson_on_restart", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libf3rg.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2505_20719_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, u64, i32, dbl = C.c_void_p, C.c_uint64, C.c_int, C.c_double
+    L.f3rg_last_error.restype = C.c_char_p
+    L.f3rg_version.restype = C.c_char_p
+    L.f3rg_matrix_create.argtypes = [C.POINTER(vp), C.POINTER(_Csr)]
+    L.f3rg_matrix_destroy.argtypes = [vp]
+    L.f3rg_matrix_rows.restype = u64
+    L.f3rg_matrix_rows.argtypes = [vp]
+    L.f3rg_matrix_nnz.restype = u64
+    L.f3rg_matrix_nnz.argtypes = [vp]
+    L.f3rg_matrix_values.argtypes = [vp, i32, vp]
+    L.f3rg_spec_canonical.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
+    L.f3rg_solver_create.argtypes = [C.POINTER(vp), vp, C.c_char_p, i32]
+    L.f3rg_solver_destroy.argtypes = [vp]
+    L.f3rg_solver_id.restype = C.c_char_p
+    L.f3rg_solver_id.argtypes = [vp]
+    L.f3rg_solve.argtypes = [vp, vp, vp, C.POINTER(_RunOpts), C.POINTER(_Report)]
+    L.f3rg_solve_device.argtypes = [vp, vp, vp, C.POINTER(_RunOpts), C.POINTER(_Report), C.c_size_t]
+    L.f3rg_solver_history.argtypes = [vp, vp, u64]
+    L.f3rg_solver_level_iterations.argtypes = [vp, vp, u64]
+    L.f3rg_solver_omegas.argtypes = [vp, vp, u64]
+    L.f3rg_solver_set_profile.argtypes = [vp, i32]
+    L.f3rg_solver_profile_entry.argtypes = [vp, u64, C.c_char_p, C.c_size_t, C.POINTER(dbl), C.POINTER(u64),
+                                            C.POINTER(dbl)]
+    L.f3rg_spmv.argtypes = [vp, i32, vp, i32, vp, i32, C.c_size_t]
+    L.f3rg_dot.argtypes = [vp, i32, vp, i32, u64, i32, C.POINTER(dbl), C.c_size_t]
+    L.f3rg_norm2.argtypes = [vp, i32, u64, C.POINTER(dbl), C.c_size_t]
+    L.f3rg_axpy.argtypes = [dbl, vp, i32, vp, i32, u64, C.c_size_t]
+    L.f3rg_add_scaled.argtypes = [vp, i32, dbl, vp, i32, vp, i32, u64, C.c_size_t]
+    L.f3rg_copy.argtypes = [vp, i32, vp, i32, u64, C.c_size_t]
+    L.f3rg_scale.argtypes = [dbl, vp, i32, u64, C.c_size_t]
+    L.f3rg_fill.argtypes = [vp, i32, u64, dbl, C.c_size_t]
+    L.f3rg_richardson_create.argtypes = [C.POINTER(vp), vp, i32, i32, u64]
+    L.f3rg_richardson_destroy.argtypes = [vp]
+    L.f3rg_richardson_set_omegas.argtypes = [vp, vp]
+    L.f3rg_richardson_state.argtypes = [vp, vp, vp]
+    L.f3rg_richardson_apply.argtypes = [vp, vp, vp, C.c_size_t]
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().f3rg_last_error().decode()
+        raise _ERRS.get(rc, F3rError)(msg)
+
+
+# ------------------------------------------------------------ precision (precision.hpp)
+class Precision(enum.IntEnum):
+    P16 = 0
+    P32 = 1
+    P64 = 2
+
+
+def compute_precision(a: Precision, b: Precision) -> Precision:
+    return Precision(max(int(a), int(b)))
+
+
+def precision_name(p) -> str:
+    return ("f16", "f32", "f64")[int(p)]
+
+
+def _torch():
+    import torch  # plumbing: device memory and streams
+    return torch
+
+
+def _prec_of(t) -> Precision:
+    torch = _torch()
+    m = {torch.float16: Precision.P16, torch.float32: Precision.P32, torch.float64: Precision.P64}
+    if t.dtype not in m:
+        raise DimensionError(f"unsupported dtype {t.dtype}")
+    if not t.is_cuda:
+        raise DimensionError("device vectors must be CUDA tensors")
+    return m[t.dtype]
+
+
+def torch_dtype(p):
+    torch = _torch()
+    return (torch.float16, torch.float32, torch.float64)[int(p)]
+
+
+def _stream():
+    torch = _torch()
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ vectors (dense_vector.hpp)
+class DenseVector:
+    """Device vector with a runtime precision (reference DenseVector,
+    include/f3r/dense_vector.hpp:25-57), backed by a torch CUDA tensor."""
+
+    def __init__(self, n_or_tensor, precision: Precision = Precision.P64):
+        torch = _torch()
+        if isinstance(n_or_tensor, int):
+            self.t = torch.zeros(n_or_tensor, dtype=torch_dtype(precision), device="cuda")
+        elif isinstance(n_or_tensor, np.ndarray):
+            self.t = torch.from_numpy(np.ascontiguousarray(n_or_tensor)).to(
+                device="cuda", dtype=torch_dtype(precision))
+        else:
+            self.t = n_or_tensor.contiguous()
+            _prec_of(self.t)
+
+    def precision(self) -> Precision:
+        return _prec_of(self.t)
+
+    def size(self) -> int:
+        return self.t.numel()
+
+    def __len__(self):
+        return self.t.numel()
+
+    def numpy(self) -> np.ndarray:
+        """exact widening to fp64"""
+        return self.t.double().cpu().numpy()
+
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+
+def _vec(x) -> DenseVector:
+    return x if isinstance(x, DenseVector) else DenseVector(x)
+
+
+def fill(x: DenseVector, value: float) -> None:
+    _check(lib().f3rg_fill(x.ptr(), x.precision(), x.size(), value, _stream()))
+
+
+def copy_into(x: DenseVector, y: DenseVector) -> None:
+    if x.size() != y.size():
+        raise DimensionError(f"copy: length mismatch ({x.size()} vs {y.size()})")
+    _check(lib().f3rg_copy(x.ptr(), x.precision(), y.ptr(), y.precision(), x.size(), _stream()))
+
+
+def converted(x: DenseVector, p: Precision) -> DenseVector:
+    out = DenseVector(x.size(), p)
+    copy_into(x, out)
+    return out
+
+
+def scale_in_place(alpha: float, x: DenseVector) -> None:
+    _check(lib().f3rg_scale(alpha, x.ptr(), x.precision(), x.size(), _stream()))
+
+
+def axpy(alpha: float, x: DenseVector, y: DenseVector) -> None:
+    if x.size() != y.size():
+        raise DimensionError(f"axpy: length mismatch ({x.size()} vs {y.size()})")
+    _check(lib().f3rg_axpy(alpha, x.ptr(), x.precision(), y.ptr(), y.precision(), x.size(), _stream()))
+
+
+def add_scaled(x: DenseVector, alpha: float, y: DenseVector, out: DenseVector) -> None:
+    if x.size() != y.size() or x.size() != out.size():
+        raise DimensionError("add_scaled: length mismatch")
+    _check(lib().f3rg_add_scaled(x.ptr(), x.precision(), alpha, y.ptr(), y.precision(), out.ptr(),
+                                 out.precision(), x.size(), _stream()))
+
+
+def dot_at_least(x: DenseVector, y: DenseVector, floor_precision: Precision) -> float:
+    if x.size() != y.size():
+        raise DimensionError(f"dot: length mismatch ({x.size()} vs {y.size()})")
+    out = C.c_double()
+    _check(lib().f3rg_dot(x.ptr(), x.precision(), y.ptr(), y.precision(), x.size(), int(floor_precision),
+                          C.byref(out), _stream()))
+    return out.value
+
+
+def dot(x: DenseVector, y: DenseVector) -> float:
+    return dot_at_least(x, y, Precision.P16)
+
+
+def norm2(x: DenseVector) -> float:
+    out = C.c_double()
+    _check(lib().f3rg_norm2(x.ptr(), x.precision(), x.size(), C.byref(out), _stream()))
+    return out.value
+
+
+# --------------------------------------------------------------------- matrices (csr.hpp)
+class SparseCsr:
+    """Host fp64 CSR with u32 indices (reference SparseCsr, include/f3r/csr.hpp:23-67).
+    Validation happens when the device replicas are built (make_replicas)."""
+
+    def __init__(self, n: int, row_ptr, col_idx, values):
+        self.n = int(n)
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint32)
+        self.col_idx = np.ascontiguousarray(col_idx, dtype=np.uint32)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        if self.row_ptr.size != self.n + 1:
+            raise DimensionError("row_ptr length must be n+1")
+        if self.values.size != self.col_idx.size:
+            raise DimensionError("values length must equal nnz")
+
+    def rows(self) -> int:
+        return self.n
+
+    def nnz(self) -> int:
+        return int(self.col_idx.size)
+
+
+class _DeviceMatrix:
+    def __init__(self, a: SparseCsr):
+        L = lib()
+        self.h = C.c_void_p()
+        csr = _Csr(a.n, a.row_ptr.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data)
+        _check(L.f3rg_matrix_create(C.byref(self.h), C.byref(csr)))
+        self.n = a.n
+        self.nnz_ = a.nnz()
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.f3rg_matrix_destroy(self.h)
+            self.h = None
+
+
+class ReplicaView:
+    """One precision of PrecisionReplicas (what PrecisionReplicas::at returns)."""
+
+    def __init__(self, dev: _DeviceMatrix, p: Precision):
+        self.dev, self.p = dev, Precision(p)
+
+    def precision(self) -> Precision:
+        return self.p
+
+    def rows(self) -> int:
+        return self.dev.n
+
+    def nnz(self) -> int:
+        return self.dev.nnz_
+
+    def values(self) -> np.ndarray:
+        """replica values widened to fp64 (exact)"""
+        out = np.zeros(self.dev.nnz_)
+        _check(lib().f3rg_matrix_values(self.dev.h, self.p, out.ctypes.data))
+        return out
+
+
+class PrecisionReplicas:
+    """reference PrecisionReplicas (include/f3r/csr.hpp:72-78): one device copy of the
+    indices, fp64 / fp32 / fp16 value arrays (RNE demotions of a64)."""
+
+    def __init__(self, a64: SparseCsr):
+        self.host = a64
+        self.dev = _DeviceMatrix(a64)
+        self.a64 = ReplicaView(self.dev, Precision.P64)
+        self.a32 = ReplicaView(self.dev, Precision.P32)
+        self.a16 = ReplicaView(self.dev, Precision.P16)
+
+    def at(self, p: Precision) -> ReplicaView:
+        return (self.a16, self.a32, self.a64)[int(p)]
+
+    def rows(self) -> int:
+        return self.dev.n
+
+
+def make_replicas(a64: SparseCsr) -> PrecisionReplicas:
+    return PrecisionReplicas(a64)
+
+
+def spmv(a: ReplicaView, x: DenseVector, y: DenseVector) -> None:
+    """y = A x at compute_precision(A, x), stored at y's precision (src/csr.cpp:138-147)."""
+    if x.size() != a.rows() or y.size() != a.rows():
+        raise DimensionError("spmv: dimension mismatch")
+    _check(lib().f3rg_spmv(a.dev.h, a.p, x.ptr(), x.precision(), y.ptr(), y.precision(), _stream()))
+
+
+# ------------------------------------------------------------ preconditioner (ilu.hpp)
+class IdentityPrecond:
+    """reference IdentityPrecond (include/f3r/ilu.hpp:34-42); the only primary
+    preconditioner of this build (ILU(0)/IC(0) is SURVEY.md §8(f)-1)."""
+    kind = 2
+
+    def __init__(self, n: int):
+        self.n = int(n)
+
+    def rows(self) -> int:
+        return self.n
+
+
+# ---------------------------------------------------------------- spec (solver_spec.hpp)
+def canonical_spec(text: str) -> str:
+    """parse_solver_spec(text).to_string() (src/solver_spec.cpp:147-212); raises ParseError."""
+    buf = C.create_string_buffer(1024)
+    _check(lib().f3rg_spec_canonical(text.encode(), buf, 1024))
+    return buf.value.decode()
+
+
+@dataclass
+class SolverSpec:
+    """A spec kept in the reference grammar; parse_solver_spec validates it."""
+    text: str
+
+    def to_string(self) -> str:
+        return canonical_spec(self.text)
+
+
+def parse_solver_spec(text: str) -> SolverSpec:
+    canonical_spec(text)
+    return SolverSpec(text)
+
+
+class F3rMode(enum.Enum):
+    FP64 = 0
+    FP32 = 1
+    FP16 = 2
+
+
+@dataclass
+class F3rConfig:
+    """reference F3rConfig (include/f3r/nesting.hpp:84-91)"""
+    m1: int = 100
+    m2: int = 8
+    m3: int = 4
+    m4: int = 2
+    c: int = 64
+    mode: F3rMode = F3rMode.FP16
+
+
+def f3r_spec(cfg: F3rConfig) -> SolverSpec:
+    """reference f3r_spec (src/nesting.cpp:359-386), terminal = the primary
+    preconditioner at the Richardson precision."""
+    if cfg.mode == F3rMode.FP16:
+        mid, low_m, low_v, rich = "f32", "f16", "f32", "f16"
+    elif cfg.mode == F3rMode.FP32:
+        mid, low_m, low_v, rich = "f32", "f32", "f32", "f32"
+    else:
+        mid, low_m, low_v, rich = "f64", "f64", "f64", "f64"
+    return SolverSpec(f"F{cfg.m1}:f64/f64 > F{cfg.m2}:{mid}/{mid} > F{cfg.m3}:{low_m}/{low_v} > "
+                      f"R{cfg.m4}:{rich},c={cfg.c} > ilu0(prec={rich})")
+
+
+# --------------------------------------------------------------------- solver (nesting.hpp)
+@dataclass
+class RunOptions:
+    """reference RunOptions (include/f3r/nesting.hpp:29-38)"""
+    tol: float = 1e-8
+    max_outer_restarts: int = 3
+    max_outer_total: int = 300
+    reset_richardson_on_restart: bool = False
+
+    def _c(self):
+        return _RunOpts(self.tol, self.max_outer_restarts, self.max_outer_total,
+                        int(self.reset_richardson_on_restart))
+
+
+@dataclass
+class ConvergenceReport:
+    """reference ConvergenceReport (include/f3r/report.hpp:18-30)"""
+    converged: bool = False
+    outer_iterations: int = 0
+    precond_invocations: int = 0
+    level_iterations: list = field(default_factory=list)
+    residual_history: list = field(default_factory=list)
+    final_true_residual: float = 0.0
+    wall_seconds: float = 0.0
+    omegas_final: list = field(default_factory=list)
+    flag: str = ""
+    solver_id: str = ""
+    problem_id: str = ""
+
+
+@dataclass
+class RunResult:
+    x: Optional[np.ndarray]
+    report: ConvergenceReport
+
+
+class ComposedSolver:
+    """reference ComposedSolver (include/f3r/nesting.hpp:55-77): the whole nest runs
+    on the GPU; one C-ABI call per solve."""
+
+    def __init__(self, spec, a: PrecisionReplicas, m: IdentityPrecond):
+        if m.rows() != a.rows():
+            raise DimensionError("preconditioner size does not match the matrix")
+        text = spec.text if isinstance(spec, SolverSpec) else str(spec)
+        self.h = C.c_void_p()
+        self._a = a
+        _check(lib().f3rg_solver_create(C.byref(self.h), a.dev.h, text.encode(), int(m.kind)))
+        self.n = a.rows()
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.f3rg_solver_destroy(self.h)
+            self.h = None
+
+    def id(self) -> str:
+        return lib().f3rg_solver_id(self.h).decode()
+
+    def _report(self, r: _Report) -> ConvergenceReport:
+        L = lib()
+        hist = np.zeros(max(1, r.n_history))
+        L.f3rg_solver_history(self.h, hist.ctypes.data, r.n_history)
+        lv = np.zeros(max(1, r.n_levels), dtype=np.uint64)
+        L.f3rg_solver_level_iterations(self.h, lv.ctypes.data, r.n_levels)
+        om = np.zeros(max(1, r.n_omegas))
+        if r.n_omegas:
+            _check(L.f3rg_solver_omegas(self.h, om.ctypes.data, r.n_omegas))
+        return ConvergenceReport(bool(r.converged), int(r.outer_iterations), int(r.precond_invocations),
+                                 [int(v) for v in lv[:r.n_levels]], list(hist[:r.n_history]),
+                                 r.final_true_residual, r.wall_seconds, list(om[:r.n_omegas]), r.flag.decode(),
+                                 self.id())
+
+    def run(self, b, opts: RunOptions = RunOptions(), want_x: bool = True) -> RunResult:
+        """b: host numpy fp64 array (host copies inside the call) or a CUDA fp64
+        tensor (device-resident; x is returned as a CUDA tensor)."""
+        r = _Report()
+        if isinstance(b, np.ndarray):
+            b = np.ascontiguousarray(b, dtype=np.float64)
+            if b.size != self.n:
+                raise DimensionError("run: rhs length mismatch")
+            x = np.zeros(self.n) if want_x else None
+            _check(lib().f3rg_solve(self.h, b.ctypes.data, x.ctypes.data if x is not None else None,
+                                    C.byref(opts._c()), C.byref(r)))
+            return RunResult(x, self._report(r))
+        t = b.t if isinstance(b, DenseVector) else b
+        if _prec_of(t) != Precision.P64 or t.numel() != self.n:
+            raise DimensionError("run: rhs must be an fp64 vector of length n")
+        torch = _torch()
+        x = torch.empty(self.n, dtype=torch.float64, device=t.device) if want_x else None
+        _check(lib().f3rg_solve_device(self.h, t.data_ptr(), x.data_ptr() if x is not None else None,
+                                       C.byref(opts._c()), C.byref(r), _stream()))
+        return RunResult(x, self._report(r))
+
+    def innermost_omegas(self) -> list:
+        om = np.zeros(64)
+        _check(lib().f3rg_solver_omegas(self.h, om.ctypes.data, 64))
+        return list(om)
+
+    def set_profile(self, on: bool = True) -> None:
+        lib().f3rg_solver_set_profile(self.h, int(on))
+
+    def profile(self) -> list:
+        """[(kernel, total_ms, launches, algorithmic_bytes)] of the last profiled run"""
+        out, i = [], 0
+        name = C.create_string_buffer(256)
+        ms, ln, by = C.c_double(), C.c_uint64(), C.c_double()
+        while lib().f3rg_solver_profile_entry(self.h, i, name, 256, C.byref(ms), C.byref(ln), C.byref(by)) == 0:
+            out.append((name.value.decode(), ms.value, ln.value, by.value))
+            i += 1
+        return out
+
+
+def build(spec, a: PrecisionReplicas, m: IdentityPrecond) -> ComposedSolver:
+    return ComposedSolver(spec, a, m)
+
+
+def build_f3r(cfg: F3rConfig, a: PrecisionReplicas, m: IdentityPrecond) -> ComposedSolver:
+    return ComposedSolver(f3r_spec(cfg), a, m)
+
+
+# ------------------------------------------------------------- Richardson (richardson.hpp)
+class RichardsonState:
+    """Persistent Richardson state on the device (reference RichardsonState,
+    include/f3r/richardson.hpp:26-46) bound to one replica; M = identity."""
+
+    def __init__(self, a: ReplicaView, m: int, cycle: int):
+        self.h = C.c_void_p()
+        _check(lib().f3rg_richardson_create(C.byref(self.h), a.dev.h, int(a.p), int(m), int(cycle)))
+        self.a, self.m_inner, self.cycle = a, int(m), int(cycle)
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.f3rg_richardson_destroy(self.h)
+            self.h = None
+
+    @property
+    def omegas(self) -> list:
+        return self._state()[0]
+
+    @omegas.setter
+    def omegas(self, w: Sequence[float]):
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        _check(lib().f3rg_richardson_set_omegas(self.h, w.ctypes.data))
+
+    def _state(self):
+        om = np.zeros(self.m_inner)
+        cnt = np.zeros(3, dtype=np.uint64)
+        _check(lib().f3rg_richardson_state(self.h, om.ctypes.data, cnt.ctypes.data))
+        return list(om), [int(c) for c in cnt]
+
+    @property
+    def call_count(self) -> int:
+        return self._state()[1][0]
+
+    @property
+    def update_count(self) -> int:
+        return self._state()[1][1]
+
+    @property
+    def degenerate_events(self) -> int:
+        return self._state()[1][2]
+
+
+def richardson_apply(state: RichardsonState, v: DenseVector, z: DenseVector) -> None:
+    """reference richardson_apply (src/richardson.cpp:10-54) with M = identity."""
+    if v.precision() != state.a.p or z.precision() != state.a.p:
+        raise DimensionError("richardson: vectors must be at the state's precision")
+    if v.size() != state.a.rows() or z.size() != state.a.rows():
+        raise DimensionError("richardson: dimension mismatch")
+    _check(lib().f3rg_richardson_apply(state.h, v.ptr(), z.ptr(), _stream()))
+
+
+__all__ = [
+    "F3rError", "ParseError", "DimensionError", "FactorizationError", "SolverError", "UnsupportedError",
+    "CudaError", "Precision", "compute_precision", "precision_name", "DenseVector", "fill", "copy_into",
+    "converted", "scale_in_place", "axpy", "add_scaled", "dot", "dot_at_least", "norm2", "SparseCsr",
+    "PrecisionReplicas", "make_replicas", "spmv", "IdentityPrecond", "SolverSpec", "parse_solver_spec",
+    "canonical_spec", "F3rMode", "F3rConfig", "f3r_spec", "RunOptions", "ConvergenceReport", "RunResult",
+    "ComposedSolver", "build", "build_f3r", "RichardsonState", "richardson_apply", "lib",
+]

@@ -1,0 +1,357 @@
+// capi.cpp -- the C ABI of include/f3rg.h over the engine (engine.hpp).
+// Exceptions never cross the boundary: each entry point maps f3rg::Error codes
+// (1:1 with the reference's exception classes) to its return value and records
+// the message for f3rg_last_error().
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/f3rg.h"
+#include "engine.hpp"
+#include "launch.hpp"
+
+using namespace f3rg;
+
+struct f3rg_matrix {
+  std::shared_ptr<DeviceMatrix> m;
+};
+
+struct f3rg_solver {
+  std::unique_ptr<Solver> s;
+  Report last;
+};
+
+struct f3rg_richardson {
+  std::shared_ptr<DeviceMatrix> a;
+  int prec = 0, m = 1;
+  DevBuf state, omegas, wused, wupd, calls, R, Za, Zb, dead, cnt, partials, counter, bar;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return F3RG_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return F3RG_EINTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return F3RG_EINTERNAL;
+  }
+}
+
+void check_prec(int p) {
+  if (p < 0 || p > 2) throw Error(ERR_DIMENSION, "precision tag must be 0 (f16), 1 (f32) or 2 (f64)");
+}
+
+cudaStream_t as_stream(uintptr_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void fill_report(const Report& r, f3rg_report* out) {
+  if (!out) return;
+  std::memset(out, 0, sizeof *out);
+  out->converged = r.converged;
+  out->outer_iterations = r.outer_iterations;
+  out->precond_invocations = r.precond_invocations;
+  out->final_true_residual = r.final_true_residual;
+  out->wall_seconds = r.wall_seconds;
+  out->n_history = r.residual_history.size();
+  out->n_levels = r.level_iterations.size();
+  out->n_omegas = r.omegas_final.size();
+  std::strncpy(out->flag, r.flag.c_str(), sizeof out->flag - 1);
+}
+
+RunOptions to_opts(const f3rg_run_options* o) {
+  RunOptions r;
+  if (o) {
+    r.tol = o->tol;
+    r.max_outer_restarts = o->max_outer_restarts;
+    r.max_outer_total = o->max_outer_total;
+    r.reset_richardson_on_restart = o->reset_richardson_on_restart != 0;
+  }
+  return r;
+}
+
+// scratch for scalar results of kernel-level reductions
+struct Scratch {
+  DevBuf partials, counter, out;
+  Scratch() {
+    partials.alloc((size_t)max_partial_blocks() * 16 * sizeof(double));
+    counter.alloc(64);
+    out.alloc(64);
+    F3RG_CUDA(cudaMemset(counter.get(), 0, 64));
+  }
+};
+Scratch& scratch() {
+  thread_local Scratch s;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* f3rg_last_error(void) { return g_err.c_str(); }
+const char* f3rg_version(void) { return "f3rg 0.1 (sm_100a)"; }
+
+void f3rg_default_run_options(f3rg_run_options* o) {
+  o->tol = 1e-8;
+  o->max_outer_restarts = 3;
+  o->max_outer_total = 300;
+  o->reset_richardson_on_restart = 0;
+}
+
+int f3rg_matrix_create(f3rg_matrix** out, const f3rg_csr* a) {
+  return guarded([&] {
+    if (!out || !a) throw Error(ERR_DIMENSION, "null argument");
+    auto h = std::make_unique<f3rg_matrix>();
+    h->m = std::make_shared<DeviceMatrix>(a->n, a->row_ptr, a->col_idx, a->values);
+    *out = h.release();
+  });
+}
+
+void f3rg_matrix_destroy(f3rg_matrix* a) { delete a; }
+uint64_t f3rg_matrix_rows(const f3rg_matrix* a) { return a ? a->m->rows() : 0; }
+uint64_t f3rg_matrix_nnz(const f3rg_matrix* a) { return a ? a->m->nnz() : 0; }
+
+int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host) {
+  return guarded([&] {
+    check_prec(prec);
+    const uint64_t nnz = a->m->nnz();
+    DevBuf tmp(nnz * 8 + 16);
+    F3RG_CUDA(launch_copy(prec, 2, Launch{}, a->m->values(prec), tmp.get(), nnz));
+    F3RG_CUDA(cudaMemcpy(out_host, tmp.get(), nnz * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int f3rg_spec_canonical(const char* spec, char* out, size_t cap) {
+  return guarded([&] {
+    const std::string s = parse_spec(spec ? spec : "").to_string();
+    if (cap) {
+      std::strncpy(out, s.c_str(), cap - 1);
+      out[cap - 1] = 0;
+    }
+  });
+}
+
+int f3rg_solver_create(f3rg_solver** out, const f3rg_matrix* a, const char* spec, int precond_kind) {
+  return guarded([&] {
+    if (!out || !a || !spec) throw Error(ERR_DIMENSION, "null argument");
+    auto h = std::make_unique<f3rg_solver>();
+    h->s = std::make_unique<Solver>(parse_spec(spec), a->m, precond_kind);
+    *out = h.release();
+  });
+}
+
+void f3rg_solver_destroy(f3rg_solver* s) { delete s; }
+const char* f3rg_solver_id(const f3rg_solver* s) { return s ? s->s->id().c_str() : ""; }
+
+int f3rg_solve_device(f3rg_solver* s, const double* b, double* x, const f3rg_run_options* o, f3rg_report* rep,
+                      uintptr_t stream) {
+  return guarded([&] {
+    s->last = s->s->run(b, x, to_opts(o), as_stream(stream));
+    fill_report(s->last, rep);
+  });
+}
+
+int f3rg_solve(f3rg_solver* s, const double* b_host, double* x_host, const f3rg_run_options* o, f3rg_report* rep) {
+  return guarded([&] {
+    const uint64_t n = s->s->rows();
+    DevBuf b(n * 8 + 16), x(n * 8 + 16);
+    F3RG_CUDA(cudaMemcpy(b.get(), b_host, n * 8, cudaMemcpyHostToDevice));
+    s->last = s->s->run(b.get<double>(), x_host ? x.get<double>() : nullptr, to_opts(o), nullptr);
+    if (x_host) F3RG_CUDA(cudaMemcpy(x_host, x.get(), n * 8, cudaMemcpyDeviceToHost));
+    fill_report(s->last, rep);
+  });
+}
+
+int f3rg_solver_history(const f3rg_solver* s, double* out, uint64_t cap) {
+  const auto& h = s->last.residual_history;
+  for (uint64_t i = 0; i < h.size() && i < cap; ++i) out[i] = h[i];
+  return F3RG_OK;
+}
+
+int f3rg_solver_level_iterations(const f3rg_solver* s, uint64_t* out, uint64_t cap) {
+  const auto& h = s->last.level_iterations;
+  for (uint64_t i = 0; i < h.size() && i < cap; ++i) out[i] = h[i];
+  return F3RG_OK;
+}
+
+int f3rg_solver_omegas(f3rg_solver* s, double* out, uint64_t cap) {
+  return guarded([&] {
+    const auto w = s->s->innermost_omegas();
+    for (uint64_t i = 0; i < w.size() && i < cap; ++i) out[i] = w[i];
+  });
+}
+
+int f3rg_solver_set_profile(f3rg_solver* s, int on) {
+  s->s->set_profile(on != 0);
+  return F3RG_OK;
+}
+
+int f3rg_solver_profile_entry(const f3rg_solver* s, uint64_t i, char* name, size_t cap, double* ms,
+                              uint64_t* launches, double* bytes) {
+  return guarded([&] {
+    const auto r = s->s->profile_results();
+    if (i >= r.size()) throw Error(ERR_DIMENSION, "profile entry out of range");
+    if (cap) {
+      std::strncpy(name, r[i].name.c_str(), cap - 1);
+      name[cap - 1] = 0;
+    }
+    *ms = r[i].ms;
+    *launches = r[i].launches;
+    *bytes = r[i].bytes;
+  });
+}
+
+// ---- kernel-level -----------------------------------------------------------------
+int f3rg_spmv(const f3rg_matrix* a, int pa, const void* x, int px, void* y, int py, uintptr_t stream) {
+  return guarded([&] {
+    check_prec(pa), check_prec(px), check_prec(py);
+    F3RG_CUDA(launch_spmv(pa, px, py, Launch{0, as_stream(stream)}, a->m->csr(), a->m->tiles(pa), x, y));
+  });
+}
+
+int f3rg_dot(const void* x, int px, const void* y, int py, uint64_t n, int floor_p, double* out, uintptr_t stream) {
+  return guarded([&] {
+    check_prec(px), check_prec(py), check_prec(floor_p);
+    auto& sc = scratch();
+    cudaStream_t s = as_stream(stream);
+    F3RG_CUDA(launch_dot(px, py, floor_p, Launch{0, s}, x, y, n, sc.out.get<double>(),
+                         SyncH{sc.partials.get<double>(), sc.counter.get<unsigned>()}));
+    F3RG_CUDA(cudaMemcpyAsync(out, sc.out.get(), 8, cudaMemcpyDeviceToHost, s));
+    F3RG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int f3rg_norm2(const void* x, int px, uint64_t n, double* out, uintptr_t stream) {
+  return guarded([&] {
+    check_prec(px);
+    auto& sc = scratch();
+    cudaStream_t s = as_stream(stream);
+    F3RG_CUDA(launch_norm2(px, Launch{0, s}, x, n, sc.out.get<double>(),
+                           SyncH{sc.partials.get<double>(), sc.counter.get<unsigned>()}));
+    F3RG_CUDA(cudaMemcpyAsync(out, sc.out.get(), 8, cudaMemcpyDeviceToHost, s));
+    F3RG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int f3rg_axpy(double alpha, const void* x, int px, void* y, int py, uint64_t n, uintptr_t stream) {
+  return guarded([&] {
+    check_prec(px), check_prec(py);
+    F3RG_CUDA(launch_axpy(px, py, Launch{0, as_stream(stream)}, alpha, x, y, n));
+  });
+}
+
+int f3rg_add_scaled(const void* x, int px, double alpha, const void* y, int py, void* out, int po, uint64_t n,
+                    uintptr_t stream) {
+  return guarded([&] {
+    check_prec(px), check_prec(py), check_prec(po);
+    F3RG_CUDA(launch_add_scaled(px, py, po, Launch{0, as_stream(stream)}, x, alpha, y, out, n));
+  });
+}
+
+int f3rg_copy(const void* x, int px, void* y, int py, uint64_t n, uintptr_t stream) {
+  return guarded([&] {
+    check_prec(px), check_prec(py);
+    F3RG_CUDA(launch_copy(px, py, Launch{0, as_stream(stream)}, x, y, n));
+  });
+}
+
+int f3rg_scale(double alpha, void* x, int px, uint64_t n, uintptr_t stream) {
+  return guarded([&] {
+    check_prec(px);
+    F3RG_CUDA(launch_scale(px, Launch{0, as_stream(stream)}, alpha, x, n));
+  });
+}
+
+int f3rg_fill(void* x, int px, uint64_t n, double value, uintptr_t stream) {
+  return guarded([&] {
+    check_prec(px);
+    F3RG_CUDA(launch_fill(px, Launch{0, as_stream(stream)}, x, n, value));
+  });
+}
+
+// ---- Richardson ---------------------------------------------------------------------
+int f3rg_richardson_create(f3rg_richardson** out, const f3rg_matrix* a, int prec, int m, uint64_t cycle) {
+  return guarded([&] {
+    check_prec(prec);
+    if (m < 1) throw Error(ERR_SOLVER, "richardson: m must be >= 1");
+    auto r = std::make_unique<f3rg_richardson>();
+    r->a = a->m;
+    r->prec = prec;
+    r->m = m;
+    const uint64_t n = a->m->rows();
+    const size_t vb = n * (prec == 0 ? 2 : prec == 1 ? 4 : 8) + 16;
+    r->omegas.alloc((size_t)m * 8);
+    r->wused.alloc((size_t)m * 8);
+    r->wupd.alloc((size_t)m * 4);
+    r->calls.alloc(32);
+    r->R.alloc(vb);
+    r->Za.alloc(vb);
+    r->Zb.alloc(vb);
+    r->dead.alloc(64);
+    r->cnt.alloc(CNT_N * 8);
+    r->partials.alloc((size_t)max_partial_blocks() * 16 * 8);
+    r->counter.alloc(64);
+    r->bar.alloc(64);
+    for (DevBuf* b : {&r->dead, &r->cnt, &r->counter, &r->bar}) F3RG_CUDA(cudaMemset(b->get(), 0, b->bytes()));
+    RichState h;
+    h.m = m;
+    h.cycle = cycle;
+    h.omegas = r->omegas.get<double>();
+    h.wused = r->wused.get<double>();
+    h.wupd = r->wupd.get<int>();
+    h.calls = r->calls.get<unsigned long long>();
+    h.R = r->R.get();
+    h.Za = r->Za.get();
+    h.Zb = r->Zb.get();
+    r->state.alloc(sizeof h);
+    F3RG_CUDA(cudaMemcpy(r->state.get(), &h, sizeof h, cudaMemcpyHostToDevice));
+    std::vector<double> w((size_t)m, 1.0);
+    F3RG_CUDA(cudaMemcpy(r->omegas.get(), w.data(), w.size() * 8, cudaMemcpyHostToDevice));
+    const unsigned long long c[4] = {1ull, 0ull, 0ull, 0ull};
+    F3RG_CUDA(cudaMemcpy(r->calls.get(), c, sizeof c, cudaMemcpyHostToDevice));
+    *out = r.release();
+  });
+}
+
+void f3rg_richardson_destroy(f3rg_richardson* r) { delete r; }
+
+int f3rg_richardson_set_omegas(f3rg_richardson* r, const double* w) {
+  return guarded([&] {
+    F3RG_CUDA(cudaDeviceSynchronize());
+    F3RG_CUDA(cudaMemcpy(r->omegas.get(), w, (size_t)r->m * 8, cudaMemcpyHostToDevice));
+  });
+}
+
+int f3rg_richardson_state(f3rg_richardson* r, double* omegas, uint64_t* counters) {
+  return guarded([&] {
+    F3RG_CUDA(cudaDeviceSynchronize());
+    if (omegas) F3RG_CUDA(cudaMemcpy(omegas, r->omegas.get(), (size_t)r->m * 8, cudaMemcpyDeviceToHost));
+    unsigned long long c[4];
+    F3RG_CUDA(cudaMemcpy(c, r->calls.get(), sizeof c, cudaMemcpyDeviceToHost));
+    if (counters) counters[0] = c[0], counters[1] = c[1], counters[2] = c[2];
+  });
+}
+
+int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t stream) {
+  return guarded([&] {
+    const int p = r->prec;
+    F3RG_CUDA(launch_richardson(p, p, p, Launch{0, as_stream(stream)}, r->a->csr(), r->a->tiles(p), v, nullptr, z,
+                                r->a->rows(), r->state.get<RichState>(), GateH{r->dead.get<int>(), 0}, 0,
+                                r->cnt.get<unsigned long long>(),
+                                SyncH{r->partials.get<double>(), r->counter.get<unsigned>()}, r->bar.get<unsigned>(),
+                                r->bar.get<unsigned>() + 1, nullptr));
+  });
+}
+
+}  // extern "C"

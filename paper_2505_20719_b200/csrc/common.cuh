@@ -1,0 +1,249 @@
+// common.cuh -- precision traits, bit-faithful arithmetic, sm_100a async-copy
+// primitives and deterministic reductions shared by every f3rg kernel.
+//
+// Numeric contract (reference include/f3r/precision.hpp,
+// include/f3r/half.hpp, src/vector_ops.cpp): an operation "at precision C"
+// widens its operands exactly, performs ONE correctly rounded IEEE op at C and
+// never contracts a*b+c into an FMA. We use the explicit _rn intrinsics
+// (__dmul_rn/__dadd_rn, __fmul_rn/__fadd_rn, __hmul_rn/__hadd_rn), which nvcc
+// never fuses, and additionally build with -fmad=false. binary16 division and
+// square root go through binary32 and round once more -- exactly what the
+// reference's software Half does (half.hpp:121-124,146), and equal to the
+// correctly rounded binary16 result.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace f3rg {
+
+enum : int { P16 = 0, P32 = 1, P64 = 2 };
+
+template <int P> struct Prec;
+template <> struct Prec<P16> { using T = __half; };
+template <> struct Prec<P32> { using T = float; };
+template <> struct Prec<P64> { using T = double; };
+template <int P> using T_ = typename Prec<P>::T;
+
+__host__ __device__ constexpr int pmax(int a, int b) { return a > b ? a : b; }
+
+// ---- conversions (RNE, subnormals kept) -------------------------------------
+template <int To> struct Cvt;
+template <> struct Cvt<P64> {
+  __device__ static double of(double x) { return x; }
+  __device__ static double of(float x) { return (double)x; }
+  __device__ static double of(__half x) { return (double)__half2float(x); }
+};
+template <> struct Cvt<P32> {
+  __device__ static float of(double x) { return __double2float_rn(x); }
+  __device__ static float of(float x) { return x; }
+  __device__ static float of(__half x) { return __half2float(x); }
+};
+template <> struct Cvt<P16> {
+  __device__ static __half of(double x) { return __double2half(x); }  // one rounding from binary64
+  __device__ static __half of(float x) { return __float2half_rn(x); }
+  __device__ static __half of(__half x) { return x; }
+};
+template <int To, class S>
+__device__ __forceinline__ T_<To> cvt(S x) { return Cvt<To>::of(x); }
+
+// ---- one rounded op at precision C --------------------------------------------
+template <int C> struct Ar;
+template <> struct Ar<P64> {
+  using T = double;
+  __device__ static T zero() { return 0.0; }
+  __device__ static T one() { return 1.0; }
+  __device__ static T mul(T a, T b) { return __dmul_rn(a, b); }
+  __device__ static T add(T a, T b) { return __dadd_rn(a, b); }
+  __device__ static T sub(T a, T b) { return __dsub_rn(a, b); }
+  __device__ static T div(T a, T b) { return __ddiv_rn(a, b); }
+  __device__ static T sqrt(T a) { return __dsqrt_rn(a); }
+  __device__ static T hypot(T a, T b) { return ::hypot(a, b); }
+  __device__ static T neg(T a) { return -a; }
+  __device__ static double wide(T a) { return a; }
+  __device__ static bool finite(T a) { return isfinite(a); }
+};
+template <> struct Ar<P32> {
+  using T = float;
+  __device__ static T zero() { return 0.0f; }
+  __device__ static T one() { return 1.0f; }
+  __device__ static T mul(T a, T b) { return __fmul_rn(a, b); }
+  __device__ static T add(T a, T b) { return __fadd_rn(a, b); }
+  __device__ static T sub(T a, T b) { return __fsub_rn(a, b); }
+  __device__ static T div(T a, T b) { return __fdiv_rn(a, b); }
+  __device__ static T sqrt(T a) { return __fsqrt_rn(a); }
+  __device__ static T hypot(T a, T b) { return ::hypotf(a, b); }
+  __device__ static T neg(T a) { return -a; }
+  __device__ static double wide(T a) { return (double)a; }
+  __device__ static bool finite(T a) { return isfinite(a); }
+};
+template <> struct Ar<P16> {
+  using T = __half;
+  __device__ static T zero() { return __ushort_as_half((unsigned short)0); }
+  __device__ static T one() { return __ushort_as_half((unsigned short)0x3c00u); }
+  __device__ static T mul(T a, T b) { return __hmul_rn(a, b); }
+  __device__ static T add(T a, T b) { return __hadd_rn(a, b); }
+  __device__ static T sub(T a, T b) { return __hsub_rn(a, b); }
+  __device__ static T div(T a, T b) { return __float2half_rn(__fdiv_rn(__half2float(a), __half2float(b))); }
+  __device__ static T sqrt(T a) { return __float2half_rn(__fsqrt_rn(__half2float(a))); }
+  __device__ static T hypot(T a, T b) { return __float2half_rn(::hypotf(__half2float(a), __half2float(b))); }
+  __device__ static T neg(T a) { return __hneg(a); }
+  __device__ static double wide(T a) { return (double)__half2float(a); }
+  __device__ static bool finite(T a) { return (__half_as_ushort(a) & 0x7c00u) != 0x7c00u; }
+};
+
+// generic typed load of element i of a precision-tagged array
+template <int P>
+__device__ __forceinline__ T_<P> ld(const void* p, uint64_t i) {
+  return static_cast<const T_<P>*>(p)[i];
+}
+template <int P>
+__device__ __forceinline__ T_<P> ldg(const void* p, uint64_t i) {
+  if constexpr (P == P16) {
+    return __ushort_as_half(__ldg(static_cast<const unsigned short*>(p) + i));
+  } else {
+    return __ldg(static_cast<const T_<P>*>(p) + i);
+  }
+}
+// L2-coherent load (bypasses L1) for data written earlier in the SAME kernel
+// (cooperative Richardson passes separated by grid barriers)
+template <int P>
+__device__ __forceinline__ T_<P> ldcg(const void* p, uint64_t i) {
+  if constexpr (P == P16) {
+    return __ushort_as_half(__ldcg(static_cast<const unsigned short*>(p) + i));
+  } else {
+    return __ldcg(static_cast<const T_<P>*>(p) + i);
+  }
+}
+template <int P>
+__device__ __forceinline__ void st(void* p, uint64_t i, T_<P> v) {
+  static_cast<T_<P>*>(p)[i] = v;
+}
+
+// ---- sm_90+/sm_100a async bulk copy (TMA 1D) + mbarrier ------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (src/dst 16B aligned, bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- deterministic reductions ----------------------------------------------------
+// Fixed-shape trees: the result depends only on the inputs' positions, never on
+// scheduling, so repeated solves are bitwise identical (reference
+// tests/test_nesting.cpp:152-165 pins determinism).
+template <int C>
+__device__ __forceinline__ T_<C> warp_sum(T_<C> v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T_<C> w;
+    if constexpr (C == P16) {
+      w = __ushort_as_half(__shfl_xor_sync(0xffffffffu, __half_as_ushort(v), o));
+    } else {
+      w = __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    v = Ar<C>::add(v, w);
+  }
+  return v;
+}
+
+// Block-wide sums of NV values per thread. Result valid in thread 0.
+// scratch: >= (blockDim/32) * NV doubles.
+template <int C, int NV>
+__device__ __forceinline__ void block_sum(T_<C> (&v)[NV], double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = warp_sum<C>(v[k]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) scratch[k * nw + wid] = Ar<C>::wide(v[k]);
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      T_<C> t = lane < nw ? cvt<C>(scratch[k * nw + lane]) : Ar<C>::zero();
+      v[k] = warp_sum<C>(t);
+    }
+  }
+  __syncthreads();
+}
+
+// "last block done": every block publishes its partials, the block that arrives
+// last returns true (and re-arms the counter for the next launch).
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(counter, 1u);
+    is_last = (t == gridDim.x - 1);
+    if (is_last) *counter = 0u;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+// Reduce partials[G][stride] columns 0..nv-1 over G blocks in a fixed tree;
+// called by one whole block; result (as double holding a C value) returned in
+// out[] (shared) -- valid for all threads after the call.
+template <int C>
+__device__ void reduce_partials(const double* partials, int G, int stride, int nv, double* out, double* scratch) {
+  for (int k = 0; k < nv; ++k) {
+    T_<C> acc[1];
+    acc[0] = Ar<C>::zero();
+    for (int b = threadIdx.x; b < G; b += blockDim.x) acc[0] = Ar<C>::add(acc[0], cvt<C>(__ldcg(partials + (size_t)b * stride + k)));
+    block_sum<C, 1>(acc, scratch);
+    if (threadIdx.x == 0) out[k] = Ar<C>::wide(acc[0]);
+    __syncthreads();
+  }
+}
+
+// Software grid barrier for cooperative launches (all blocks co-resident).
+__device__ __forceinline__ void grid_barrier(unsigned* count, volatile unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd((unsigned*)gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace f3rg

@@ -1,0 +1,42 @@
+// dispatch.cuh -- runtime precision tag -> compile-time template argument, plus
+// the launch-geometry helpers shared by the launch_*.cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "launch.hpp"
+#include "levels.cuh"
+
+namespace f3rg {
+
+template <int P>
+using PC = std::integral_constant<int, P>;
+
+template <class F>
+inline void with_p(int p, F&& f) {
+  switch (p) {
+    case P16: f(PC<P16>{}); break;
+    case P32: f(PC<P32>{}); break;
+    default: f(PC<P64>{}); break;
+  }
+}
+
+inline Sync to_sync(SyncH s) { return Sync{s.partials, s.counter}; }
+inline Gate to_gate(GateH g) { return Gate{g.dead, g.n}; }
+
+constexpr int kThreads = 256;
+
+// occupancy-derived persistent grid for a tile kernel instantiation (cached per
+// instantiation by the caller through a function-local static)
+template <class K>
+inline int occupancy_blocks(K kernel, int smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, smem);
+  return nb < 1 ? 1 : nb;
+}
+
+}  // namespace f3rg

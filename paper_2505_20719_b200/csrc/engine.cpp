@@ -1,0 +1,616 @@
+// engine.cpp -- host driver of the device level chain.
+//
+// Mirrors ComposedSolver (reference src/nesting.cpp:176-352) with every level
+// below the outermost one executed as device work captured ONCE into a CUDA graph
+// (one graph = one full invocation of level 2, i.e. the preconditioning action of
+// one outer Arnoldi step, ~130 kernel nodes for fp16-F3R). The host synchronises
+// once per outer step, for the reference's only data-dependent stop
+// (|g_{j+1}| < tol*||b||, src/fgmres.cpp:127). Inner levels run their full
+// budgets with no tolerance test (src/nesting.cpp:99); their rare early stops
+// (happy breakdown / NaN) are honoured on the device through per-level "dead"
+// flags that gate every later kernel of that invocation.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "launch.hpp"
+
+namespace f3rg {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Error(ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void DevBuf::alloc(size_t bytes) {
+  release();
+  if (bytes == 0) bytes = 16;
+  F3RG_CUDA(cudaMalloc(&p_, bytes));
+  n_ = bytes;
+}
+void DevBuf::release() {
+  if (p_) cudaFree(p_);
+  p_ = nullptr;
+  n_ = 0;
+}
+
+static size_t psize(int p) { return p == 0 ? 2 : p == 1 ? 4 : 8; }
+
+// ---- DeviceMatrix -------------------------------------------------------------------
+void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci) {
+  const uint64_t lim = uint64_t{1} << 31;
+  if (n >= lim) throw Error(ERR_DIMENSION, "matrix exceeds 32-bit index range");
+  if (!rp) throw Error(ERR_DIMENSION, "row_ptr length must be n+1");
+  const uint64_t nnz = rp[n];
+  if (nnz >= lim) throw Error(ERR_DIMENSION, "matrix exceeds 32-bit index range");
+  if (rp[0] != 0) throw Error(ERR_DIMENSION, "row_ptr endpoints invalid");
+  for (uint64_t i = 0; i < n; ++i) {
+    if (rp[i] > rp[i + 1]) throw Error(ERR_DIMENSION, "row_ptr must be non-decreasing");
+    for (uint32_t k = rp[i]; k < rp[i + 1]; ++k) {
+      if (ci[k] >= n) throw Error(ERR_DIMENSION, "column index out of bounds in row " + std::to_string(i));
+      if (k > rp[i] && ci[k] <= ci[k - 1])
+        throw Error(ERR_DIMENSION, "columns must be strictly increasing in row " + std::to_string(i));
+    }
+  }
+}
+
+DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values)
+    : n_(n), nnz_(row_ptr ? row_ptr[n] : 0) {
+  validate_csr(n, row_ptr, col_idx);
+  // padded so the 16-byte-granular bulk copies never read past an allocation
+  rp_.alloc((n_ + 1) * 4 + 32);
+  ci_.alloc(nnz_ * 4 + 32);
+  F3RG_CUDA(cudaMemset(rp_.get(), 0, rp_.bytes()));
+  F3RG_CUDA(cudaMemset(ci_.get(), 0, ci_.bytes()));
+  F3RG_CUDA(cudaMemcpy(rp_.get(), row_ptr, (n_ + 1) * 4, cudaMemcpyHostToDevice));
+  if (nnz_) F3RG_CUDA(cudaMemcpy(ci_.get(), col_idx, nnz_ * 4, cudaMemcpyHostToDevice));
+  for (int p = 0; p < 3; ++p) {
+    val_[p].alloc(nnz_ * psize(p) + 32);
+    F3RG_CUDA(cudaMemset(val_[p].get(), 0, val_[p].bytes()));
+  }
+  if (nnz_) F3RG_CUDA(cudaMemcpy(val_[2].get(), values, nnz_ * 8, cudaMemcpyHostToDevice));
+  // replicas: element-wise RNE demotion on the device (cvt.rn.f32.f64 / cvt.rn.f16.f64)
+  F3RG_CUDA(launch_copy(2, 1, Launch{}, val_[2].get(), val_[1].get(), nnz_));
+  F3RG_CUDA(launch_copy(2, 0, Launch{}, val_[2].get(), val_[0].get(), nnz_));
+  std::vector<uint32_t> r0, k0;
+  for (int p = 0; p < 3; ++p) {
+    build_tiles(n_, row_ptr, tile_max_rows(), tile_max_nnz(p), r0, k0);
+    ntiles_[p] = (uint32_t)(r0.size() - 1);
+    tr0_[p].alloc(r0.size() * 4);
+    tk0_[p].alloc(k0.size() * 4);
+    F3RG_CUDA(cudaMemcpy(tr0_[p].get(), r0.data(), r0.size() * 4, cudaMemcpyHostToDevice));
+    F3RG_CUDA(cudaMemcpy(tk0_[p].get(), k0.data(), k0.size() * 4, cudaMemcpyHostToDevice));
+  }
+  F3RG_CUDA(cudaDeviceSynchronize());
+}
+
+CsrDev DeviceMatrix::csr() const {
+  CsrDev c;
+  c.n = n_;
+  c.nnz = nnz_;
+  c.rp = rp_.get<const uint32_t>();
+  c.ci = ci_.get<const uint32_t>();
+  for (int p = 0; p < 3; ++p) c.val[p] = val_[p].get();
+  return c;
+}
+
+TilesDev DeviceMatrix::tiles(int p) const {
+  TilesDev t;
+  t.r0 = tr0_[p].get<const uint32_t>();
+  t.k0 = tk0_[p].get<const uint32_t>();
+  t.ntiles = ntiles_[p];
+  return t;
+}
+
+// ---- Solver ---------------------------------------------------------------------------
+struct Solver::Level {
+  LevelSpec spec;
+  int W = 2;   // basis / rhs precision (level 0: fp64, the precision of b)
+  int PA = 2;  // matrix replica
+  int PZ = 2;  // storage precision of the preconditioned vectors Z (child output, exact)
+  int child = 2;  // 0 FGMRES, 1 Richardson, 2 primary preconditioner
+  // FGMRES
+  DevBuf V, Z, state, H, cs, sn, g, y, scale;
+  LevelState* dstate = nullptr;
+  LevelState host;
+  // Richardson
+  DevBuf rs, omegas, wused, wupd, calls, R, Za, Zb;
+  RichState* drs = nullptr;
+  size_t vbytes(uint64_t n) const { return n * psize(W); }
+  size_t zbytes(uint64_t n) const { return n * psize(PZ); }
+};
+
+struct Solver::ProfRec {
+  std::string name;
+  double bytes;
+  cudaEvent_t e0, e1;
+};
+
+Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind) : spec_(spec), a_(std::move(a)) {
+  if (spec_.levels.empty()) throw Error(ERR_SOLVER, "composed solver needs at least one level");
+  for (const auto& L : spec_.levels)
+    if (L.m < 1) throw Error(ERR_SOLVER, "every level needs m >= 1");
+  for (size_t d = 1; d < spec_.levels.size(); ++d) {
+    const auto& up = spec_.levels[d - 1];
+    const auto& dn = spec_.levels[d];
+    if (dn.pa > up.pa || dn.pv > up.pv)
+      throw Error(ERR_SOLVER, "precision increases from level " + std::to_string(d) + " to level " +
+                                  std::to_string(d + 1) + " (pass allow_precision_increase to permit)");
+  }
+  if (spec_.levels.size() > 15) throw Error(ERR_SOLVER, "at most 15 nesting levels are supported");
+  if (precond_kind != PK_IDENTITY)
+    throw Error(ERR_UNSUPPORTED, "device primary preconditioner: only 'identity' is implemented (ILU(0)/IC(0) is "
+                                 "SURVEY.md 8(f)-1)");
+  for (size_t d = 0; d + 1 < spec_.levels.size(); ++d)
+    if (spec_.levels[d].kind == LK_RICHARDSON)
+      throw Error(ERR_UNSUPPORTED, "a Richardson level with an inner solver below it is not implemented on the device");
+  for (const auto& L : spec_.levels)
+    if (L.kind == LK_FGMRES && L.m > 1000) throw Error(ERR_UNSUPPORTED, "FGMRES cycle length above 1000");
+  id_ = spec_.to_string();
+  n_ = a_->rows();
+  build_levels();
+  capture_inner_graph();
+}
+
+Solver::~Solver() {
+  if (inner_exec_) cudaGraphExecDestroy(inner_exec_);
+  if (own_stream_) cudaStreamDestroy(own_stream_);
+  if (info_host_) cudaFreeHost(info_host_);
+  if (io_host_) cudaFreeHost(io_host_);
+  if (stage_host_) cudaFreeHost(stage_host_);
+  for (auto& p : prof_) {
+    cudaEventDestroy(p->e0);
+    cudaEventDestroy(p->e1);
+  }
+}
+
+void Solver::build_levels() {
+  const int D = (int)spec_.levels.size();
+  F3RG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+  dead_.alloc(16 * sizeof(int));
+  cnt_.alloc(CNT_N * sizeof(unsigned long long));
+  partials_.alloc((size_t)max_partial_blocks() * 16 * sizeof(double));
+  counter_.alloc(64);
+  bar_.alloc(64);
+  info_.alloc(sizeof(StepInfo));
+  norm_.alloc(64);
+  F3RG_CUDA(cudaMemset(dead_.get(), 0, dead_.bytes()));
+  F3RG_CUDA(cudaMemset(cnt_.get(), 0, cnt_.bytes()));
+  F3RG_CUDA(cudaMemset(counter_.get(), 0, counter_.bytes()));
+  F3RG_CUDA(cudaMemset(bar_.get(), 0, bar_.bytes()));
+  F3RG_CUDA(cudaHostAlloc((void**)&info_host_, sizeof(StepInfo), cudaHostAllocDefault));
+  F3RG_CUDA(cudaHostAlloc((void**)&stage_host_, 64 * sizeof(double), cudaHostAllocDefault));
+
+  for (int d = 0; d < D; ++d) {
+    auto L = std::make_unique<Level>();
+    L->spec = spec_.levels[d];
+    L->PA = L->spec.pa;
+    L->W = d == 0 ? (L->spec.kind == LK_FGMRES ? 2 : L->spec.pv) : L->spec.pv;
+    lv_.push_back(std::move(L));
+  }
+  for (int d = 0; d < D; ++d) {
+    Level& L = *lv_[d];
+    if (d + 1 < D) {
+      L.child = lv_[d + 1]->spec.kind == LK_FGMRES ? 0 : 1;
+      L.PZ = lv_[d + 1]->W;  // child output precision (exactly representable)
+    } else {
+      L.child = 2;
+      L.PZ = L.W;
+    }
+    if (L.spec.kind == LK_FGMRES) {
+      const int m = L.spec.m;
+      L.V.alloc((size_t)(m + 1) * L.vbytes(n_) + 16);
+      L.Z.alloc((size_t)m * L.zbytes(n_) + 16);
+      L.H.alloc((size_t)(m + 1) * m * 8);
+      L.cs.alloc((size_t)m * 8);
+      L.sn.alloc((size_t)m * 8);
+      L.g.alloc((size_t)(m + 1) * 8);
+      L.y.alloc((size_t)m * 8);
+      L.scale.alloc((size_t)(m + 1) * 8);
+      F3RG_CUDA(cudaMemset(L.H.get(), 0, L.H.bytes()));
+      F3RG_CUDA(cudaMemset(L.scale.get(), 0, L.scale.bytes()));
+      std::memset(&L.host, 0, sizeof L.host);
+      L.host.m = m;
+      L.host.div_step = -1;
+      L.host.H = L.H.get<double>();
+      L.host.cs = L.cs.get<double>();
+      L.host.sn = L.sn.get<double>();
+      L.host.g = L.g.get<double>();
+      L.host.y = L.y.get<double>();
+      L.host.scale = L.scale.get<double>();
+      L.state.alloc(sizeof(LevelState));
+      F3RG_CUDA(cudaMemcpy(L.state.get(), &L.host, sizeof(LevelState), cudaMemcpyHostToDevice));
+      L.dstate = L.state.get<LevelState>();
+    } else {
+      const int m = L.spec.m;
+      L.omegas.alloc((size_t)m * 8);
+      L.wused.alloc((size_t)m * 8);
+      L.wupd.alloc((size_t)m * 4);
+      L.calls.alloc(4 * 8);
+      L.R.alloc(L.vbytes(n_) + 16);
+      L.Za.alloc(L.vbytes(n_) + 16);
+      L.Zb.alloc(m > 2 ? L.vbytes(n_) + 16 : 16);
+      RichState h;
+      h.m = m;
+      h.cycle = L.spec.cycle;
+      h.omegas = L.omegas.get<double>();
+      h.wused = L.wused.get<double>();
+      h.wupd = L.wupd.get<int>();
+      h.calls = L.calls.get<unsigned long long>();
+      h.R = L.R.get();
+      h.Za = L.Za.get();
+      h.Zb = L.Zb.get();
+      L.rs.alloc(sizeof(RichState));
+      F3RG_CUDA(cudaMemcpy(L.rs.get(), &h, sizeof h, cudaMemcpyHostToDevice));
+      L.drs = L.rs.get<RichState>();
+      reset_richardson(d, nullptr);
+      F3RG_CUDA(cudaDeviceSynchronize());
+    }
+  }
+  Level& top = *lv_[0];
+  xbuf_.alloc(n_ * psize(top.spec.pv) + 16);
+  rbuf_.alloc(n_ * 8 + 16);
+  zbuf_.alloc(n_ * 8 + 16);
+  if (top.spec.kind == LK_FGMRES) {
+    io_.alloc(sizeof(IoSlot));
+    F3RG_CUDA(cudaHostAlloc((void**)&io_host_, sizeof(IoSlot) * (size_t)top.spec.m, cudaHostAllocDefault));
+  }
+}
+
+void Solver::reset_richardson(int l, cudaStream_t s) {
+  Level& L = *lv_[l];
+  std::vector<double> w((size_t)L.spec.m, L.spec.has_omega ? L.spec.omega : 1.0);
+  const unsigned long long calls[4] = {1ull, 0ull, 0ull, 0ull};
+  // synchronous: the state is tiny and resets are rare
+  F3RG_CUDA(cudaStreamSynchronize(s));
+  F3RG_CUDA(cudaMemcpy(L.omegas.get(), w.data(), w.size() * 8, cudaMemcpyHostToDevice));
+  F3RG_CUDA(cudaMemcpy(L.calls.get(), calls, sizeof calls, cudaMemcpyHostToDevice));
+}
+
+// ---- profiling (eager mode only) ------------------------------------------------------
+void Solver::prof_begin(cudaStream_t s) {
+  if (!profiling_now_) return;
+  auto r = std::make_unique<ProfRec>();
+  cudaEventCreate(&r->e0);
+  cudaEventCreate(&r->e1);
+  cudaEventRecord(r->e0, s);
+  prof_.push_back(std::move(r));
+}
+void Solver::prof_end(cudaStream_t s, const char* name, double bytes) {
+  if (!profiling_now_) return;
+  auto& r = prof_.back();
+  r->name = name;
+  r->bytes = bytes;
+  cudaEventRecord(r->e1, s);
+}
+
+std::vector<Solver::KernelTime> Solver::profile_results() const {
+  std::vector<KernelTime> out;
+  for (const auto& r : prof_) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r->e0, r->e1);
+    auto it = std::find_if(out.begin(), out.end(), [&](const KernelTime& k) { return k.name == r->name; });
+    if (it == out.end()) {
+      out.push_back({r->name, 0.0, 0, 0.0});
+      it = out.end() - 1;
+    }
+    it->ms += ms;
+    it->launches += 1;
+    it->bytes += r->bytes;
+  }
+  return out;
+}
+
+#define PROF(name, bytes, call)        \
+  do {                                 \
+    prof_begin(s);                     \
+    F3RG_CUDA(call);                   \
+    prof_end(s, name, (double)(bytes)); \
+  } while (0)
+
+static std::string kname(const char* base, int a, int b, int c) {
+  return std::string(base) + "[" + precision_name(a) + "," + precision_name(b) + "," + precision_name(c) + "]";
+}
+
+// ---- device level chain ----------------------------------------------------------------
+void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
+  Level& L = *lv_[l];
+  const uint64_t n = n_;
+  const double nnz = (double)a_->nnz();
+  void* vj = L.V.get<char>() + (size_t)j * L.vbytes(n);
+  const double* sj = L.scale.get<double>() + j;
+  void* zj = L.Z.get<char>() + (size_t)j * L.zbytes(n);
+  int* dead = dead_.get<int>();
+  auto* cnt = cnt_.get<unsigned long long>();
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  bool materialized = false;
+  if (L.child == 0) {
+    if (top) {
+      io_host_[j] = IoSlot{vj, sj, zj};
+      F3RG_CUDA(cudaMemcpyAsync(io_.get(), &io_host_[j], sizeof(IoSlot), cudaMemcpyHostToDevice, s));
+      if (has_inner_graph_ && !profiling_now_) {
+        F3RG_CUDA(cudaGraphLaunch(inner_exec_, s));
+      } else {
+        enqueue_fgmres(l + 1, nullptr, nullptr, nullptr, io_.get<IoSlot>(), s);
+      }
+    } else {
+      enqueue_fgmres(l + 1, vj, sj, zj, nullptr, s);
+    }
+    materialized = true;
+  } else if (L.child == 1) {
+    Level& R = *lv_[l + 1];
+    const TilesDev T = a_->tiles(R.PA);
+    PROF(kname("richardson", R.PA, R.W, L.W).c_str(),
+         nnz * (psize(R.PA) + 4) + 4.0 * (n + 1) + (double)n * (psize(L.W) + psize(R.W)),
+         launch_richardson(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, vj, sj, zj, n, R.drs, GateH{dead, l + 1}, l + 1,
+                           cnt, sync, bar_.get<unsigned>(), bar_.get<unsigned>() + 1, nullptr));
+  } else {
+    PROF(kname("copy_scaled", L.W, L.W, L.W).c_str(), 2.0 * n * psize(L.W),
+         launch_copy_scaled(L.W, Launch{0, s}, vj, sj, zj, n, GateH{dead, l + 1}, cnt));
+  }
+  const TilesDev T = a_->tiles(L.PA);
+  const int nd = std::min(j + 1, 8);
+  PROF(kname("spmv_dots", L.PA, L.PZ, L.W).c_str(),
+       nnz * (psize(L.PA) + 4) + 4.0 * (n + 1) + (double)n * (psize(L.PZ) + psize(L.W)) + (double)nd * n * psize(L.W),
+       launch_spmv_dots(L.PA, L.PZ, L.W, Launch{0, s}, a_->csr(), T, zj, L.V.get(), n, j, materialized ? nullptr : sj,
+                        L.dstate, GateH{dead, l + 1}, sync));
+  for (int k0 = 8; k0 <= j; k0 += 8)
+    PROF(kname("multi_dot", L.W, L.W, L.W).c_str(), (double)n * psize(L.W) * (1 + std::min(8, j + 1 - k0)),
+         launch_multi_dot(L.W, Launch{0, s}, L.V.get(), n, j, k0, L.dstate, GateH{dead, l + 1}, sync));
+  PROF(kname("cgs", L.W, L.W, L.W).c_str(), (double)n * psize(L.W) * (j + 3),
+       launch_cgs(L.W, Launch{0, s}, L.V.get(), n, j, L.dstate, dead, GateH{dead, l + 1}, l, top ? 1 : 0, top ? 1 : 0,
+                  top ? info_.get<StepInfo>() : nullptr, sync));
+}
+
+void Solver::enqueue_fgmres(int l, void* src, const double* src_scale, void* dst, const IoSlot* io, cudaStream_t s) {
+  Level& L = *lv_[l];
+  Level& P = *lv_[l - 1];
+  const uint64_t n = n_;
+  int* dead = dead_.get<int>();
+  auto* cnt = cnt_.get<unsigned long long>();
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  PROF(kname("level_start", P.W, L.W, L.W).c_str(), (double)n * (2 * psize(P.W) + psize(L.W)),
+       launch_level_start(P.W, L.W, Launch{0, s}, src, src_scale, 1, L.V.get(), n, L.dstate, dead, GateH{dead, l}, l,
+                          cnt, sync, io));
+  for (int j = 0; j < L.spec.m; ++j) enqueue_child_step(l, j, s, false);
+  PROF(kname("level_finish", L.PZ, L.W, L.W).c_str(), (double)n * (L.spec.m * psize(L.PZ) + psize(L.W)),
+       launch_level_finish(L.PZ, L.W, L.W, Launch{0, s}, L.Z.get(), n, L.dstate, dst, 1, GateH{dead, l}, l, cnt, 1, io));
+}
+
+void Solver::capture_inner_graph() {
+  if (lv_.size() < 2 || lv_[0]->spec.kind != LK_FGMRES || lv_[1]->spec.kind != LK_FGMRES) return;
+  cudaStream_t cs = nullptr;
+  F3RG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  F3RG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  try {
+    enqueue_fgmres(1, nullptr, nullptr, nullptr, io_.get<IoSlot>(), cs);
+  } catch (...) {
+    cudaStreamEndCapture(cs, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    throw;
+  }
+  F3RG_CUDA(cudaStreamEndCapture(cs, &graph));
+  const cudaError_t e = cudaGraphInstantiate(&inner_exec_, graph, 0);
+  cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  F3RG_CUDA(e);
+  has_inner_graph_ = true;
+}
+
+double Solver::read_double(const double* dev, cudaStream_t s) {
+  F3RG_CUDA(cudaMemcpyAsync(stage_host_, dev, 8, cudaMemcpyDeviceToHost, s));
+  F3RG_CUDA(cudaStreamSynchronize(s));
+  return stage_host_[0];
+}
+
+double Solver::true_rel(const double* b, double bnorm, cudaStream_t s) {
+  Level& top = *lv_[0];
+  const double nnz = (double)a_->nnz();
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  PROF(kname("residual", 2, top.spec.pv, 2).c_str(), nnz * 12 + 4.0 * (n_ + 1) + (double)n_ * (psize(top.spec.pv) + 16),
+       launch_residual(2, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(2), xbuf_.get(), b, rbuf_.get(), nullptr,
+                       norm_.get<double>(), sync));
+  return read_double(norm_.get<double>(), s) / bnorm;
+}
+
+Report Solver::run(const double* b, double* x_out, const RunOptions& opts, cudaStream_t stream) {
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t s = stream ? stream : own_stream_;
+  profiling_now_ = profile_;
+  if (profiling_now_) {
+    for (auto& p : prof_) {
+      cudaEventDestroy(p->e0);
+      cudaEventDestroy(p->e1);
+    }
+    prof_.clear();
+  }
+  Report rep;
+  rep.solver_id = id_;
+  const int D = (int)lv_.size();
+  F3RG_CUDA(cudaMemsetAsync(cnt_.get(), 0, cnt_.bytes(), s));
+  F3RG_CUDA(cudaMemsetAsync(dead_.get(), 0, dead_.bytes(), s));
+  F3RG_CUDA(cudaMemsetAsync(xbuf_.get(), 0, xbuf_.bytes(), s));
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  PROF("norm2[b]", 8.0 * n_, launch_norm2(2, Launch{0, s}, b, n_, norm_.get<double>(), sync));
+  const double bnorm = read_double(norm_.get<double>(), s);
+  if (bnorm == 0.0) {
+    rep.converged = true;
+    rep.residual_history.push_back(0.0);
+  } else {
+    rep.residual_history.push_back(1.0);
+    rep = lv_[0]->spec.kind == LK_FGMRES ? run_fgmres_top(b, opts, s, bnorm, std::move(rep))
+                                         : run_richardson_top(b, opts, s, bnorm, std::move(rep));
+    rep.final_true_residual = true_rel(b, bnorm, s);
+  }
+  // counters (src/nesting.cpp:347-351)
+  unsigned long long cnt[CNT_N];
+  F3RG_CUDA(cudaMemcpyAsync(stage_host_, cnt_.get(), sizeof cnt, cudaMemcpyDeviceToHost, s));
+  F3RG_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(cnt, stage_host_, sizeof cnt);
+  rep.precond_invocations = cnt[CNT_PRECOND];
+  rep.level_iterations.assign((size_t)D, 0ull);
+  for (int d = 1; d < D; ++d) rep.level_iterations[d] = cnt[CNT_IT + d];
+  rep.level_iterations[0] = lv_[0]->spec.kind == LK_FGMRES ? rep.outer_iterations : cnt[CNT_IT + 0];
+  rep.omegas_final = innermost_omegas();
+  if (x_out) F3RG_CUDA(launch_copy(lv_[0]->spec.pv, 2, Launch{0, s}, xbuf_.get(), x_out, n_));
+  F3RG_CUDA(cudaStreamSynchronize(s));
+  profiling_now_ = false;
+  rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return rep;
+}
+
+Report Solver::run_fgmres_top(const double* b, const RunOptions& opts, cudaStream_t s, double bnorm, Report rep) {
+  Level& top = *lv_[0];
+  const int m1 = top.spec.m;
+  const uint64_t n = n_;
+  const double nnz = (double)a_->nnz();
+  int* dead = dead_.get<int>();
+  auto* cnt = cnt_.get<unsigned long long>();
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  int executions = 0;
+  const int max_exec = 1 + std::max(0, opts.max_outer_restarts);
+  for (;;) {
+    const unsigned long long remaining = opts.max_outer_total - rep.outer_iterations;
+    if (remaining == 0) {
+      rep.flag = "capped";
+      break;
+    }
+    const int len = (int)std::min<unsigned long long>((unsigned long long)m1, remaining);
+    // ---- one cycle (src/fgmres.cpp:21-148) ----
+    const bool first = executions == 0;
+    if (first) {  // r = b
+      PROF("level_start[f64,f64,f64]", 16.0 * n,
+           launch_level_start(2, 2, Launch{0, s}, const_cast<double*>(b), nullptr, 0, top.V.get(), n, top.dstate, dead,
+                              GateH{dead, 0}, 0, cnt, sync, nullptr));
+    } else {  // r = b - A x
+      PROF(kname("residual", top.PA, top.spec.pv, 2).c_str(),
+           nnz * (psize(top.PA) + 4) + 4.0 * (n + 1) + (double)n * (psize(top.spec.pv) + 16),
+           launch_residual(top.PA, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(top.PA), xbuf_.get(), b,
+                           top.V.get(), top.dstate, nullptr, sync));
+    }
+    F3RG_CUDA(cudaMemsetAsync(dead, 0, sizeof(int), s));
+    F3RG_CUDA(cudaMemcpyAsync(stage_host_, top.dstate, sizeof(LevelState), cudaMemcpyDeviceToHost, s));
+    F3RG_CUDA(cudaStreamSynchronize(s));
+    LevelState st;
+    std::memcpy(&st, stage_host_, sizeof st);
+    const double beta = st.beta;
+    // cycle-level outcome
+    int iterations = 0;
+    bool diverged = false, happy = false;
+    int div_step = -1;
+    double residual_norm = beta;
+    if (beta == 0.0 || !std::isfinite(beta)) {
+      diverged = !std::isfinite(beta);
+      div_step = diverged ? 0 : -1;
+    } else {
+      // x_is_zero: bnorm = beta; else norm2(converted(b, W)) = ||b|| at fp64
+      F3RG_CUDA(launch_set_outer(Launch{0, s}, top.dstate, first ? beta : bnorm, opts.tol));
+      for (int j = 0; j < len; ++j) {
+        enqueue_child_step(0, j, s, true);
+        F3RG_CUDA(cudaMemcpyAsync(info_host_, info_.get(), sizeof(StepInfo), cudaMemcpyDeviceToHost, s));
+        F3RG_CUDA(cudaStreamSynchronize(s));
+        const StepInfo inf = *info_host_;
+        if (inf.diverged) {
+          diverged = true;
+          div_step = inf.div_step;
+          break;
+        }
+        iterations = inf.k;
+        residual_norm = inf.estimate;
+        rep.residual_history.push_back(inf.estimate / bnorm);
+        if (inf.happy) {
+          happy = true;
+          break;
+        }
+        if (inf.tol_hit) break;
+      }
+      (void)happy;
+      // back-substitution + x += Z y
+      PROF(kname("level_finish", top.PZ, top.W, top.spec.pv).c_str(),
+           (double)n * (iterations * psize(top.PZ) + 2 * psize(top.spec.pv)),
+           launch_level_finish(top.PZ, top.W, top.spec.pv, Launch{0, s}, top.Z.get(), n, top.dstate, xbuf_.get(), 0,
+                               GateH{dead, 0}, 0, cnt, 0, nullptr));
+    }
+    rep.outer_iterations += (unsigned long long)iterations;
+    if (diverged) {
+      rep.flag = "divergence at outer step " + std::to_string(div_step);
+      break;
+    }
+    if (residual_norm < opts.tol * bnorm && true_rel(b, bnorm, s) < opts.tol) {
+      rep.converged = true;
+      break;
+    }
+    ++executions;
+    if (executions >= max_exec) {
+      rep.flag = "capped";
+      break;
+    }
+    if (opts.reset_richardson_on_restart)
+      for (int d = 1; d < (int)lv_.size(); ++d)
+        if (lv_[d]->spec.kind == LK_RICHARDSON) reset_richardson(d, s);
+  }
+  return rep;
+}
+
+Report Solver::run_richardson_top(const double* b, const RunOptions& opts, cudaStream_t s, double bnorm, Report rep) {
+  Level& top = *lv_[0];
+  const int pv = top.spec.pv;
+  const uint64_t n = n_;
+  const double nnz = (double)a_->nnz();
+  int* dead = dead_.get<int>();
+  auto* cnt = cnt_.get<unsigned long long>();
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  F3RG_CUDA(launch_copy(2, pv, Launch{0, s}, b, rbuf_.get(), n));  // r = b
+  for (;;) {
+    if (rep.outer_iterations >= opts.max_outer_total) {
+      rep.flag = "capped";
+      break;
+    }
+    PROF(kname("richardson", top.PA, pv, pv).c_str(), nnz * (psize(top.PA) + 4) + 4.0 * (n + 1) + 2.0 * n * psize(pv),
+         launch_richardson(top.PA, pv, pv, Launch{0, s}, a_->csr(), a_->tiles(top.PA), rbuf_.get(), nullptr,
+                           zbuf_.get(), n, top.drs, GateH{dead, 0}, 0, cnt, sync, bar_.get<unsigned>(),
+                           bar_.get<unsigned>() + 1, nullptr));
+    F3RG_CUDA(launch_axpy(pv, pv, Launch{0, s}, 1.0, zbuf_.get(), xbuf_.get(), n));
+    rep.outer_iterations += 1;
+    PROF(kname("residual", top.PA, pv, pv).c_str(), nnz * (psize(top.PA) + 4) + 4.0 * (n + 1) + (double)n * (2 * psize(pv) + 8),
+         launch_residual(top.PA, pv, pv, Launch{0, s}, a_->csr(), a_->tiles(top.PA), xbuf_.get(), b, rbuf_.get(),
+                         nullptr, norm_.get<double>(), sync));
+    const double rel = read_double(norm_.get<double>(), s) / bnorm;
+    rep.residual_history.push_back(rel);
+    if (!std::isfinite(rel)) {
+      rep.flag = "divergence";
+      break;
+    }
+    if (rel < opts.tol && true_rel(b, bnorm, s) < opts.tol) {
+      rep.converged = true;
+      break;
+    }
+  }
+  return rep;
+}
+
+std::vector<double> Solver::innermost_omegas() {
+  for (int d = (int)lv_.size() - 1; d >= 1; --d) {
+    Level& L = *lv_[d];
+    if (L.spec.kind == LK_RICHARDSON) {
+      std::vector<double> w((size_t)L.spec.m);
+      F3RG_CUDA(cudaDeviceSynchronize());
+      F3RG_CUDA(cudaMemcpy(w.data(), L.omegas.get(), w.size() * 8, cudaMemcpyDeviceToHost));
+      return w;
+    }
+  }
+  return {};
+}
+
+std::vector<unsigned long long> Solver::level_invocations() {
+  unsigned long long cnt[CNT_N];
+  F3RG_CUDA(cudaDeviceSynchronize());
+  F3RG_CUDA(cudaMemcpy(cnt, cnt_.get(), sizeof cnt, cudaMemcpyDeviceToHost));
+  return std::vector<unsigned long long>(cnt + CNT_INV, cnt + CNT_INV + lv_.size());
+}
+
+}  // namespace f3rg

@@ -1,0 +1,208 @@
+// engine.hpp -- host-side C++ of the f3rg engine: error classes, the solver-spec
+// grammar, device-resident CSR replicas with their tile tables, and the composed
+// solver that drives the device level chain. The public boundary is the C ABI in
+// include/f3rg.h (capi.cpp); this header is internal.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "state.hpp"
+
+namespace f3rg {
+
+// error codes shared with include/f3rg.h
+enum ErrCode {
+  ERR_OK = 0,
+  ERR_DIMENSION = 2,      // f3r::DimensionError
+  ERR_SOLVER = 3,         // f3r::SolverError
+  ERR_PARSE = 4,          // f3r::ParseError
+  ERR_FACTORIZATION = 5,  // f3r::FactorizationError
+  ERR_CUDA = 6,           // CUDA runtime failure (no reference counterpart)
+  ERR_UNSUPPORTED = 7,    // valid reference input this device build does not implement
+  ERR_INTERNAL = 9
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define F3RG_CUDA(x) ::f3rg::cuda_check((x), #x)
+
+// ---- device memory ----------------------------------------------------------------
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t bytes) { alloc(bytes); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_, n_ = o.n_;
+      o.p_ = nullptr, o.n_ = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t bytes);
+  void release();
+  template <class T = void>
+  T* get() const {
+    return static_cast<T*>(p_);
+  }
+  size_t bytes() const { return n_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// ---- solver spec (reference include/f3r/solver_spec.hpp:30-62) ---------------------
+enum LevelKind { LK_FGMRES = 0, LK_RICHARDSON = 1 };
+enum PrecondKind { PK_ILU0 = 0, PK_IC0 = 1, PK_IDENTITY = 2 };
+
+struct LevelSpec {
+  int kind = LK_FGMRES;
+  int m = 1;
+  int pa = 2;  // matrix precision (Richardson: its one precision)
+  int pv = 2;  // vector precision
+  unsigned long long cycle = 64;
+  bool has_omega = false;
+  double omega = 1.0;
+};
+
+struct PrecondSpec {
+  bool has_kind = false;
+  int kind = PK_ILU0;
+  bool has_blocks = false;
+  unsigned long long blocks = 0;
+  bool has_alpha = false;
+  double alpha = 1.0;
+  bool has_prec = false;
+  int prec = 2;
+};
+
+struct Spec {
+  std::vector<LevelSpec> levels;
+  bool has_precond = false;
+  PrecondSpec precond;
+  std::string to_string() const;  // canonical form (src/solver_spec.cpp:165-212)
+};
+
+Spec parse_spec(const std::string& text);  // throws Error(ERR_PARSE)
+const char* precision_name(int p);
+
+// ---- tiles ----------------------------------------------------------------------------
+// Contiguous row ranges with <= max_rows rows and <= max_nnz nonzeros; a row longer
+// than max_nnz forms its own tile. Outputs r0/k0 of length ntiles+1.
+void build_tiles(uint64_t n, const uint32_t* rp, uint32_t max_rows, uint32_t max_nnz, std::vector<uint32_t>& r0,
+                 std::vector<uint32_t>& k0);
+uint32_t tile_max_nnz(int pa);
+uint32_t tile_max_rows();
+
+// ---- device matrix (reference SparseCsr + PrecisionReplicas, include/f3r/csr.hpp) ----
+class DeviceMatrix {
+ public:
+  // validates like SparseCsr::validate (src/csr.cpp:51-69) and uploads one shared
+  // index copy plus the fp64 / fp32 / fp16 value replicas (RNE demotions, :83-92)
+  DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values);
+  uint64_t rows() const { return n_; }
+  uint64_t nnz() const { return nnz_; }
+  CsrDev csr() const;
+  TilesDev tiles(int p) const;
+  const void* values(int p) const { return val_[p].get(); }
+
+ private:
+  uint64_t n_ = 0, nnz_ = 0;
+  DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3];
+  uint32_t ntiles_[3] = {0, 0, 0};
+};
+
+void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci);
+
+// ---- composed solver (reference include/f3r/nesting.hpp:55-77) ------------------------
+struct RunOptions {
+  double tol = 1e-8;
+  int max_outer_restarts = 3;
+  unsigned long long max_outer_total = 300;
+  bool reset_richardson_on_restart = false;
+};
+
+struct Report {
+  bool converged = false;
+  unsigned long long outer_iterations = 0;
+  unsigned long long precond_invocations = 0;
+  std::vector<unsigned long long> level_iterations;
+  std::vector<double> residual_history;
+  double final_true_residual = 0.0;
+  double wall_seconds = 0.0;
+  std::vector<double> omegas_final;
+  std::string flag;
+  std::string solver_id;
+};
+
+class Solver {
+ public:
+  Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind);
+  ~Solver();
+  Solver(const Solver&) = delete;
+  Solver& operator=(const Solver&) = delete;
+
+  // b, x: device fp64 vectors of length n (x may be null). stream 0 = own stream.
+  Report run(const double* b_dev, double* x_dev, const RunOptions& opts, cudaStream_t stream);
+  std::vector<double> innermost_omegas();
+  std::vector<unsigned long long> level_invocations();
+  const std::string& id() const { return id_; }
+  uint64_t rows() const { return a_->rows(); }
+  // per-kernel timing of the NEXT run (CUDA events around every launch, eager mode)
+  void set_profile(bool on) { profile_ = on; }
+  struct KernelTime {
+    std::string name;
+    double ms;
+    unsigned long long launches;
+    double bytes;  // algorithmic bytes over all launches
+  };
+  std::vector<KernelTime> profile_results() const;
+
+ private:
+  struct Level;
+  void build_levels();
+  void capture_inner_graph();
+  void enqueue_fgmres(int l, void* src, const double* src_scale, void* dst, const IoSlot* io, cudaStream_t s);
+  void enqueue_child_step(int l, int j, cudaStream_t s, bool top);
+  void reset_richardson(int l, cudaStream_t s);
+  double read_double(const double* dev, cudaStream_t s);
+  Report run_fgmres_top(const double* b, const RunOptions& opts, cudaStream_t s, double bnorm, Report rep);
+  Report run_richardson_top(const double* b, const RunOptions& opts, cudaStream_t s, double bnorm, Report rep);
+  double true_rel(const double* b, double bnorm, cudaStream_t s);
+  void prof_begin(cudaStream_t s);
+  void prof_end(cudaStream_t s, const char* name, double bytes);
+
+  Spec spec_;
+  std::string id_;
+  std::shared_ptr<DeviceMatrix> a_;
+  std::vector<std::unique_ptr<Level>> lv_;
+  uint64_t n_ = 0;
+  DevBuf dead_, cnt_, partials_, counter_, bar_, info_, io_, norm_, xbuf_, rbuf_, zbuf_;
+  StepInfo* info_host_ = nullptr;
+  IoSlot* io_host_ = nullptr;
+  double* stage_host_ = nullptr;
+  cudaStream_t own_stream_ = nullptr;
+  cudaGraphExec_t inner_exec_ = nullptr;
+  bool has_inner_graph_ = false;
+  bool profile_ = false;
+  bool profiling_now_ = false;
+  struct ProfRec;
+  std::vector<std::unique_ptr<ProfRec>> prof_;
+};
+
+}  // namespace f3rg

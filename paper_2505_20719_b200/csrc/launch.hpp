@@ -1,0 +1,80 @@
+// launch.hpp -- host-side launchers: map runtime precision tags (0 = f16, 1 = f32,
+// 2 = f64) onto the kernel template instantiations. Implemented in launch_*.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace f3rg {
+
+struct CsrDev;
+struct TilesDev;
+struct LevelState;
+struct RichState;
+struct StepInfo;
+struct IoSlot;
+
+struct GateH {
+  const int* dead;
+  int n;
+};
+struct SyncH {
+  double* partials;
+  unsigned* counter;
+};
+
+struct Launch {
+  int grid = 0;  // 0: launcher picks (persistent, occupancy-sized)
+  cudaStream_t stream = nullptr;
+};
+
+// grid used for streaming (BLAS-1 style) kernels and for tile kernels (per value
+// precision and whether the kernel is the cooperative Richardson one)
+int stream_grid();
+int tile_grid(int pa, uint32_t ntiles);
+int richardson_grid(int pa, int pw, int pv, uint32_t ntiles);
+int max_partial_blocks();
+int sm_count();
+
+// ---- FGMRES level ------------------------------------------------------------------
+cudaError_t launch_level_start(int ps, int pw, Launch l, void* src, const double* src_scale, int writeback, void* dst,
+                               uint64_t n, LevelState* L, int* dead, GateH gate, int level, unsigned long long* cnt,
+                               SyncH sync, const IoSlot* io);
+cudaError_t launch_copy_scaled(int pw, Launch l, void* v, const double* scale, void* z, uint64_t n, GateH gate,
+                               unsigned long long* cnt);
+cudaError_t launch_spmv_dots(int pa, int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z,
+                             void* V, uint64_t n, int j, const double* scale_j, LevelState* L, GateH gate,
+                             SyncH sync);
+cudaError_t launch_multi_dot(int pw, Launch l, const void* V, uint64_t n, int j, int k0, LevelState* L, GateH gate,
+                             SyncH sync);
+cudaError_t launch_cgs(int pw, Launch l, void* V, uint64_t n, int j, LevelState* L, int* dead, GateH gate, int level,
+                       int outer, int use_tol, StepInfo* info, SyncH sync);
+cudaError_t launch_level_finish(int pz, int pw, int px, Launch l, const void* Z, uint64_t n, LevelState* L, void* x,
+                                int x_is_zero, GateH gate, int level, unsigned long long* cnt, int count_iterations,
+                                const IoSlot* io);
+cudaError_t launch_residual(int pa, int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
+                            const double* b, void* r, LevelState* L, double* out_norm, SyncH sync);
+cudaError_t launch_set_outer(Launch l, LevelState* L, double bnorm, double tol);
+
+// ---- Richardson (cooperative) ----------------------------------------------------
+cudaError_t launch_richardson(int pa, int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, const void* v,
+                              const double* v_scale, void* out, uint64_t n, RichState* RS, GateH gate, int level,
+                              unsigned long long* cnt, SyncH sync, unsigned* bar_count, unsigned* bar_gen,
+                              const IoSlot* io);
+
+// ---- BLAS-1 / SpMV (kernel-level entry points) ----------------------------------
+cudaError_t launch_fill(int p, Launch l, void* x, uint64_t n, double value);
+cudaError_t launch_copy(int px, int py, Launch l, const void* x, void* y, uint64_t n);
+cudaError_t launch_scale(int p, Launch l, double alpha, void* x, uint64_t n);
+cudaError_t launch_axpy(int px, int py, Launch l, double alpha, const void* x, void* y, uint64_t n);
+cudaError_t launch_add_scaled(int px, int py, int po, Launch l, const void* x, double alpha, const void* y, void* out,
+                              uint64_t n);
+// dot at C = max(floor, px, py) -> *out (device); norm: sqrt at precision px of the
+// result rounded to px (norm2 semantics, x == y)
+cudaError_t launch_dot(int px, int py, int floor_p, Launch l, const void* x, const void* y, uint64_t n, double* out,
+                       SyncH sync);
+cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* out, SyncH sync);
+cudaError_t launch_spmv(int pa, int px, int py, Launch l, const CsrDev& A, const TilesDev& T, const void* x, void* y);
+
+}  // namespace f3rg

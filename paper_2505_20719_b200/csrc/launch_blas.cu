@@ -1,0 +1,92 @@
+// launch_blas.cu -- launchers for the precision-generic BLAS-1 / SpMV kernels (blas1.cuh).
+#include "blas1.cuh"
+#include "dispatch.cuh"
+
+namespace f3rg {
+
+cudaError_t launch_fill(int p, Launch l, void* x, uint64_t n, double value) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(p, [&](auto P) { k_fill<decltype(P)::value><<<g, kThreads, 0, l.stream>>>(x, n, value); });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(int px, int py, Launch l, const void* x, void* y, uint64_t n) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(px, [&](auto X) {
+    with_p(py, [&](auto Y) { k_copy<decltype(X)::value, decltype(Y)::value><<<g, kThreads, 0, l.stream>>>(x, y, n); });
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale(int p, Launch l, double alpha, void* x, uint64_t n) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(p, [&](auto P) { k_scale<decltype(P)::value><<<g, kThreads, 0, l.stream>>>(alpha, x, n); });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy(int px, int py, Launch l, double alpha, const void* x, void* y, uint64_t n) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(px, [&](auto X) {
+    with_p(py, [&](auto Y) {
+      k_axpy<decltype(X)::value, decltype(Y)::value><<<g, kThreads, 0, l.stream>>>(alpha, x, y, n);
+    });
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_scaled(int px, int py, int po, Launch l, const void* x, double alpha, const void* y, void* out,
+                              uint64_t n) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(px, [&](auto X) {
+    with_p(py, [&](auto Y) {
+      with_p(po, [&](auto O) {
+        k_add_scaled<decltype(X)::value, decltype(Y)::value, decltype(O)::value>
+            <<<g, kThreads, 0, l.stream>>>(x, alpha, y, out, n);
+      });
+    });
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot(int px, int py, int floor_p, Launch l, const void* x, const void* y, uint64_t n, double* out,
+                       SyncH sync) {
+  const int g = l.grid ? l.grid : stream_grid();
+  const int c = floor_p > px ? (floor_p > py ? floor_p : py) : (px > py ? px : py);
+  with_p(px, [&](auto X) {
+    with_p(py, [&](auto Y) {
+      with_p(c, [&](auto C) {
+        constexpr int CX = decltype(C)::value, PX = decltype(X)::value, PY = decltype(Y)::value;
+        if constexpr (CX >= PX && CX >= PY)
+          k_dot<PX, PY, CX, false, CX><<<g, kThreads, 0, l.stream>>>(x, y, n, out, to_sync(sync));
+      });
+    });
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* out, SyncH sync) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(px, [&](auto X) {
+    constexpr int PX = decltype(X)::value;
+    k_dot<PX, PX, PX, true, PX><<<g, kThreads, 0, l.stream>>>(x, x, n, out, to_sync(sync));
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmv(int pa, int px, int py, Launch l, const CsrDev& A, const TilesDev& T, const void* x, void* y) {
+  with_p(pa, [&](auto PA_) {
+    constexpr int PA = decltype(PA_)::value;
+    with_p(px, [&](auto X) {
+      with_p(py, [&](auto Y) {
+        auto kern = k_spmv<PA, decltype(X)::value, decltype(Y)::value>;
+        static const int occ = occupancy_blocks(kern, TileCfg<PA>::SMEM_BYTES);
+        (void)occ;
+        const int g = l.grid ? l.grid : tile_grid(PA, T.ntiles);
+        kern<<<g, kThreads, TileCfg<PA>::SMEM_BYTES, l.stream>>>(A, T, x, y);
+      });
+    });
+  });
+  return cudaGetLastError();
+}
+
+}  // namespace f3rg

@@ -1,0 +1,135 @@
+// launch_level.cu -- launchers for the FGMRES level kernels (levels.cuh).
+#include "dispatch.cuh"
+#include "levels.cuh"
+
+namespace f3rg {
+
+int sm_count() {
+  static int sms = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 1;
+  }();
+  return sms;
+}
+int stream_grid() { return sm_count() * 8; }
+int max_partial_blocks() { return sm_count() * 8; }
+
+int tile_grid(int pa, uint32_t ntiles) {
+  int occ = 1;
+  with_p(pa, [&](auto A) {
+    constexpr int PA = decltype(A)::value;
+    // all tile kernels of one value precision share the smem footprint; the
+    // plain SpMV instantiation stands in for the family
+    static const int o = occupancy_blocks(k_spmv_dots<PA, PA, PA>, TileCfg<PA>::SMEM_BYTES);
+    occ = o;
+  });
+  long g = (long)occ * sm_count();
+  if (g > (long)ntiles) g = ntiles;
+  return g < 1 ? 1 : (int)g;
+}
+
+cudaError_t launch_level_start(int ps, int pw, Launch l, void* src, const double* src_scale, int writeback, void* dst,
+                               uint64_t n, LevelState* L, int* dead, GateH gate, int level, unsigned long long* cnt,
+                               SyncH sync, const IoSlot* io) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(ps, [&](auto S) {
+    with_p(pw, [&](auto W) {
+      k_level_start<decltype(S)::value, decltype(W)::value><<<g, kThreads, 0, l.stream>>>(
+          src, src_scale, writeback, dst, n, L, dead, to_gate(gate), level, cnt, to_sync(sync), io);
+    });
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_scaled(int pw, Launch l, void* v, const double* scale, void* z, uint64_t n, GateH gate,
+                               unsigned long long* cnt) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(pw, [&](auto W) {
+    k_copy_scaled<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(v, scale, z, n, to_gate(gate), cnt);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmv_dots(int pa, int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z,
+                             void* V, uint64_t n, int j, const double* scale_j, LevelState* L, GateH gate,
+                             SyncH sync) {
+  with_p(pa, [&](auto PA_) {
+    constexpr int PA = decltype(PA_)::value;
+    with_p(pz, [&](auto Z) {
+      with_p(pw, [&](auto W) {
+        auto kern = k_spmv_dots<PA, decltype(Z)::value, decltype(W)::value>;
+        static const int occ = occupancy_blocks(kern, TileCfg<PA>::SMEM_BYTES);
+        (void)occ;
+        const int g = l.grid ? l.grid : tile_grid(PA, T.ntiles);
+        kern<<<g, kThreads, TileCfg<PA>::SMEM_BYTES, l.stream>>>(A, T, z, V, n, j, scale_j, L, to_gate(gate),
+                                                                 to_sync(sync));
+      });
+    });
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_multi_dot(int pw, Launch l, const void* V, uint64_t n, int j, int k0, LevelState* L, GateH gate,
+                             SyncH sync) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(pw, [&](auto W) {
+    k_multi_dot<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(V, n, j, k0, L, to_gate(gate), to_sync(sync));
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cgs(int pw, Launch l, void* V, uint64_t n, int j, LevelState* L, int* dead, GateH gate, int level,
+                       int outer, int use_tol, StepInfo* info, SyncH sync) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(pw, [&](auto W) {
+    k_cgs<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(V, n, j, L, dead, to_gate(gate), level, outer, use_tol,
+                                                            info, to_sync(sync));
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_level_finish(int pz, int pw, int px, Launch l, const void* Z, uint64_t n, LevelState* L, void* x,
+                                int x_is_zero, GateH gate, int level, unsigned long long* cnt, int count_iterations,
+                                const IoSlot* io) {
+  const int g = l.grid ? l.grid : stream_grid();
+  with_p(pz, [&](auto PZ) {
+    with_p(pw, [&](auto W) {
+      with_p(px, [&](auto X) {
+        k_level_finish<decltype(PZ)::value, decltype(W)::value, decltype(X)::value><<<g, kThreads, 0, l.stream>>>(
+            Z, n, L, x, x_is_zero, to_gate(gate), level, cnt, count_iterations, io);
+      });
+    });
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_residual(int pa, int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
+                            const double* b, void* r, LevelState* L, double* out_norm, SyncH sync) {
+  with_p(pa, [&](auto PA_) {
+    constexpr int PA = decltype(PA_)::value;
+    with_p(px, [&](auto X) {
+      with_p(pw, [&](auto W) {
+        auto kern = k_residual<PA, decltype(X)::value, decltype(W)::value>;
+        static const int occ = occupancy_blocks(kern, TileCfg<PA>::SMEM_BYTES);
+        (void)occ;
+        const int g = l.grid ? l.grid : tile_grid(PA, T.ntiles);
+        kern<<<g, kThreads, TileCfg<PA>::SMEM_BYTES, l.stream>>>(A, T, x, b, r, L, out_norm, to_sync(sync));
+      });
+    });
+  });
+  return cudaGetLastError();
+}
+
+__global__ void k_set_outer(LevelState* L, double bnorm, double tol) {
+  L->bnorm = bnorm;
+  L->tol = tol;
+}
+
+cudaError_t launch_set_outer(Launch l, LevelState* L, double bnorm, double tol) {
+  k_set_outer<<<1, 1, 0, l.stream>>>(L, bnorm, tol);
+  return cudaGetLastError();
+}
+
+}  // namespace f3rg

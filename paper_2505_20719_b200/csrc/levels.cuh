@@ -1,0 +1,383 @@
+// levels.cuh -- device kernels of one FGMRES level (reference src/fgmres.cpp:21-148
+// and src/nesting.cpp:46-112), all Hessenberg / Givens / least-squares work kept on
+// the device so an inner level never synchronises with the host.
+//
+// Per Arnoldi step j of a level with basis precision W:
+//   [child solve on v_j]                 -> z_j  (child's output precision, exact)
+//   k_spmv_dots : w = A z_j (C = promote(A, W), rounded to W) fused with the
+//                 classical Gram-Schmidt projections h_i = (w, v_i), i <= j
+//                 (fp16-F3R: j+1 <= 8 always; larger j adds k_multi_dot passes)
+//   k_cgs       : w -= sum_i h_i v_i (sequential axpys per element, as the
+//                 reference), ||w||, divergence test, Givens update, estimate
+// and per invocation:
+//   k_level_start : demote the parent's v_j (cast, src/nesting.cpp:60), ||b||,
+//                   v_0 scale -- the Arnoldi start (src/fgmres.cpp:29-54)
+//   k_level_finish: back-substitution + x += Z y (src/fgmres.cpp:133-146)
+//
+// Basis storage: slot j+1 holds the UN-normalised w written by k_cgs together with
+// its scale fl_W(1/||w||) (reference scale_in_place, a reciprocal multiply); the
+// first kernel that reads v_{j+1} row-locally applies the scale and writes the
+// normalised values back, so normalisation costs no extra pass over HBM.
+#pragma once
+
+#include "common.cuh"
+#include "spmv.cuh"
+
+namespace f3rg {
+
+constexpr int kMaxPart = 16;  // partial slots per block
+
+
+struct Gate {
+  const int* dead;  // per-level "stopped early" flags
+  int n;            // kernel is skipped if any dead[0..n-1] != 0
+  __device__ __forceinline__ bool closed() const {
+    for (int i = 0; i < n; ++i)
+      if (dead[i]) return true;
+    return false;
+  }
+};
+
+
+
+struct Sync {
+  double* partials;   // gridDim.x * kMaxPart
+  unsigned* counter;  // last-block counter
+};
+
+// ------------------------------------------------------------------------------
+// v_0 of an invocation: dst = demote(src * s) (s optional); optionally write the
+// scaled source back (materialising the parent's normalised basis vector); norm.
+template <int PS, int PW>
+__global__ void __launch_bounds__(256) k_level_start(void* src, const double* src_scale, int writeback, void* dst,
+                                                     uint64_t n, LevelState* L, int* dead, Gate gate, int level,
+                                                     unsigned long long* cnt, Sync sync, const IoSlot* io) {
+  __shared__ double scratch[64];
+  if (gate.closed()) return;
+  if (io) {
+    src = io->src;
+    src_scale = io->src_scale;
+  }
+  const T_<PS> s = src_scale ? cvt<PS>(*src_scale) : Ar<PS>::one();
+  T_<PW> acc[1] = {Ar<PW>::zero()};
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    T_<PS> v = ld<PS>(src, i);
+    if (src_scale) {
+      v = Ar<PS>::mul(s, v);
+      if (writeback) st<PS>(src, i, v);
+    }
+    const T_<PW> d = cvt<PW>(v);
+    st<PW>(dst, i, d);
+    acc[0] = Ar<PW>::add(acc[0], Ar<PW>::mul(d, d));
+  }
+  block_sum<PW, 1>(acc, scratch);
+  if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
+  if (!last_block(sync.counter)) return;
+  __shared__ double tot[1];
+  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, 1, tot, scratch);
+  if (threadIdx.x == 0) {
+    using A = Ar<PW>;
+    const T_<PW> beta = A::sqrt(cvt<PW>(tot[0]));  // norm2 at the storage precision
+    L->beta = A::wide(beta);
+    L->bnorm = A::wide(beta);
+    L->k = 0;
+    L->happy = L->diverged = L->tol_hit = 0;
+    L->div_step = -1;
+    L->estimate = A::wide(beta);
+    L->g[0] = A::wide(beta);
+    L->scale[0] = A::wide(A::div(A::one(), beta));
+    const bool stop = A::wide(beta) == 0.0 || !A::finite(beta);
+    if (stop) L->diverged = !A::finite(beta);
+    dead[level] = stop ? 1 : 0;
+    cnt[CNT_INV + level] += 1;
+  }
+}
+
+// z_j = v_j for a level whose child is the identity primary preconditioner
+// (src/ilu.cpp:33-36): materialise the normalised basis vector into the Z slot.
+template <int PW>
+__global__ void __launch_bounds__(256) k_copy_scaled(void* v, const double* scale, void* z, uint64_t n, Gate gate,
+                                                     unsigned long long* cnt) {
+  if (gate.closed()) return;
+  const T_<PW> s = scale ? cvt<PW>(*scale) : Ar<PW>::one();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    T_<PW> x = ld<PW>(v, i);
+    if (scale) x = Ar<PW>::mul(s, x);
+    st<PW>(z, i, x);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[CNT_PRECOND] += 1;
+}
+
+// ------------------------------------------------------------------------------
+// w = A z (rounded to W) fused with h_i = (w, v_i) for i < min(j+1, 8).
+template <int C, int PW>
+struct EpiDots {
+  void* w;
+  void* V;
+  uint64_t n;
+  int nd;          // number of projections computed here
+  int j;           // v_j may need normalising + write-back
+  T_<PW> sj;       // its scale
+  bool scale_j;
+  T_<PW> d[8];
+  __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
+    const T_<PW> wi = cvt<PW>(acc);
+    st<PW>(w, i, wi);
+    T_<PW> vj = Ar<PW>::zero();
+    if (scale_j) {  // normalise v_j row-locally and write it back
+      vj = Ar<PW>::mul(sj, ld<PW>(V, (uint64_t)j * n + i));
+      st<PW>(V, (uint64_t)j * n + i, vj);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (k < nd) {
+        const T_<PW> vk = (k == j && scale_j) ? vj : ld<PW>(V, (uint64_t)k * n + i);
+        d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, vk));
+      }
+    }
+  }
+};
+
+template <int PA, int PZ, int PW>
+__global__ void __launch_bounds__(256) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t n, int j,
+                                                   const double* scale_j, LevelState* L, Gate gate, Sync sync) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ double scratch[64];
+  __shared__ double res[8];
+  if (gate.closed()) return;
+  constexpr int C = pmax(PA, PW);
+  GatherPlain<PZ, C> g{z};
+  EpiDots<C, PW> e;
+  e.w = static_cast<uint8_t*>(V) + (size_t)(j + 1) * n * sizeof(T_<PW>);
+  e.V = V;
+  e.n = n;
+  e.nd = j + 1 < 8 ? j + 1 : 8;
+  e.j = j;
+  e.scale_j = scale_j != nullptr;
+  e.sj = scale_j ? cvt<PW>(*scale_j) : Ar<PW>::one();
+#pragma unroll
+  for (int k = 0; k < 8; ++k) e.d[k] = Ar<PW>::zero();
+  spmv_tiles<PA, C>(A, T, g, e, smem);
+  block_sum<PW, 8>(e.d, scratch);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(e.d[k]);
+  if (!last_block(sync.counter)) return;
+  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, e.nd, res, scratch);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < e.nd; ++k) L->H[(size_t)j * (L->m + 1) + k] = res[k];
+}
+
+// remaining projections h_i, i in [k0, min(k0+8, j+1)), for long outer cycles
+template <int PW>
+__global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, int j, int k0, LevelState* L,
+                                                   Gate gate, Sync sync) {
+  __shared__ double scratch[8 * 8];
+  __shared__ double res[8];
+  if (gate.closed()) return;
+  const int nd = (j + 1 - k0) < 8 ? (j + 1 - k0) : 8;
+  T_<PW> d[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) d[k] = Ar<PW>::zero();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const T_<PW> wi = ld<PW>(V, (uint64_t)(j + 1) * n + i);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (k < nd) d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, ld<PW>(V, (uint64_t)(k0 + k) * n + i)));
+  }
+  block_sum<PW, 8>(d, scratch);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(d[k]);
+  if (!last_block(sync.counter)) return;
+  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, nd, res, scratch);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nd; ++k) L->H[(size_t)j * (L->m + 1) + k0 + k] = res[k];
+}
+
+
+// ------------------------------------------------------------------------------
+// CGS subtraction + norm + Givens (src/fgmres.cpp:74-129). `outer` levels never set
+// their dead flag (the host decides) and report through `info`.
+template <int PW>
+__global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelState* L, int* dead, Gate gate,
+                                             int level, int outer, int use_tol, StepInfo* info, Sync sync) {
+  __shared__ double scratch[64];
+  __shared__ double hs[128];
+  __shared__ double tot[1];
+  if (gate.closed()) return;
+  using A = Ar<PW>;
+  const int m1 = L->m + 1;
+  double* h = L->H + (size_t)j * m1;
+  const int nh = j + 1 <= 128 ? j + 1 : 128;
+  for (int k = threadIdx.x; k < nh; k += blockDim.x) hs[k] = -h[k];
+  __syncthreads();
+  T_<PW> acc[1] = {A::zero()};
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  T_<PW>* w = static_cast<T_<PW>*>(V) + (size_t)(j + 1) * n;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    T_<PW> wi = w[i];
+    for (int k = 0; k <= j; ++k) {
+      const T_<PW> a = k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]);
+      wi = A::add(A::mul(a, ld<PW>(V, (uint64_t)k * n + i)), wi);
+    }
+    w[i] = wi;
+    acc[0] = A::add(acc[0], A::mul(wi, wi));
+  }
+  block_sum<PW, 1>(acc, scratch);
+  if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = A::wide(acc[0]);
+  if (!last_block(sync.counter)) return;
+  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, 1, tot, scratch);
+  if (threadIdx.x != 0) return;
+
+  const T_<PW> wnorm = A::sqrt(cvt<PW>(tot[0]));
+  h[j + 1] = A::wide(wnorm);
+  bool bad = !A::finite(wnorm);
+  for (int i = 0; i <= j + 1; ++i) bad = bad || !isfinite(h[i]);
+  bool stop = false;
+  if (bad) {
+    L->diverged = 1;
+    L->div_step = j;
+    stop = true;
+  } else {
+    const bool happy = A::wide(wnorm) == 0.0;
+    if (!happy) L->scale[j + 1] = A::wide(A::div(A::one(), wnorm));
+    // apply the accumulated rotations to column j, then generate the new one
+    for (int i = 0; i < j; ++i) {
+      const T_<PW> c = cvt<PW>(L->cs[i]), s = cvt<PW>(L->sn[i]);
+      const T_<PW> hi = cvt<PW>(h[i]), hi1 = cvt<PW>(h[i + 1]);
+      const T_<PW> t = A::add(A::mul(c, hi), A::mul(s, hi1));
+      h[i + 1] = A::wide(A::add(A::mul(A::neg(s), hi), A::mul(c, hi1)));
+      h[i] = A::wide(t);
+    }
+    const T_<PW> hj = cvt<PW>(h[j]), hj1 = cvt<PW>(h[j + 1]);
+    const T_<PW> rho = A::hypot(hj, hj1);
+    T_<PW> c, s;
+    if (A::wide(rho) == 0.0) {
+      c = A::one();
+      s = A::zero();
+    } else {
+      c = A::div(hj, rho);
+      s = A::div(hj1, rho);
+    }
+    L->cs[j] = A::wide(c);
+    L->sn[j] = A::wide(s);
+    h[j] = A::wide(rho);
+    h[j + 1] = 0.0;
+    const T_<PW> gj = cvt<PW>(L->g[j]);
+    L->g[j + 1] = A::wide(A::mul(A::neg(s), gj));
+    L->g[j] = A::wide(A::mul(c, gj));
+    L->k = j + 1;
+    const double est = fabs(L->g[j + 1]);
+    L->estimate = est;
+    if (happy) {
+      L->happy = 1;
+      stop = true;
+    } else if (use_tol && est < L->tol * L->bnorm) {
+      L->tol_hit = 1;
+      stop = true;
+    }
+  }
+  if (!outer && stop) dead[level] = 1;
+  if (info) {
+    info->estimate = L->estimate;
+    info->k = L->k;
+    info->happy = L->happy;
+    info->diverged = L->diverged;
+    info->div_step = L->div_step;
+    info->tol_hit = L->tol_hit;
+  }
+}
+
+// ------------------------------------------------------------------------------
+// Back-substitution (in W) + x (+)= sum_l y_l z_l, sequential axpys per element
+// (src/fgmres.cpp:133-146). x_is_zero: inner levels start from fill(out, 0).
+template <int PZ, int PW, int PX>
+__global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n, LevelState* L, void* x,
+                                                      int x_is_zero, Gate gate, int level, unsigned long long* cnt,
+                                                      int count_iterations, const IoSlot* io) {
+  __shared__ double ys[1024];
+  if (gate.closed()) return;
+  if (io) x = io->dst;
+  using A = Ar<PW>;
+  const int k = L->k;
+  const int m1 = L->m + 1;
+  if (threadIdx.x == 0) {
+    for (int i = k - 1; i >= 0; --i) {
+      T_<PW> acc = cvt<PW>(L->g[i]);
+      for (int l = i + 1; l < k; ++l)
+        acc = A::sub(acc, A::mul(cvt<PW>(L->H[(size_t)l * m1 + i]), cvt<PW>(ys[l])));
+      ys[i] = A::wide(A::div(acc, cvt<PW>(L->H[(size_t)i * m1 + i])));
+    }
+    if (blockIdx.x == 0) {
+      for (int i = 0; i < k; ++i) L->y[i] = ys[i];
+      if (count_iterations) cnt[CNT_IT + level] += (unsigned long long)k;
+    }
+  }
+  __syncthreads();
+  constexpr int C = pmax(PW, PX);  // axpy(y, z, x): compute at promote(z, x)
+  using AC = Ar<C>;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    T_<PX> xi = x_is_zero ? cvt<PX>(0.0) : ld<PX>(x, i);
+    for (int l = 0; l < k; ++l) {
+      const T_<C> a = cvt<C>(ys[l]);
+      xi = cvt<PX>(AC::add(AC::mul(a, cvt<C>(ld<PZ>(Z, (uint64_t)l * n + i))), cvt<C>(xi)));
+    }
+    st<PX>(x, i, xi);
+  }
+}
+
+// ------------------------------------------------------------------------------
+// r = b - A x (restart residual / true residual, src/fgmres.cpp:31-38,
+// src/nesting.cpp:165-173) with ||r||^2 partials. ax is rounded to W first,
+// exactly as op.multiply(x, ax) followed by add_scaled(b, -1, ax, r).
+template <int C, int PW>
+struct EpiResidual {
+  const double* b;  // fp64 right-hand side
+  void* r;
+  T_<PW> acc;
+  __device__ __forceinline__ void row(uint32_t i, T_<C> y) {
+    constexpr int CR = pmax(P64, PW);  // promote(b=f64, ax=W, r=W)
+    const T_<CR> ax = cvt<CR>(cvt<PW>(y));
+    const T_<PW> ri = cvt<PW>(Ar<CR>::add(cvt<CR>(b[i]), Ar<CR>::neg(ax)));
+    st<PW>(r, i, ri);
+    acc = Ar<PW>::add(acc, Ar<PW>::mul(ri, ri));
+  }
+};
+
+// result: L (if non-null) gets the Arnoldi start like k_level_start; norm2 (W) is
+// also written to *out_norm.
+template <int PA, int PX, int PW>
+__global__ void __launch_bounds__(256) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
+                                                  LevelState* L, double* out_norm, Sync sync) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ double scratch[64];
+  __shared__ double tot[1];
+  constexpr int C = pmax(PA, PX);
+  GatherPlain<PX, C> g{x};
+  EpiResidual<C, PW> e{b, r, Ar<PW>::zero()};
+  spmv_tiles<PA, C>(A, T, g, e, smem);
+  T_<PW> acc[1] = {e.acc};
+  block_sum<PW, 1>(acc, scratch);
+  if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
+  if (!last_block(sync.counter)) return;
+  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, 1, tot, scratch);
+  if (threadIdx.x == 0) {
+    using AW = Ar<PW>;
+    const T_<PW> beta = AW::sqrt(cvt<PW>(tot[0]));
+    if (out_norm) *out_norm = AW::wide(beta);
+    if (L) {
+      L->beta = AW::wide(beta);
+      L->k = 0;
+      L->happy = L->diverged = L->tol_hit = 0;
+      L->div_step = -1;
+      L->estimate = AW::wide(beta);
+      L->g[0] = AW::wide(beta);
+      L->scale[0] = AW::wide(AW::div(AW::one(), beta));
+    }
+  }
+}
+
+}  // namespace f3rg

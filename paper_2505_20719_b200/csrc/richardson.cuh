@@ -1,0 +1,218 @@
+// richardson.cuh -- the innermost weighted-Richardson solve (reference
+// src/richardson.cpp:10-54, include/f3r/richardson.hpp:26-53) with the identity
+// primary preconditioner, as ONE kernel per invocation.
+//
+// Non-update calls (63 of every 64 with c = 64) take the fused sweep: with z0 = 0
+// and M = I, z1 = fl(fl(w0*v) + 0) is an element-wise function of v, so the m = 2
+// solve  z2 = z1 + w1 (v - A z1)  is a single SpMV pass that recomputes z1 on the
+// fly for every gathered column. The residual and z1 never touch HBM: the pass
+// reads v (the parent's basis vector, demoted in-register), A16 + indices and
+// writes z2 -- SURVEY.md Appendix A.1's exact per-element sequence.
+//
+// Update calls (call_count % c == 0) compute w' = (r, A r) / (A r, A r) at >= fp32
+// with device-side reductions and grid barriers (the kernel is launched
+// cooperatively so all CTAs are co-resident); the weight bookkeeping (cumulative
+// average with l = call_count/c - 1, degenerate fallback) runs on the device, so
+// no call ever synchronises with the host.
+#pragma once
+
+#include "common.cuh"
+#include "levels.cuh"
+#include "spmv.cuh"
+
+namespace f3rg {
+
+
+// Right-hand side of the call: v_i = demote(s * parent_v_i) (s optional).
+template <int PV, int PW>
+struct RhsView {
+  const void* v;
+  T_<PV> s;
+  bool scaled;
+  __device__ __forceinline__ T_<PW> operator()(uint64_t i) const {
+    T_<PV> x = ldg<PV>(v, i);
+    if (scaled) x = Ar<PV>::mul(s, x);
+    return cvt<PW>(x);
+  }
+};
+
+// z1 = fl(fl(w0 * v) + 0)  -- axpy into a zero-filled z (the +0 turns -0 into +0)
+template <int PV, int PW, int C>
+struct GatherZ1 {
+  RhsView<PV, PW> rhs;
+  T_<PW> w0;
+  __device__ __forceinline__ T_<C> operator()(uint32_t c) const {
+    return cvt<C>(Ar<PW>::add(Ar<PW>::mul(w0, rhs(c)), Ar<PW>::zero()));
+  }
+};
+
+// one fused step k >= 1: r = v - A z_k ; z_{k+1} = z_k + w_k r  (M = I, p = r)
+template <int PV, int PW, int C, bool Z1_ON_THE_FLY>
+struct EpiStep {
+  RhsView<PV, PW> rhs;
+  T_<PW> w0, wk;
+  const void* zk;  // materialised z_k (when not on the fly)
+  void* out;
+  __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
+    using A = Ar<PW>;
+    const T_<PW> s = cvt<PW>(acc);
+    const T_<PW> vi = rhs(i);
+    const T_<PW> r = A::add(vi, A::neg(s));  // add_scaled(v, -1, s): C = wp, -1*s exact
+    T_<PW> zi;
+    if constexpr (Z1_ON_THE_FLY) {
+      zi = A::add(A::mul(w0, vi), A::zero());
+    } else {
+      zi = ldcg<PW>(zk, i);
+    }
+    st<PW>(out, i, A::add(A::mul(wk, r), zi));
+  }
+};
+
+// update-call phase B: s = A p (rounded to wp), (r, s) and (s, s) at >= fp32
+template <int PV, int PW, int C, int CD>
+struct EpiDotsRs {
+  RhsView<PV, PW> rhs;
+  const void* R;  // p = r (nullptr: r = v)
+  T_<CD> num, den;
+  __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
+    const T_<PW> s = cvt<PW>(acc);
+    const T_<PW> r = R ? ldcg<PW>(R, i) : rhs(i);
+    num = Ar<CD>::add(num, Ar<CD>::mul(cvt<CD>(r), cvt<CD>(s)));
+    den = Ar<CD>::add(den, Ar<CD>::mul(cvt<CD>(s), cvt<CD>(s)));
+  }
+};
+
+// update-call phase A: r_k = v - A z_k (materialised)
+template <int PV, int PW, int C>
+struct EpiResid {
+  RhsView<PV, PW> rhs;
+  void* R;
+  __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
+    const T_<PW> s = cvt<PW>(acc);
+    st<PW>(R, i, Ar<PW>::add(rhs(i), Ar<PW>::neg(s)));
+  }
+};
+
+template <int PA, int PW, int PV>
+__global__ void __launch_bounds__(256) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
+                                                    void* out, uint64_t n, RichState* RS, Gate gate, int level,
+                                                    unsigned long long* cnt, Sync sync, unsigned* bar_count,
+                                                    unsigned* bar_gen, const IoSlot* io) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ double scratch[64];
+  __shared__ double red[2];
+  if (gate.closed()) return;
+  if (io) {
+    v = io->src;
+    v_scale = io->src_scale;
+    out = io->dst;
+  }
+  constexpr int C = pmax(PA, PW);    // SpMV accumulator (multiply(z, scratch))
+  constexpr int CD = pmax(P32, PW);  // w' inner products: dot_at_least(.., P32)
+  using AW = Ar<PW>;
+  const int m = RS->m;
+  const unsigned long long call = RS->calls[0];
+  const bool update = RS->cycle != 0ull && (call % RS->cycle) == 0ull;
+  RhsView<PV, PW> rhs{v, v_scale ? cvt<PV>(*v_scale) : Ar<PV>::one(), v_scale != nullptr};
+  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+
+  if (!update) {
+    const T_<PW> w0 = cvt<PW>(RS->omegas[0]);
+    if (m == 1) {
+      for (uint64_t i = gtid; i < n; i += gstride) st<PW>(out, i, AW::add(AW::mul(w0, rhs(i)), AW::zero()));
+    } else {
+      // step 1 with z1 on the fly, then steps 2..m-1 ping-ponging through scratch
+      {
+        GatherZ1<PV, PW, C> g{rhs, w0};
+        EpiStep<PV, PW, C, true> e{rhs, w0, cvt<PW>(RS->omegas[1]), nullptr, m == 2 ? out : RS->Za};
+        spmv_tiles<PA, C>(A, T, g, e, smem);
+      }
+      for (int k = 2; k < m; ++k) {
+        grid_barrier(bar_count, bar_gen);
+        const void* zk = (k % 2 == 0) ? RS->Za : RS->Zb;
+        void* zn = (k + 1 == m) ? out : ((k % 2 == 0) ? RS->Zb : RS->Za);
+        GatherCG<PW, C> g{zk};
+        EpiStep<PV, PW, C, false> e{rhs, w0, cvt<PW>(RS->omegas[k]), zk, zn};
+        spmv_tiles<PA, C>(A, T, g, e, smem);
+      }
+    }
+  } else {
+    // generic adaptive-weight call: for each step k
+    //   A (k>0): r = v - A z_k      B: s = A r, (r,s), (s,s) -> w'      C: z += w' r
+    for (int k = 0; k < m; ++k) {
+      if (k > 0) {
+        GatherCG<PW, C> g{RS->Za};
+        EpiResid<PV, PW, C> e{rhs, RS->R};
+        spmv_tiles<PA, C>(A, T, g, e, smem);
+        grid_barrier(bar_count, bar_gen);
+      }
+      {
+        EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? RS->R : nullptr, Ar<CD>::zero(), Ar<CD>::zero()};
+        if (k == 0) {
+          struct GatherRhs {
+            RhsView<PV, PW> rhs;
+            __device__ __forceinline__ T_<C> operator()(uint32_t c) const { return cvt<C>(rhs(c)); }
+          } g{rhs};
+          spmv_tiles<PA, C>(A, T, g, e, smem);
+        } else {
+          GatherCG<PW, C> g{RS->R};
+          spmv_tiles<PA, C>(A, T, g, e, smem);
+        }
+        T_<CD> acc[2] = {e.num, e.den};
+        block_sum<CD, 2>(acc, scratch);
+        if (threadIdx.x == 0) {
+          sync.partials[(size_t)blockIdx.x * kMaxPart + 0] = Ar<CD>::wide(acc[0]);
+          sync.partials[(size_t)blockIdx.x * kMaxPart + 1] = Ar<CD>::wide(acc[1]);
+        }
+        grid_barrier(bar_count, bar_gen);
+        // every CTA reduces the partials in the same fixed order -> identical w'
+        reduce_partials<CD>(sync.partials, gridDim.x, kMaxPart, 2, red, scratch);
+      }
+      const double num = red[0], den = red[1];
+      double wk;
+      int fresh;
+      if (den == 0.0 || !isfinite(num) || !isfinite(den)) {
+        wk = RS->omegas[k];
+        fresh = 0;
+      } else {
+        wk = Ar<CD>::wide(Ar<CD>::div(cvt<CD>(num), cvt<CD>(den)));
+        fresh = 1;
+      }
+      const T_<PW> wh = cvt<PW>(wk);
+      void* zn = (k + 1 == m) ? out : RS->Za;
+      for (uint64_t i = gtid; i < n; i += gstride) {
+        const T_<PW> p = k > 0 ? ldcg<PW>(RS->R, i) : rhs(i);
+        const T_<PW> zi = k > 0 ? ldcg<PW>(RS->Za, i) : AW::zero();
+        st<PW>(zn, i, AW::add(AW::mul(wh, p), zi));
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        RS->wused[k] = wk;
+        RS->wupd[k] = fresh;
+      }
+      if (k + 1 < m) grid_barrier(bar_count, bar_gen);
+      __syncthreads();
+    }
+  }
+  // bookkeeping once every CTA is done reading the state
+  if (!last_block(sync.counter)) return;
+  if (threadIdx.x == 0) {
+    if (update) {
+      const double l = (double)(call / RS->cycle - 1ull);
+      for (int k = 0; k < m; ++k) {
+        if (RS->wupd[k]) {
+          RS->omegas[k] = __ddiv_rn(__dadd_rn(__dmul_rn(l, RS->omegas[k]), RS->wused[k]), __dadd_rn(l, 1.0));
+        } else {
+          RS->calls[2] += 1ull;
+        }
+      }
+      RS->calls[1] += 1ull;
+    }
+    RS->calls[0] = call + 1ull;
+    cnt[CNT_INV + level] += 1ull;
+    cnt[CNT_IT + level] += (unsigned long long)m;
+    cnt[CNT_PRECOND] += (unsigned long long)m;
+  }
+}
+
+}  // namespace f3rg

@@ -1,0 +1,69 @@
+// state.hpp -- plain structs shared by host (C++) and device (CUDA) code: the
+// device-resident CSR view, tile table, per-level FGMRES state, Richardson state,
+// step summary and the I/O indirection slot. No device code here.
+#pragma once
+
+#include <cstdint>
+
+namespace f3rg {
+
+struct CsrDev {
+  uint64_t n = 0, nnz = 0;
+  const uint32_t* rp = nullptr;  // n+1 (+pad)
+  const uint32_t* ci = nullptr;  // nnz (+pad)
+  const void* val[3] = {nullptr, nullptr, nullptr};
+};
+
+struct TilesDev {
+  const uint32_t* r0 = nullptr;  // ntiles+1 row starts
+  const uint32_t* k0 = nullptr;  // ntiles+1 nnz starts (= rp[r0])
+  uint32_t ntiles = 0;
+};
+
+// Device-resident state of one FGMRES level. H is column-major: column j holds
+// h(0..j+1, j) at H[j*(m+1) + i]. All scalars are values of precision W held in
+// doubles (exact).
+struct LevelState {
+  int m;
+  int k;  // Arnoldi steps completed in the current invocation
+  int happy, diverged, div_step, tol_hit;
+  double beta, bnorm, estimate, tol;
+  double* H;
+  double* cs;
+  double* sn;
+  double* g;
+  double* y;
+  double* scale;
+};
+
+// counters layout (unsigned long long): [0..15] level invocations, [16..31] level
+// iterations, [32] primary-preconditioner applications
+enum { CNT_INV = 0, CNT_IT = 16, CNT_PRECOND = 32, CNT_N = 40 };
+
+// Pointers of the outermost inner invocation, read by the captured graph at run
+// time so one graph instance serves every outer Arnoldi step.
+struct IoSlot {
+  void* src;
+  const double* src_scale;
+  void* dst;
+};
+
+// Host-visible summary of one outer step (copied to pinned memory).
+struct StepInfo {
+  double estimate;
+  int k, happy, diverged, div_step, tol_hit, pad;
+};
+
+struct RichState {
+  int m;
+  unsigned long long cycle;
+  double* omegas;             // [m] persistent weights (binary64, as the reference)
+  double* wused;              // [m] weight applied at each step of the current call
+  int* wupd;                  // [m] 1 if step k computed a fresh w'
+  unsigned long long* calls;  // [0] call_count (starts at 1), [1] update_count, [2] degenerate events
+  void* R;                    // scratch vectors at the working precision
+  void* Za;
+  void* Zb;
+};
+
+}  // namespace f3rg

@@ -1,0 +1,154 @@
+"""GPU parity of the composed solve (the hot path) against the CPU oracle and the
+reference itself, mirroring the reference's own suites (tests/test_nesting.cpp,
+tests/acceptance/acceptance.cpp criteria 1, 2, 6, 7):
+
+* outer iteration count equal to the oracle's (north star: within +-10%; the
+  counts here are 2..25, so +-10% means equality up to one iteration),
+* final fp64 relative residual <= tol, recomputed from scratch,
+* level iteration ratios exactly m2, m3, m4 and precond count % 64 == 0,
+* bitwise-deterministic repeated runs, restart / cap arithmetic, zero rhs.
+"""
+import numpy as np
+import pytest
+
+from _util import F3R16, F3R32, F3R64, normwise, small_problems
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _solver(p, spec):
+    import paper_2505_20719_b200 as f
+    reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
+    return f.build(f.parse_solver_spec(spec), reps, f.IdentityPrecond(p.n)), reps
+
+
+@pytest.fixture(scope="module")
+def probs(cuda):
+    return small_problems()
+
+
+@pytest.mark.parametrize("spec", [F3R16, F3R32, F3R64])
+def test_f3r_matches_oracle(probs, oracle, spec):
+    import paper_2505_20719_b200 as f
+    for name, p in probs:
+        s, _ = _solver(p, spec)
+        run = s.run(p.b, f.RunOptions(tol=TOL))
+        ref = oracle.solve((p.n, p.row_ptr, p.col_idx), p.values, spec, p.b, tol=TOL)
+        rep = run.report
+        assert rep.converged == ref.converged, name
+        assert rep.final_true_residual <= TOL, (name, rep.final_true_residual)
+        assert abs(rep.outer_iterations - ref.outer_iterations) <= max(1, round(0.1 * ref.outer_iterations)), \
+            (name, rep.outer_iterations, ref.outer_iterations)
+        assert rep.level_iterations[1] == 8 * rep.level_iterations[0]
+        assert rep.level_iterations[2] == 4 * rep.level_iterations[1]
+        assert rep.level_iterations[3] == 2 * rep.level_iterations[2]
+        assert rep.precond_invocations == rep.level_iterations[3]
+        assert rep.precond_invocations % 64 == 0
+        assert len(rep.residual_history) == rep.outer_iterations + 1
+        # estimates agree with the oracle's early history (before rounding noise dominates)
+        k = min(3, len(ref.residual_history), len(rep.residual_history))
+        assert np.allclose(rep.residual_history[:k], ref.residual_history[:k], rtol=1e-3), name
+        assert normwise(run.x, ref.x) < 1e-6, name
+
+
+def test_config1_full_vs_reference(cuda, reference):
+    """BASELINE config 1 (7-pt Poisson 64^3) against the UNMODIFIED reference."""
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+    p = problems.problem(1)
+    s, _ = _solver(p, F3R16)
+    run = s.run(p.b, f.RunOptions(tol=TOL))
+    reference.set_threads(0)
+    m = reference.matrix(p.row_ptr, p.col_idx, p.values)
+    ref = reference.solve(m, F3R16, p.b, tol=TOL)
+    assert run.report.converged and ref.converged
+    assert run.report.outer_iterations == ref.outer_iterations
+    assert run.report.final_true_residual <= TOL
+    assert run.report.precond_invocations == ref.precond_invocations
+
+
+def test_determinism_bitwise(probs):
+    import paper_2505_20719_b200 as f
+    name, p = probs[0]
+    s1, _ = _solver(p, F3R16)
+    s2, _ = _solver(p, F3R16)
+    r1 = s1.run(p.b, f.RunOptions(tol=TOL))
+    r2 = s2.run(p.b, f.RunOptions(tol=TOL))
+    assert r1.report.residual_history == r2.report.residual_history
+    assert np.array_equal(r1.x, r2.x)
+
+
+def test_device_and_host_entry_points_agree(probs, cuda):
+    import paper_2505_20719_b200 as f
+    name, p = probs[1]
+    s1, _ = _solver(p, F3R16)
+    s2, _ = _solver(p, F3R16)
+    r1 = s1.run(p.b, f.RunOptions(tol=TOL))
+    bd = cuda.from_numpy(p.b).cuda()
+    r2 = s2.run(bd, f.RunOptions(tol=TOL))
+    assert r1.report.residual_history == r2.report.residual_history
+    assert np.array_equal(r1.x, r2.x.cpu().numpy())
+
+
+def test_zero_rhs(probs):
+    import paper_2505_20719_b200 as f
+    name, p = probs[0]
+    s, _ = _solver(p, F3R16)
+    run = s.run(np.zeros(p.n), f.RunOptions(tol=TOL))
+    assert run.report.converged and run.report.outer_iterations == 0
+    assert run.report.residual_history == [0.0]
+    assert not np.any(run.x)
+
+
+def test_restart_cap_arithmetic(cuda, oracle):
+    """reference tests/test_nesting.cpp:168-195"""
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+    p = problems.problem(2, grid=4)
+    s, _ = _solver(p, "F2:f64/f64 > F2:f64/f64")
+    run = s.run(p.b, f.RunOptions(tol=1e-300, max_outer_restarts=3, max_outer_total=300))
+    assert not run.report.converged and run.report.flag == "capped"
+    assert run.report.outer_iterations == 8
+    s, _ = _solver(p, "F100:f64/f64 > F2:f64/f64")
+    run = s.run(p.b, f.RunOptions(tol=1e-300, max_outer_restarts=3, max_outer_total=150))
+    assert not run.report.converged and run.report.outer_iterations == 150
+
+
+@pytest.mark.parametrize("spec", [
+    "F16:f64/f64",
+    "F100:f64/f64 > F8:f32/f32",
+    "F100:f64/f64 > R2:f16,c=64",
+    "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R3:f16,c=5",
+    "F100:f64/f64 > F64:f16/f16",
+    "R2:f64,c=3",
+    "F10:f64/f64 > R3:f16,c=2,omega=0.7",
+])
+def test_other_specs_match_oracle(cuda, oracle, spec):
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+    p = problems.problem(2, grid=8) if "R2:f64" in spec else problems.problem(4, grid=12)
+    s, _ = _solver(p, spec)
+    run = s.run(p.b, f.RunOptions(tol=TOL))
+    ref = oracle.solve((p.n, p.row_ptr, p.col_idx), p.values, spec, p.b, tol=TOL)
+    assert run.report.converged == ref.converged, spec
+    if ref.converged:
+        assert run.report.final_true_residual <= TOL
+    assert abs(run.report.outer_iterations - ref.outer_iterations) <= max(1, round(0.1 * ref.outer_iterations)), \
+        (spec, run.report.outer_iterations, ref.outer_iterations)
+    assert run.report.precond_invocations == ref.precond_invocations or \
+        abs(run.report.outer_iterations - ref.outer_iterations) > 0
+
+
+def test_build_validation(cuda):
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+    p = problems.problem(2, grid=2)
+    reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
+    with pytest.raises(f.SolverError):
+        f.build(f.parse_solver_spec("F8:f32/f32 > F4:f64/f64"), reps, f.IdentityPrecond(p.n))
+    with pytest.raises(f.DimensionError):
+        f.build(f.parse_solver_spec("F8:f32/f32"), reps, f.IdentityPrecond(p.n + 1))
+    with pytest.raises(f.ParseError):
+        f.parse_solver_spec("F8:f32")
