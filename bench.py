@@ -1,0 +1,290 @@
+#!/usr/bin/env python
+"""bench.py -- time-to-solution of the fp16-F3R solve (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One "step" = one complete fp16-F3R solve (F100:f64/f64 > F8:f32/f32 > F4:f16/f32 >
+R2:f16,c=64, identity M) of BASELINE config 2 (27-point 128^3, n = 2,097,152,
+nnz = 55,742,968, x_true ~ U[-1,1] seed 1) to relative residual 1e-10, from a
+zero initial guess, inputs resident in HBM. The matrix replicas (A16 + indices
+alone: 334 MB) exceed the 126 MB L2, so no explicit flush is needed between steps.
+
+Printed JSON line (rank 0): value = mean time-to-solution (s, lower is better),
+e2e = the same solve through the C ABI with host buffers (pinned b in, x out),
+roofline = the dominant kernel's achieved HBM GB/s (algorithmic bytes, SURVEY.md
+§8(d)) over the measured copy peak, cpu_baseline = the unmodified reference CPU
+solver on this host (one outer iteration, extrapolated to the full count).
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, built from
+/root/reference/proj/src) on all host threads; each step = one outer iteration
+of the same config, value extrapolated to the reference's full outer count.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+SPEC = "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > identity"
+METRIC = "time-to-solution to rel. residual 1e-10 (s)"
+TOL = 1e-10
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        self.index = index
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        mx = float(rows[0][1])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def reference_runs():
+    path = os.path.join(ROOT, "tests", "golden", "reference_runs.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return {}
+
+
+def cpu_reference_sample(p, outer_full: int, threads: int, sample_outer: int = 1):
+    """Times the UNMODIFIED reference solve for `sample_outer` outer iterations
+    (RunOptions.max_outer_total, include/f3r/nesting.hpp:35); returns seconds per
+    outer iteration and the extrapolated time-to-solution."""
+    from oracle_bind import Reference
+    r = Reference()
+    r.set_threads(threads)
+    m = r.matrix(p.row_ptr, p.col_idx, p.values)
+    rep = r.solve(m, SPEC, p.b, tol=TOL, max_outer_total=sample_outer, want_x=False)
+    per_outer = rep.wall_seconds / max(1, rep.outer_iterations)
+    return per_outer, per_outer * outer_full, rep
+
+
+def run_reference_arm(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from paper_2505_20719_b200 import problems
+    p = problems.problem(args.config)
+    threads = os.cpu_count()
+    runs = reference_runs().get(f"config{args.config}/fp16-f3r", {})
+    outer_full = int(runs.get("outer_iterations", 0)) or None
+    from oracle_bind import Reference, reference_available
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libf3r_ref.so not built"}))
+        return
+    r = Reference()
+    r.set_threads(threads)
+    m = r.matrix(p.row_ptr, p.col_idx, p.values)
+    if outer_full is None:  # no committed full run for this config: measure it once
+        full = r.solve(m, SPEC, p.b, tol=TOL, want_x=False)
+        outer_full = full.outer_iterations
+    for _ in range(min(args.warmup, 1)):
+        r.solve(m, SPEC, p.b, tol=TOL, max_outer_total=1, want_x=False)
+    times = []
+    for _ in range(args.steps):
+        rep = r.solve(m, SPEC, p.b, tol=TOL, max_outer_total=1, want_x=False)
+        times.append(rep.wall_seconds)
+    per_outer = float(np.mean(times))
+    value = per_outer * outer_full
+    sample = (f"1 outer iteration (of {outer_full}) of the reference fp16-F3R solve per step, "
+              f"config {args.config}; value = mean x {outer_full}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": min(args.warmup, 1), "ms_per_step": per_outer * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "mixed f64/f32/f16 (software binary16)",
+        "data": "synthetic", "config": _config(args, p),
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def _config(args, p):
+    return {"workload": f"BASELINE config {args.config}: fp16-F3R solve to 1e-10 (M = identity)", "n": p.n,
+            "nnz": p.nnz, "solver": SPEC, "problem": p.name, "tol": TOL,
+            "l2_flush": "none: working set (A16+idx 334 MB, A32+idx 446 MB) exceeds the 126 MB L2",
+            "parallelism": f"dp{args.gpus}" if args.gpus > 1 else "single GPU"}
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+
+    rank, local, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    p = problems.problem(args.config)
+    reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
+    solver = f.build(f.parse_solver_spec(SPEC), reps, f.IdentityPrecond(p.n))
+    opts = f.RunOptions(tol=TOL)
+    b_dev = torch.from_numpy(p.b).cuda()
+    stream = torch.cuda.current_stream()
+
+    # every step is a fresh solve: the reference's run_once builds a new
+    # ComposedSolver per repeat (src/bench.cpp:210-219); reset() restores that state
+    for _ in range(max(args.warmup, 0)):
+        solver.reset()
+        run = solver.run(b_dev, opts)
+    solver.reset()
+    run = solver.run(b_dev, opts)
+    outer = run.report.outer_iterations
+    assert run.report.converged and run.report.final_true_residual <= TOL, run.report
+
+    # ---- timed region: K full solves, device-resident inputs ----
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            solver.reset()
+            run = solver.run(b_dev, opts)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    if not (run.report.converged and run.report.final_true_residual <= TOL):
+        raise SystemExit(f"timed solve did not converge: {run.report}")
+
+    # ---- e2e: through the C ABI with host buffers (pinned b in, x out) ----
+    b_pin = torch.from_numpy(p.b).pin_memory()
+    b_host = b_pin.numpy()
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 5))):
+        t0 = time.perf_counter()
+        solver.reset()
+        r2 = solver.run(b_host, opts)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e = float(np.mean(e2e_t))
+    assert r2.report.converged
+
+    # ---- per-kernel timing (CUDA events around every launch, eager mode) ----
+    solver.set_profile(True)
+    solver.reset()
+    solver.run(b_dev, opts)
+    solver.set_profile(False)
+    prof = solver.profile()
+    total_ms = sum(k[1] for k in prof)
+    launches = int(sum(k[2] for k in prof))
+    top = max(prof, key=lambda k: k[1])
+    peak, peak_kind = _peaks()
+    per_launch_ms = top[1] / top[2]
+    per_launch_bytes = top[3] / top[2]
+    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    breakdown = sorted(prof, key=lambda k: -k[1])
+    kernels = [{"kernel": k[0], "share": round(k[1] / total_ms, 4), "launches": k[2],
+                "avg_us": round(1e3 * k[1] / k[2], 2),
+                "gbs": round(k[3] / k[2] / (k[1] / k[2] * 1e-3) / 1e9, 1)} for k in breakdown[:8]]
+
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "mixed f64/f32/f16", "data": "synthetic", "config": _config(args, p),
+        "outer_iterations": outer, "final_true_residual": run.report.final_true_residual,
+        "roofline": {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "bytes_per_launch": per_launch_bytes, "avg_launch_us": per_launch_ms * 1e3},
+        "kernels": kernels,
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(p.n * 8), "d2h_bytes_per_step": int(p.n * 8)},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count()
+            per_outer, extrap, rep = cpu_reference_sample(p, outer, threads)
+            line["cpu_baseline"] = {"value": extrap, "unit": "s", "cores": threads, "kind": "reference",
+                                    "sample": f"1 outer iteration of the unmodified reference fp16-F3R solve "
+                                              f"({per_outer:.2f} s), extrapolated x{outer} outer iterations"}
+        except Exception as e:  # keep the GPU line even if the CPU leg fails
+            line["cpu_baseline"] = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

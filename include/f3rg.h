@@ -109,6 +109,10 @@ int f3rg_solve(f3rg_solver* s, const double* b_host, double* x_host, const f3rg_
 /* b, x: DEVICE fp64 arrays (x may be NULL); stream: cudaStream_t or 0 (own stream) */
 int f3rg_solve_device(f3rg_solver* s, const double* b_dev, double* x_dev, const f3rg_run_options* opts,
                       f3rg_report* rep, uintptr_t stream);
+/* restore a freshly built solver's state (Richardson weights and call counters,
+ * include/f3r/richardson.hpp:26-46; they persist across solves exactly as in the
+ * reference's ComposedSolver); stream-ordered on `stream` (0 = own stream) */
+int f3rg_solver_reset_state(f3rg_solver* s, uintptr_t stream);
 /* report vectors of the LAST solve (host memory, up to cap entries) */
 int f3rg_solver_history(const f3rg_solver* s, double* out, uint64_t cap);
 int f3rg_solver_level_iterations(const f3rg_solver* s, uint64_t* out, uint64_t cap);

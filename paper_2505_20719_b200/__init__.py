@@ -108,6 +108,7 @@ def lib():
     L.f3rg_solve.argtypes = [vp, vp, vp, C.POINTER(_RunOpts), C.POINTER(_Report)]
     L.f3rg_solve_device.argtypes = [vp, vp, vp, C.POINTER(_RunOpts), C.POINTER(_Report), C.c_size_t]
     L.f3rg_solver_history.argtypes = [vp, vp, u64]
+    L.f3rg_solver_reset_state.argtypes = [vp, C.c_size_t]
     L.f3rg_solver_level_iterations.argtypes = [vp, vp, u64]
     L.f3rg_solver_omegas.argtypes = [vp, vp, u64]
     L.f3rg_solver_set_profile.argtypes = [vp, i32]
@@ -509,6 +510,11 @@ class ComposedSolver:
         _check(lib().f3rg_solve_device(self.h, t.data_ptr(), x.data_ptr() if x is not None else None,
                                        C.byref(opts._c()), C.byref(r), _stream()))
         return RunResult(x, self._report(r))
+
+    def reset(self) -> None:
+        """Back to a freshly built solver (Richardson weights/counters persist across
+        run() calls, as in the reference); stream-ordered, no host sync."""
+        _check(lib().f3rg_solver_reset_state(self.h, _stream()))
 
     def innermost_omegas(self) -> list:
         om = np.zeros(64)

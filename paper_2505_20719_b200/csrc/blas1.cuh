@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint6
   block_sum<C, 1>(acc, scratch);
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<C>::wide(acc[0]);
   if (!last_block(sync.counter)) return;
-  reduce_partials<C>(sync.partials, gridDim.x, kMaxPart, 1, tot, scratch);
+  reduce_partials<C, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
   if (threadIdx.x == 0) {
     if constexpr (SQRT) {
       *out = Ar<PS>::wide(Ar<PS>::sqrt(cvt<PS>(tot[0])));
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint6
 
 // plain y = A x (any precision triple), for the kernel-level entry point
 template <int PA, int PX, int PY>
-__global__ void __launch_bounds__(256) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {
+__global__ void __launch_bounds__(256, 2) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int C = pmax(PA, PX);
   GatherPlain<PX, C> g{x};

@@ -173,6 +173,10 @@ int f3rg_solve(f3rg_solver* s, const double* b_host, double* x_host, const f3rg_
   });
 }
 
+int f3rg_solver_reset_state(f3rg_solver* s, uintptr_t stream) {
+  return guarded([&] { s->s->reset_state(as_stream(stream)); });
+}
+
 int f3rg_solver_history(const f3rg_solver* s, double* out, uint64_t cap) {
   const auto& h = s->last.residual_history;
   for (uint64_t i = 0; i < h.size() && i < cap; ++i) out[i] = h[i];

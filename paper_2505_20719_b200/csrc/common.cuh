@@ -213,19 +213,24 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return is_last;
 }
 
-// Reduce partials[G][stride] columns 0..nv-1 over G blocks in a fixed tree;
-// called by one whole block; result (as double holding a C value) returned in
-// out[] (shared) -- valid for all threads after the call.
-template <int C>
-__device__ void reduce_partials(const double* partials, int G, int stride, int nv, double* out, double* scratch) {
-  for (int k = 0; k < nv; ++k) {
-    T_<C> acc[1];
-    acc[0] = Ar<C>::zero();
-    for (int b = threadIdx.x; b < G; b += blockDim.x) acc[0] = Ar<C>::add(acc[0], cvt<C>(__ldcg(partials + (size_t)b * stride + k)));
-    block_sum<C, 1>(acc, scratch);
-    if (threadIdx.x == 0) out[k] = Ar<C>::wide(acc[0]);
-    __syncthreads();
+// Reduce partials[G][stride] columns 0..NV-1 over G blocks in a fixed tree;
+// called by one whole block; results (doubles holding C values) in out[] (shared),
+// valid for all threads after the call.
+template <int C, int NV>
+__device__ void reduce_partials(const double* partials, int G, int stride, double* out, double* scratch) {
+  T_<C> acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = Ar<C>::zero();
+  for (int b = threadIdx.x; b < G; b += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = Ar<C>::add(acc[k], cvt<C>(__ldcg(partials + (size_t)b * stride + k)));
   }
+  block_sum<C, NV>(acc, scratch);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = Ar<C>::wide(acc[k]);
+  }
+  __syncthreads();
 }
 
 // Software grid barrier for cooperative launches (all blocks co-resident).

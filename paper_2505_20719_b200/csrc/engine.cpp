@@ -160,6 +160,7 @@ Solver::~Solver() {
   if (info_host_) cudaFreeHost(info_host_);
   if (io_host_) cudaFreeHost(io_host_);
   if (stage_host_) cudaFreeHost(stage_host_);
+  if (reset_host_) cudaFreeHost(reset_host_);
   for (auto& p : prof_) {
     cudaEventDestroy(p->e0);
     cudaEventDestroy(p->e1);
@@ -248,6 +249,15 @@ void Solver::build_levels() {
       reset_richardson(d, nullptr);
       F3RG_CUDA(cudaDeviceSynchronize());
     }
+  }
+  // pinned images of every Richardson level's initial state (reset_state)
+  F3RG_CUDA(cudaHostAlloc((void**)&reset_host_, (size_t)D * 1024 * sizeof(double), cudaHostAllocDefault));
+  for (int d = 0; d < D; ++d) {
+    const LevelSpec& S = spec_.levels[d];
+    double* img = reset_host_ + (size_t)d * 1024;
+    for (int k = 0; k < S.m && k < 1000; ++k) img[k] = S.has_omega ? S.omega : 1.0;
+    unsigned long long calls[4] = {1ull, 0ull, 0ull, 0ull};
+    std::memcpy(img + 1000, calls, sizeof calls);
   }
   Level& top = *lv_[0];
   xbuf_.alloc(n_ * psize(top.spec.pv) + 16);
@@ -591,6 +601,17 @@ Report Solver::run_richardson_top(const double* b, const RunOptions& opts, cudaS
     }
   }
   return rep;
+}
+
+void Solver::reset_state(cudaStream_t stream) {
+  cudaStream_t s = stream ? stream : own_stream_;
+  for (int d = 0; d < (int)lv_.size(); ++d) {
+    Level& L = *lv_[d];
+    if (L.spec.kind != LK_RICHARDSON) continue;
+    const double* img = reset_host_ + (size_t)d * 1024;
+    F3RG_CUDA(cudaMemcpyAsync(L.omegas.get(), img, (size_t)L.spec.m * 8, cudaMemcpyHostToDevice, s));
+    F3RG_CUDA(cudaMemcpyAsync(L.calls.get(), img + 1000, 4 * 8, cudaMemcpyHostToDevice, s));
+  }
 }
 
 std::vector<double> Solver::innermost_omegas() {

@@ -159,6 +159,9 @@ class Solver {
 
   // b, x: device fp64 vectors of length n (x may be null). stream 0 = own stream.
   Report run(const double* b_dev, double* x_dev, const RunOptions& opts, cudaStream_t stream);
+  // back to a freshly built solver's state (Richardson weights 1 or fixed, call
+  // counters 1), stream-ordered; equivalent to constructing a new ComposedSolver
+  void reset_state(cudaStream_t stream);
   std::vector<double> innermost_omegas();
   std::vector<unsigned long long> level_invocations();
   const std::string& id() const { return id_; }
@@ -196,6 +199,7 @@ class Solver {
   StepInfo* info_host_ = nullptr;
   IoSlot* io_host_ = nullptr;
   double* stage_host_ = nullptr;
+  double* reset_host_ = nullptr;  // pinned initial Richardson states, per level
   cudaStream_t own_stream_ = nullptr;
   cudaGraphExec_t inner_exec_ = nullptr;
   bool has_inner_graph_ = false;

@@ -23,6 +23,8 @@
 #include "common.cuh"
 #include "spmv.cuh"
 
+#include <type_traits>
+
 namespace f3rg {
 
 constexpr int kMaxPart = 16;  // partial slots per block
@@ -75,7 +77,7 @@ __global__ void __launch_bounds__(256) k_level_start(void* src, const double* sr
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
   if (!last_block(sync.counter)) return;
   __shared__ double tot[1];
-  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, 1, tot, scratch);
+  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
   if (threadIdx.x == 0) {
     using A = Ar<PW>;
     const T_<PW> beta = A::sqrt(cvt<PW>(tot[0]));  // norm2 at the storage precision
@@ -112,6 +114,30 @@ __global__ void __launch_bounds__(256) k_copy_scaled(void* v, const double* scal
 
 // ------------------------------------------------------------------------------
 // w = A z (rounded to W) fused with h_i = (w, v_i) for i < min(j+1, 8).
+// fixed-size register "array" addressed only with compile-time indices
+template <class T>
+struct Reg8 {
+  T r0, r1, r2, r3, r4, r5, r6, r7;
+  template <int K>
+  __device__ __forceinline__ T& at() {
+    if constexpr (K == 0) return r0;
+    else if constexpr (K == 1) return r1;
+    else if constexpr (K == 2) return r2;
+    else if constexpr (K == 3) return r3;
+    else if constexpr (K == 4) return r4;
+    else if constexpr (K == 5) return r5;
+    else if constexpr (K == 6) return r6;
+    else return r7;
+  }
+};
+template <int K, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (K < N) {
+    f(std::integral_constant<int, K>{});
+    static_for<K + 1, N>(f);
+  }
+}
+
 template <int C, int PW>
 struct EpiDots {
   void* w;
@@ -121,27 +147,35 @@ struct EpiDots {
   int j;           // v_j may need normalising + write-back
   T_<PW> sj;       // its scale
   bool scale_j;
-  T_<PW> d[8];
+  Reg8<T_<PW>> d;
+  Reg8<T_<PW>> vk;  // prefetched v_k(i), k < nd
+  T_<PW> vjr;       // prefetched raw v_j(i) when j >= 8
+  __device__ __forceinline__ void prefetch(uint32_t i) {
+    static_for<0, 8>([&](auto K) {
+      vk.template at<K>() = K < nd ? ld<PW>(V, (uint64_t)K * n + i) : Ar<PW>::zero();
+    });
+    if (scale_j && j >= 8) vjr = ld<PW>(V, (uint64_t)j * n + i);
+  }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> wi = cvt<PW>(acc);
-    st<PW>(w, i, wi);
-    T_<PW> vj = Ar<PW>::zero();
-    if (scale_j) {  // normalise v_j row-locally and write it back
-      vj = Ar<PW>::mul(sj, ld<PW>(V, (uint64_t)j * n + i));
-      st<PW>(V, (uint64_t)j * n + i, vj);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (k < nd) {
-        const T_<PW> vk = (k == j && scale_j) ? vj : ld<PW>(V, (uint64_t)k * n + i);
-        d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, vk));
+    static_for<0, 8>([&](auto K) {
+      if (K < nd) {
+        const bool sk = scale_j && K == j;  // normalise v_j row-locally, write it back
+        T_<PW> v = vk.template at<K>();
+        if (sk) {
+          v = Ar<PW>::mul(sj, v);
+          st<PW>(V, (uint64_t)j * n + i, v);
+        }
+        d.template at<K>() = Ar<PW>::add(d.template at<K>(), Ar<PW>::mul(wi, v));
       }
-    }
+    });
+    if (scale_j && j >= 8) st<PW>(V, (uint64_t)j * n + i, Ar<PW>::mul(sj, vjr));
+    st<PW>(w, i, wi);
   }
 };
 
 template <int PA, int PZ, int PW>
-__global__ void __launch_bounds__(256) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t n, int j,
+__global__ void __launch_bounds__(256, 2) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t n, int j,
                                                    const double* scale_j, LevelState* L, Gate gate, Sync sync) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
@@ -157,14 +191,15 @@ __global__ void __launch_bounds__(256) k_spmv_dots(CsrDev A, TilesDev T, const v
   e.j = j;
   e.scale_j = scale_j != nullptr;
   e.sj = scale_j ? cvt<PW>(*scale_j) : Ar<PW>::one();
-#pragma unroll
-  for (int k = 0; k < 8; ++k) e.d[k] = Ar<PW>::zero();
+  static_for<0, 8>([&](auto K) { e.d.template at<K>() = Ar<PW>::zero(); });
   spmv_tiles<PA, C>(A, T, g, e, smem);
-  block_sum<PW, 8>(e.d, scratch);
+  T_<PW> dd[8];
+  static_for<0, 8>([&](auto K) { dd[K] = e.d.template at<K>(); });
+  block_sum<PW, 8>(dd, scratch);
   if (threadIdx.x == 0)
-    for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(e.d[k]);
+    for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(dd[k]);
   if (!last_block(sync.counter)) return;
-  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, e.nd, res, scratch);
+  reduce_partials<PW, 8>(sync.partials, gridDim.x, kMaxPart, res, scratch);
   if (threadIdx.x == 0)
     for (int k = 0; k < e.nd; ++k) L->H[(size_t)j * (L->m + 1) + k] = res[k];
 }
@@ -191,7 +226,7 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, in
   if (threadIdx.x == 0)
     for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(d[k]);
   if (!last_block(sync.counter)) return;
-  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, nd, res, scratch);
+  reduce_partials<PW, 8>(sync.partials, gridDim.x, kMaxPart, res, scratch);
   if (threadIdx.x == 0)
     for (int k = 0; k < nd; ++k) L->H[(size_t)j * (L->m + 1) + k0 + k] = res[k];
 }
@@ -216,19 +251,40 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
   T_<PW> acc[1] = {A::zero()};
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   T_<PW>* w = static_cast<T_<PW>*>(V) + (size_t)(j + 1) * n;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    T_<PW> wi = w[i];
-    for (int k = 0; k <= j; ++k) {
-      const T_<PW> a = k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]);
-      wi = A::add(A::mul(a, ld<PW>(V, (uint64_t)k * n + i)), wi);
+  // the first <= 8 coefficients live in registers and the loop is specialised on
+  // their count (uniform per launch): no per-element predicates or conversions
+  auto body = [&](auto NJ_) {
+    constexpr int NJ = decltype(NJ_)::value;
+    T_<PW> a[NJ];
+#pragma unroll
+    for (int u = 0; u < NJ; ++u) a[u] = cvt<PW>(hs[u]);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      T_<PW> vv[NJ];
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) vv[u] = ld<PW>(V, (uint64_t)u * n + i);
+      T_<PW> wi = w[i];
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) wi = A::add(A::mul(a[u], vv[u]), wi);
+      for (int k = NJ; k <= j; ++k)  // long outer cycles only
+        wi = A::add(A::mul(k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]), ld<PW>(V, (uint64_t)k * n + i)), wi);
+      w[i] = wi;
+      acc[0] = A::add(acc[0], A::mul(wi, wi));
     }
-    w[i] = wi;
-    acc[0] = A::add(acc[0], A::mul(wi, wi));
+  };
+  switch (j + 1 < 8 ? j + 1 : 8) {
+    case 1: body(std::integral_constant<int, 1>{}); break;
+    case 2: body(std::integral_constant<int, 2>{}); break;
+    case 3: body(std::integral_constant<int, 3>{}); break;
+    case 4: body(std::integral_constant<int, 4>{}); break;
+    case 5: body(std::integral_constant<int, 5>{}); break;
+    case 6: body(std::integral_constant<int, 6>{}); break;
+    case 7: body(std::integral_constant<int, 7>{}); break;
+    default: body(std::integral_constant<int, 8>{}); break;
   }
   block_sum<PW, 1>(acc, scratch);
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = A::wide(acc[0]);
   if (!last_block(sync.counter)) return;
-  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, 1, tot, scratch);
+  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
   if (threadIdx.x != 0) return;
 
   const T_<PW> wnorm = A::sqrt(cvt<PW>(tot[0]));
@@ -319,13 +375,34 @@ __global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n,
   constexpr int C = pmax(PW, PX);  // axpy(y, z, x): compute at promote(z, x)
   using AC = Ar<C>;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    T_<PX> xi = x_is_zero ? cvt<PX>(0.0) : ld<PX>(x, i);
-    for (int l = 0; l < k; ++l) {
-      const T_<C> a = cvt<C>(ys[l]);
-      xi = cvt<PX>(AC::add(AC::mul(a, cvt<C>(ld<PZ>(Z, (uint64_t)l * n + i))), cvt<C>(xi)));
+  // first <= 8 coefficients in registers, loop specialised on their count
+  auto body = [&](auto K_) {
+    constexpr int K = decltype(K_)::value;
+    T_<C> yy[K > 0 ? K : 1];
+#pragma unroll
+    for (int u = 0; u < K; ++u) yy[u] = cvt<C>(ys[u]);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      T_<PZ> zz[K > 0 ? K : 1];
+#pragma unroll
+      for (int u = 0; u < K; ++u) zz[u] = ld<PZ>(Z, (uint64_t)u * n + i);
+      T_<PX> xi = x_is_zero ? cvt<PX>(0.0) : ld<PX>(x, i);
+#pragma unroll
+      for (int u = 0; u < K; ++u) xi = cvt<PX>(AC::add(AC::mul(yy[u], cvt<C>(zz[u])), cvt<C>(xi)));
+      for (int l = K; l < k; ++l)  // long outer cycles only
+        xi = cvt<PX>(AC::add(AC::mul(cvt<C>(ys[l]), cvt<C>(ld<PZ>(Z, (uint64_t)l * n + i))), cvt<C>(xi)));
+      st<PX>(x, i, xi);
     }
-    st<PX>(x, i, xi);
+  };
+  switch (k < 8 ? k : 8) {
+    case 0: body(std::integral_constant<int, 0>{}); break;
+    case 1: body(std::integral_constant<int, 1>{}); break;
+    case 2: body(std::integral_constant<int, 2>{}); break;
+    case 3: body(std::integral_constant<int, 3>{}); break;
+    case 4: body(std::integral_constant<int, 4>{}); break;
+    case 5: body(std::integral_constant<int, 5>{}); break;
+    case 6: body(std::integral_constant<int, 6>{}); break;
+    case 7: body(std::integral_constant<int, 7>{}); break;
+    default: body(std::integral_constant<int, 8>{}); break;
   }
 }
 
@@ -338,10 +415,12 @@ struct EpiResidual {
   const double* b;  // fp64 right-hand side
   void* r;
   T_<PW> acc;
+  double bi;
+  __device__ __forceinline__ void prefetch(uint32_t i) { bi = __ldg(b + i); }
   __device__ __forceinline__ void row(uint32_t i, T_<C> y) {
     constexpr int CR = pmax(P64, PW);  // promote(b=f64, ax=W, r=W)
     const T_<CR> ax = cvt<CR>(cvt<PW>(y));
-    const T_<PW> ri = cvt<PW>(Ar<CR>::add(cvt<CR>(b[i]), Ar<CR>::neg(ax)));
+    const T_<PW> ri = cvt<PW>(Ar<CR>::add(cvt<CR>(bi), Ar<CR>::neg(ax)));
     st<PW>(r, i, ri);
     acc = Ar<PW>::add(acc, Ar<PW>::mul(ri, ri));
   }
@@ -350,20 +429,20 @@ struct EpiResidual {
 // result: L (if non-null) gets the Arnoldi start like k_level_start; norm2 (W) is
 // also written to *out_norm.
 template <int PA, int PX, int PW>
-__global__ void __launch_bounds__(256) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
+__global__ void __launch_bounds__(256, 2) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
                                                   LevelState* L, double* out_norm, Sync sync) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double tot[1];
   constexpr int C = pmax(PA, PX);
   GatherPlain<PX, C> g{x};
-  EpiResidual<C, PW> e{b, r, Ar<PW>::zero()};
+  EpiResidual<C, PW> e{b, r, Ar<PW>::zero(), 0.0};
   spmv_tiles<PA, C>(A, T, g, e, smem);
   T_<PW> acc[1] = {e.acc};
   block_sum<PW, 1>(acc, scratch);
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
   if (!last_block(sync.counter)) return;
-  reduce_partials<PW>(sync.partials, gridDim.x, kMaxPart, 1, tot, scratch);
+  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
   if (threadIdx.x == 0) {
     using AW = Ar<PW>;
     const T_<PW> beta = AW::sqrt(cvt<PW>(tot[0]));

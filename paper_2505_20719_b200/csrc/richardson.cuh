@@ -29,21 +29,24 @@ struct RhsView {
   const void* v;
   T_<PV> s;
   bool scaled;
-  __device__ __forceinline__ T_<PW> operator()(uint64_t i) const {
-    T_<PV> x = ldg<PV>(v, i);
-    if (scaled) x = Ar<PV>::mul(s, x);
-    return cvt<PW>(x);
-  }
+  __device__ __forceinline__ T_<PV> raw(uint64_t i) const { return ldg<PV>(v, i); }
+  // s = 1 when unscaled: fl(1 * x) == x exactly (no flush-to-zero), so no select
+  __device__ __forceinline__ T_<PW> apply(T_<PV> x) const { return cvt<PW>(Ar<PV>::mul(s, x)); }
+  __device__ __forceinline__ T_<PW> operator()(uint64_t i) const { return apply(raw(i)); }
 };
 
-// z1 = fl(fl(w0 * v) + 0)  -- axpy into a zero-filled z (the +0 turns -0 into +0)
+// z1 = fl(fl(w0 * v) + 0) -- axpy into a zero-filled z; the +0 only turns -0 into
+// +0. As a SpMV operand the sign of a zero z1 cannot matter: the row accumulator
+// starts at +0 and an RNE sum is -0 only if both addends are -0, so it is never
+// -0 and acc + (+-0) == acc. The gather therefore skips the +0 (bit-exact); the
+// epilogue, where z1 is added to a possibly -0 term, keeps it.
 template <int PV, int PW, int C>
 struct GatherZ1 {
+  using Raw = T_<PV>;
   RhsView<PV, PW> rhs;
   T_<PW> w0;
-  __device__ __forceinline__ T_<C> operator()(uint32_t c) const {
-    return cvt<C>(Ar<PW>::add(Ar<PW>::mul(w0, rhs(c)), Ar<PW>::zero()));
-  }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
+  __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(Ar<PW>::mul(w0, rhs.apply(r))); }
 };
 
 // one fused step k >= 1: r = v - A z_k ; z_{k+1} = z_k + w_k r  (M = I, p = r)
@@ -53,17 +56,16 @@ struct EpiStep {
   T_<PW> w0, wk;
   const void* zk;  // materialised z_k (when not on the fly)
   void* out;
+  T_<PW> vi, zi;
+  __device__ __forceinline__ void prefetch(uint32_t i) {
+    vi = rhs(i);
+    if constexpr (!Z1_ON_THE_FLY) zi = ldcg<PW>(zk, i);
+  }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     using A = Ar<PW>;
     const T_<PW> s = cvt<PW>(acc);
-    const T_<PW> vi = rhs(i);
     const T_<PW> r = A::add(vi, A::neg(s));  // add_scaled(v, -1, s): C = wp, -1*s exact
-    T_<PW> zi;
-    if constexpr (Z1_ON_THE_FLY) {
-      zi = A::add(A::mul(w0, vi), A::zero());
-    } else {
-      zi = ldcg<PW>(zk, i);
-    }
+    if constexpr (Z1_ON_THE_FLY) zi = A::add(A::mul(w0, vi), A::zero());
     st<PW>(out, i, A::add(A::mul(wk, r), zi));
   }
 };
@@ -74,9 +76,10 @@ struct EpiDotsRs {
   RhsView<PV, PW> rhs;
   const void* R;  // p = r (nullptr: r = v)
   T_<CD> num, den;
+  T_<PW> r;
+  __device__ __forceinline__ void prefetch(uint32_t i) { r = R ? ldcg<PW>(R, i) : rhs(i); }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> s = cvt<PW>(acc);
-    const T_<PW> r = R ? ldcg<PW>(R, i) : rhs(i);
     num = Ar<CD>::add(num, Ar<CD>::mul(cvt<CD>(r), cvt<CD>(s)));
     den = Ar<CD>::add(den, Ar<CD>::mul(cvt<CD>(s), cvt<CD>(s)));
   }
@@ -87,14 +90,16 @@ template <int PV, int PW, int C>
 struct EpiResid {
   RhsView<PV, PW> rhs;
   void* R;
+  T_<PW> vi;
+  __device__ __forceinline__ void prefetch(uint32_t i) { vi = rhs(i); }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> s = cvt<PW>(acc);
-    st<PW>(R, i, Ar<PW>::add(rhs(i), Ar<PW>::neg(s)));
+    st<PW>(R, i, Ar<PW>::add(vi, Ar<PW>::neg(s)));
   }
 };
 
 template <int PA, int PW, int PV>
-__global__ void __launch_bounds__(256) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
+__global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
                                                     void* out, uint64_t n, RichState* RS, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, unsigned* bar_count,
                                                     unsigned* bar_gen, const IoSlot* io) {
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(256) k_richardson(CsrDev A, TilesDev T, const 
       // step 1 with z1 on the fly, then steps 2..m-1 ping-ponging through scratch
       {
         GatherZ1<PV, PW, C> g{rhs, w0};
-        EpiStep<PV, PW, C, true> e{rhs, w0, cvt<PW>(RS->omegas[1]), nullptr, m == 2 ? out : RS->Za};
+        EpiStep<PV, PW, C, true> e{rhs, w0, cvt<PW>(RS->omegas[1]), nullptr, m == 2 ? out : RS->Za, {}, {}};
         spmv_tiles<PA, C>(A, T, g, e, smem);
       }
       for (int k = 2; k < m; ++k) {
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(256) k_richardson(CsrDev A, TilesDev T, const 
         const void* zk = (k % 2 == 0) ? RS->Za : RS->Zb;
         void* zn = (k + 1 == m) ? out : ((k % 2 == 0) ? RS->Zb : RS->Za);
         GatherCG<PW, C> g{zk};
-        EpiStep<PV, PW, C, false> e{rhs, w0, cvt<PW>(RS->omegas[k]), zk, zn};
+        EpiStep<PV, PW, C, false> e{rhs, w0, cvt<PW>(RS->omegas[k]), zk, zn, {}, {}};
         spmv_tiles<PA, C>(A, T, g, e, smem);
       }
     }
@@ -143,16 +148,18 @@ __global__ void __launch_bounds__(256) k_richardson(CsrDev A, TilesDev T, const 
     for (int k = 0; k < m; ++k) {
       if (k > 0) {
         GatherCG<PW, C> g{RS->Za};
-        EpiResid<PV, PW, C> e{rhs, RS->R};
+        EpiResid<PV, PW, C> e{rhs, RS->R, {}};
         spmv_tiles<PA, C>(A, T, g, e, smem);
         grid_barrier(bar_count, bar_gen);
       }
       {
-        EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? RS->R : nullptr, Ar<CD>::zero(), Ar<CD>::zero()};
+        EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? RS->R : nullptr, Ar<CD>::zero(), Ar<CD>::zero(), {}};
         if (k == 0) {
           struct GatherRhs {
+            using Raw = T_<PV>;
             RhsView<PV, PW> rhs;
-            __device__ __forceinline__ T_<C> operator()(uint32_t c) const { return cvt<C>(rhs(c)); }
+            __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
+            __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
           } g{rhs};
           spmv_tiles<PA, C>(A, T, g, e, smem);
         } else {
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(256) k_richardson(CsrDev A, TilesDev T, const 
         }
         grid_barrier(bar_count, bar_gen);
         // every CTA reduces the partials in the same fixed order -> identical w'
-        reduce_partials<CD>(sync.partials, gridDim.x, kMaxPart, 2, red, scratch);
+        reduce_partials<CD, 2>(sync.partials, gridDim.x, kMaxPart, red, scratch);
       }
       const double num = red[0], den = red[1];
       double wk;

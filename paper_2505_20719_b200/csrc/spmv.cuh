@@ -37,6 +37,16 @@ struct TileCfg {
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 64;
 };
 
+// N consecutive entries of one row: issue the N gathers, then accumulate in order.
+template <int C, int N, class TA, class Gather>
+__device__ __forceinline__ void row_chunk(T_<C>& acc, const TA* pv, const uint32_t* pc, const Gather& g) {
+  typename Gather::Raw xs[N];
+#pragma unroll
+  for (int u = 0; u < N; ++u) xs[u] = g.load(pc[u]);
+#pragma unroll
+  for (int u = 0; u < N; ++u) acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[u]), g.value(xs[u])));
+}
+
 // Streams all tiles owned by this CTA (tile t = blockIdx.x + i*gridDim.x) through
 // shared memory and calls epi.row(row, acc) for every row with acc at
 // C = promote(PA, gather precision).
@@ -81,32 +91,55 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
       if (t < T.ntiles) issue(t, s);
     }
   }
+  // gathers are issued CHUNK at a time (independent loads in flight per thread)
+  // before the sequential, order-preserving accumulation consumes them
+  constexpr int CHUNK = 8;
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < T.ntiles; t += G, ++it) {
     const int s = (int)(it % ST);
     const uint32_t par = (it / ST) & 1u;
     const uint32_t r0 = T.r0[t], r1 = T.r0[t + 1], k0 = T.k0[t], k1 = T.k0[t + 1];
+    const bool longrow = k1 - k0 > (uint32_t)Cfg::TNNZ;
+    const uint32_t row = r0 + tid;
+    // row-local epilogue operands do not depend on the tile: start them now so
+    // their latency hides behind the tile transfer and the row sum
+    if (longrow ? tid == 0 : row < r1) e.prefetch(longrow ? r0 : row);
     mbar_wait(&bars[s], par);
-    if (k1 - k0 <= (uint32_t)Cfg::TNNZ) {
+    if (!longrow) {
       const uint8_t* sp = stage_ptr(s);
       const TA* sv = reinterpret_cast<const TA*>(sp);
       const uint32_t* sc = reinterpret_cast<const uint32_t*>(sp + Cfg::VAL_BYTES);
       const uint32_t* sr = reinterpret_cast<const uint32_t*>(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES);
       const uint32_t k0v = k0 & ~(uint32_t)(VAL - 1), k0c = k0 & ~3u, r0a = r0 & ~3u;
-      const uint32_t row = r0 + tid;
       if (row < r1) {
         const uint32_t kb = sr[row - r0a], ke = sr[row + 1 - r0a];
         T_<C> acc = Ar<C>::zero();
         const TA* pv = sv + (kb - k0v);
         const uint32_t* pc = sc + (kb - k0c);
         const uint32_t len = ke - kb;
-#pragma unroll 4
-        for (uint32_t q = 0; q < len; ++q) acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[q]), g(pc[q])));
+        // unpredicated chunks of 8 then 4 (raw loads first: all in flight, few live
+        // registers), then a predicated tail of <= 3
+        uint32_t q = 0;
+        for (; q + CHUNK <= len; q += CHUNK) row_chunk<C, CHUNK>(acc, pv + q, pc + q, g);
+        if (CHUNK > 4 && q + 4 <= len) {
+          row_chunk<C, 4>(acc, pv + q, pc + q, g);
+          q += 4;
+        }
+        {
+          typename Gather::Raw xs[3];
+#pragma unroll
+          for (int u = 0; u < 3; ++u)
+            if (q + u < len) xs[u] = g.load(pc[q + u]);
+#pragma unroll
+          for (int u = 0; u < 3; ++u)
+            if (q + u < len) acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[q + u]), g.value(xs[u])));
+        }
         e.row(row, acc);
       }
     } else if (tid == 0) {
       T_<C> acc = Ar<C>::zero();
-      for (uint32_t k = k0; k < k1; ++k) acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vals[k]), g(A.ci[k])));
+      for (uint32_t k = k0; k < k1; ++k)
+        acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vals[k]), g.value(g.load(A.ci[k]))));
       e.row(r0, acc);
     }
     __syncthreads();
@@ -124,24 +157,33 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
 }
 
 // ---- gathers ----------------------------------------------------------------------
+// Two phases so a chunk of loads can be in flight with few live registers:
+// load(c) issues the raw global load, value(raw) turns it into the operand at C.
 // x[c] stored at PX, widened to C
 template <int PX, int C>
 struct GatherPlain {
+  using Raw = T_<PX>;
   const void* x;
-  __device__ __forceinline__ T_<C> operator()(uint32_t c) const { return cvt<C>(ldg<PX>(x, c)); }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return ldg<PX>(x, c); }
+  __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(r); }
 };
 
 // same, for a vector written earlier in the same (cooperative) kernel
 template <int PX, int C>
 struct GatherCG {
+  using Raw = T_<PX>;
   const void* x;
-  __device__ __forceinline__ T_<C> operator()(uint32_t c) const { return cvt<C>(ldcg<PX>(x, c)); }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return ldcg<PX>(x, c); }
+  __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(r); }
 };
 
 // ---- epilogues --------------------------------------------------------------------
+// Epilogue contract: prefetch(i) is called for the thread's row before the tile
+// lands (issue independent loads there), row(i, acc) after its sum is complete.
 template <int C, int PY>
 struct EpiStore {
   void* y;
+  __device__ __forceinline__ void prefetch(uint32_t) {}
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) { st<PY>(y, i, cvt<PY>(acc)); }
 };
 
