@@ -26,7 +26,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libf3rg.so")
+# F3RG_LIB selects a tuning-sweep build (lib/variants/); default is the product library
+LIB_PATH = os.environ.get("F3RG_LIB") or os.path.join(_HERE, "lib", "libf3rg.so")
 
 
 # ---------------------------------------------------------------- errors (errors.hpp)

@@ -66,7 +66,22 @@ def _run(cmd, log=None):
     return r
 
 
-def build_lib(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
+def build_lib(force: bool = False, jobs: int = 8, verbose: bool = False, defines=(), name: str = "") -> str:
+    """Builds lib/libf3rg.so, or (tuning sweeps) lib/variants/libf3rg_<name>.so with
+    extra -D defines (F3RG_TILE_SCALE, F3RG_STAGES, F3RG_CHUNK)."""
+    global OBJDIR, LIB
+    saved = (OBJDIR, LIB)
+    if name:
+        OBJDIR = os.path.join(ROOT, "build", "obj_" + name)
+        LIB = os.path.join(LIBDIR, "variants", f"libf3rg_{name}.so")
+        os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    try:
+        return _build_lib(force, jobs, verbose, [f"-D{d}" for d in defines])
+    finally:
+        OBJDIR, LIB = saved
+
+
+def _build_lib(force, jobs, verbose, dflags):
     os.makedirs(LIBDIR, exist_ok=True)
     os.makedirs(OBJDIR, exist_ok=True)
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
@@ -79,9 +94,9 @@ def build_lib(force: bool = False, jobs: int = 8, verbose: bool = False) -> str:
         if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), hdr_time):
             continue
         if src.endswith(".cu"):
-            cmd = [NVCC] + NVCC_FLAGS + ["-c", path, "-o", obj]
+            cmd = [NVCC] + NVCC_FLAGS + dflags + ["-c", path, "-o", obj]
         else:
-            cmd = [CXX] + CXX_FLAGS + _gomp_flags() + ["-c", path, "-o", obj]
+            cmd = [CXX] + CXX_FLAGS + dflags + _gomp_flags() + ["-c", path, "-o", obj]
         jobs_list.append((cmd, obj + ".log"))
     if jobs_list:
         with cf.ThreadPoolExecutor(max_workers=jobs) as ex:

@@ -56,14 +56,16 @@ struct EpiStep {
   T_<PW> w0, wk;
   const void* zk;  // materialised z_k (when not on the fly)
   void* out;
-  T_<PW> vi, zi;
+  T_<PV> vraw;  // raw loads only in prefetch: their latency hides behind the row sum
+  T_<PW> zi;
   __device__ __forceinline__ void prefetch(uint32_t i) {
-    vi = rhs(i);
+    vraw = rhs.raw(i);
     if constexpr (!Z1_ON_THE_FLY) zi = ldcg<PW>(zk, i);
   }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     using A = Ar<PW>;
     const T_<PW> s = cvt<PW>(acc);
+    const T_<PW> vi = rhs.apply(vraw);
     const T_<PW> r = A::add(vi, A::neg(s));  // add_scaled(v, -1, s): C = wp, -1*s exact
     if constexpr (Z1_ON_THE_FLY) zi = A::add(A::mul(w0, vi), A::zero());
     st<PW>(out, i, A::add(A::mul(wk, r), zi));
@@ -76,10 +78,15 @@ struct EpiDotsRs {
   RhsView<PV, PW> rhs;
   const void* R;  // p = r (nullptr: r = v)
   T_<CD> num, den;
-  T_<PW> r;
-  __device__ __forceinline__ void prefetch(uint32_t i) { r = R ? ldcg<PW>(R, i) : rhs(i); }
+  T_<PW> rr;
+  T_<PV> vraw;
+  __device__ __forceinline__ void prefetch(uint32_t i) {
+    if (R) rr = ldcg<PW>(R, i);
+    else vraw = rhs.raw(i);
+  }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> s = cvt<PW>(acc);
+    const T_<PW> r = R ? rr : rhs.apply(vraw);
     num = Ar<CD>::add(num, Ar<CD>::mul(cvt<CD>(r), cvt<CD>(s)));
     den = Ar<CD>::add(den, Ar<CD>::mul(cvt<CD>(s), cvt<CD>(s)));
   }
@@ -90,11 +97,11 @@ template <int PV, int PW, int C>
 struct EpiResid {
   RhsView<PV, PW> rhs;
   void* R;
-  T_<PW> vi;
-  __device__ __forceinline__ void prefetch(uint32_t i) { vi = rhs(i); }
+  T_<PV> vraw;
+  __device__ __forceinline__ void prefetch(uint32_t i) { vraw = rhs.raw(i); }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> s = cvt<PW>(acc);
-    st<PW>(R, i, Ar<PW>::add(vi, Ar<PW>::neg(s)));
+    st<PW>(R, i, Ar<PW>::add(rhs.apply(vraw), Ar<PW>::neg(s)));
   }
 };
 
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, con
         grid_barrier(bar_count, bar_gen);
       }
       {
-        EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? RS->R : nullptr, Ar<CD>::zero(), Ar<CD>::zero(), {}};
+        EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? RS->R : nullptr, Ar<CD>::zero(), Ar<CD>::zero(), {}, {}};
         if (k == 0) {
           struct GatherRhs {
             using Raw = T_<PV>;

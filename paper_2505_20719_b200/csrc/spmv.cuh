@@ -25,11 +25,18 @@ namespace f3rg {
 
 template <int PA>
 struct TileCfg {
+#ifndef F3RG_TILE_SCALE
+#define F3RG_TILE_SCALE 8
+#endif
+#ifndef F3RG_STAGES
+#define F3RG_STAGES 2
+#endif
   static constexpr int NT = 256;                                      // threads = max rows per tile
   static constexpr int SA = (int)sizeof(T_<PA>);
-  static constexpr int TNNZ = PA == P16 ? 8192 : PA == P32 ? 6144 : 4096;  // ~48 KB of (val, col) per stage
+  // ~48 KB of (val, col) per stage at scale 8 (TNNZ multiples of 1024)
+  static constexpr int TNNZ = (PA == P16 ? 1024 : PA == P32 ? 768 : 512) * F3RG_TILE_SCALE;
   static constexpr int VAL = 16 / SA;                                 // elements per 16 B
-  static constexpr int STAGES = 2;
+  static constexpr int STAGES = F3RG_STAGES;
   static constexpr int VAL_BYTES = ((TNNZ + 2 * VAL) * SA + 15) / 16 * 16;
   static constexpr int COL_BYTES = (TNNZ + 8) * 4;
   static constexpr int RP_BYTES = (NT + 12) * 4;
@@ -93,7 +100,10 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   }
   // gathers are issued CHUNK at a time (independent loads in flight per thread)
   // before the sequential, order-preserving accumulation consumes them
-  constexpr int CHUNK = 8;
+#ifndef F3RG_CHUNK
+#define F3RG_CHUNK 8
+#endif
+  constexpr int CHUNK = F3RG_CHUNK;
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < T.ntiles; t += G, ++it) {
     const int s = (int)(it % ST);
@@ -121,10 +131,7 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
         // registers), then a predicated tail of <= 3
         uint32_t q = 0;
         for (; q + CHUNK <= len; q += CHUNK) row_chunk<C, CHUNK>(acc, pv + q, pc + q, g);
-        if (CHUNK > 4 && q + 4 <= len) {
-          row_chunk<C, 4>(acc, pv + q, pc + q, g);
-          q += 4;
-        }
+        for (; q + 4 <= len; q += 4) row_chunk<C, 4>(acc, pv + q, pc + q, g);
         {
           typename Gather::Raw xs[3];
 #pragma unroll

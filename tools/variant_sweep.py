@@ -1,0 +1,67 @@
+"""Tuning sweep of the tile pipeline (stages x tile size x gather chunk).
+
+Here (CPU):   python tools/variant_sweep.py build     -> lib/variants/libf3rg_<name>.so
+On the GPU:   python tools/variant_sweep.py run       -> one line per variant: time per
+              config-2 solve (graph mode) and per-kernel GB/s (eager profile)
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+VARIANTS = {
+    "s2x8_c8": ["F3RG_STAGES=2", "F3RG_TILE_SCALE=8", "F3RG_CHUNK=8"],
+    "s3x5_c8": ["F3RG_STAGES=3", "F3RG_TILE_SCALE=5", "F3RG_CHUNK=8"],
+    "s4x4_c8": ["F3RG_STAGES=4", "F3RG_TILE_SCALE=4", "F3RG_CHUNK=8"],
+    "s2x8_c16": ["F3RG_STAGES=2", "F3RG_TILE_SCALE=8", "F3RG_CHUNK=16"],
+    "s3x5_c16": ["F3RG_STAGES=3", "F3RG_TILE_SCALE=5", "F3RG_CHUNK=16"],
+    "s2x4_c8": ["F3RG_STAGES=2", "F3RG_TILE_SCALE=4", "F3RG_CHUNK=8"],
+}
+
+CHILD = r"""
+import sys, time, json, torch
+sys.path.insert(0, %r)
+import paper_2505_20719_b200 as f
+from paper_2505_20719_b200 import problems
+p = problems.problem(2)
+reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
+s = f.build(f.parse_solver_spec("F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > identity"), reps, f.IdentityPrecond(p.n))
+b = torch.from_numpy(p.b).cuda()
+o = f.RunOptions(tol=1e-10)
+for _ in range(2):
+    s.reset(); s.run(b, o)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    s.reset(); r = s.run(b, o)
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+s.set_profile(True); s.reset(); s.run(b, o); s.set_profile(False)
+prof = {k[0]: round(k[3] / k[2] / (k[1] / k[2] * 1e-3) / 1e9) for k in s.profile()}
+tot = {k[0]: round(k[1], 2) for k in s.profile()}
+print(json.dumps({"ms": round(ms, 2), "outer": r.report.outer_iterations, "gbs": prof, "kernel_ms": tot}))
+""" % ROOT
+
+
+def build():
+    from paper_2505_20719_b200 import buildlib
+    for name, defs in VARIANTS.items():
+        buildlib.build_lib(defines=defs, name=name)
+        print("built", name, flush=True)
+
+
+def run():
+    for name in VARIANTS:
+        lib = os.path.join(ROOT, "paper_2505_20719_b200", "lib", "variants", f"libf3rg_{name}.so")
+        env = dict(os.environ, F3RG_LIB=lib)
+        r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
+        line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
+        print(name, line, flush=True)
+
+
+if __name__ == "__main__":
+    {"build": build, "run": run}[sys.argv[1]]()
