@@ -77,13 +77,13 @@ __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint6
 }
 
 // plain y = A x (any precision triple), for the kernel-level entry point
-template <int PA, int PX, int PY>
-__global__ void __launch_bounds__(256, 2) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {
+template <int PA, int PX, int PY, int IDX>
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int C = pmax(PA, PX);
   GatherPlain<PX, C> g{x};
   EpiStore<C, PY> e{y};
-  spmv_tiles<PA, C>(A, T, g, e, smem);
+  spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
 }
 
 }  // namespace f3rg

@@ -213,6 +213,19 @@ __device__ __forceinline__ bool last_block(unsigned* counter) {
   return is_last;
 }
 
+// Light variant for bookkeeping that publishes no data between CTAs: one atomic per
+// CTA after the CTA's work, no fences; the last CTA to arrive returns true.
+__device__ __forceinline__ bool last_block_light(unsigned* counter) {
+  __shared__ bool is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (is_last) *counter = 0u;
+  }
+  __syncthreads();
+  return is_last;
+}
+
 // Reduce partials[G][stride] columns 0..NV-1 over G blocks in a fixed tree;
 // called by one whole block; results (doubles holding C values) in out[] (shared),
 // valid for all threads after the call.

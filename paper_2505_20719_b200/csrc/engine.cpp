@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "launch.hpp"
@@ -74,6 +75,28 @@ DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* 
   // replicas: element-wise RNE demotion on the device (cvt.rn.f32.f64 / cvt.rn.f16.f64)
   F3RG_CUDA(launch_copy(2, 1, Launch{}, val_[2].get(), val_[1].get(), nnz_));
   F3RG_CUDA(launch_copy(2, 0, Launch{}, val_[2].get(), val_[0].get(), nnz_));
+  // D16 column stream when every in-row gap fits 16 bits (F3RG_COLUMNS=u32 forces
+  // the plain u32 stream, for A/B tests)
+  const char* colfmt = std::getenv("F3RG_COLUMNS");
+  bool d16 = !(colfmt && std::string(colfmt) == "u32") && nnz_ > 0;
+  for (uint64_t i = 0; d16 && i < n_; ++i)
+    for (uint32_t k = row_ptr[i] + 1; k < row_ptr[i + 1]; ++k)
+      if (col_idx[k] - col_idx[k - 1] > 65535u) {
+        d16 = false;
+        break;
+      }
+  if (d16) {
+    std::vector<uint16_t> dc(nnz_ + 16, 0);
+    std::vector<uint32_t> fc(n_ + 16, 0);
+    for (uint64_t i = 0; i < n_; ++i) {
+      if (row_ptr[i] < row_ptr[i + 1]) fc[i] = col_idx[row_ptr[i]];
+      for (uint32_t k = row_ptr[i] + 1; k < row_ptr[i + 1]; ++k) dc[k] = (uint16_t)(col_idx[k] - col_idx[k - 1]);
+    }
+    dcol_.alloc(dc.size() * 2);
+    first_.alloc(fc.size() * 4);
+    F3RG_CUDA(cudaMemcpy(dcol_.get(), dc.data(), dc.size() * 2, cudaMemcpyHostToDevice));
+    F3RG_CUDA(cudaMemcpy(first_.get(), fc.data(), fc.size() * 4, cudaMemcpyHostToDevice));
+  }
   std::vector<uint32_t> r0, k0;
   for (int p = 0; p < 3; ++p) {
     build_tiles(n_, row_ptr, tile_max_rows(), tile_max_nnz(p), r0, k0);
@@ -93,6 +116,8 @@ CsrDev DeviceMatrix::csr() const {
   c.rp = rp_.get<const uint32_t>();
   c.ci = ci_.get<const uint32_t>();
   for (int p = 0; p < 3; ++p) c.val[p] = val_[p].get();
+  c.dcol = dcol_.get<const uint16_t>();
+  c.first = first_.get<const uint32_t>();
   return c;
 }
 
@@ -173,6 +198,7 @@ void Solver::build_levels() {
   dead_.alloc(16 * sizeof(int));
   cnt_.alloc(CNT_N * sizeof(unsigned long long));
   partials_.alloc((size_t)max_partial_blocks() * 16 * sizeof(double));
+  dpartials_.alloc((size_t)max_partial_blocks() * 16 * sizeof(double));  // projection partials (k_spmv_dots)
   counter_.alloc(64);
   bar_.alloc(64);
   info_.alloc(sizeof(StepInfo));
@@ -320,6 +346,13 @@ std::vector<Solver::KernelTime> Solver::profile_results() const {
     prof_end(s, name, (double)(bytes)); \
   } while (0)
 
+// bytes one pass over the matrix replica `pa` streams: values, the column stream
+// actually in use (u32, or D16 = u16 deltas + u32 first column per row), row_ptr
+double Solver::mbytes(int pa) const {
+  const double n = (double)n_, nnz = (double)a_->nnz();
+  return nnz * psize(pa) + (a_->d16() ? 2.0 * nnz + 4.0 * n : 4.0 * nnz) + 4.0 * (n + 1);
+}
+
 static std::string kname(const char* base, int a, int b, int c) {
   return std::string(base) + "[" + precision_name(a) + "," + precision_name(b) + "," + precision_name(c) + "]";
 }
@@ -335,7 +368,6 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
   int* dead = dead_.get<int>();
   auto* cnt = cnt_.get<unsigned long long>();
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
-  bool materialized = false;
   if (L.child == 0) {
     if (top) {
       io_host_[j] = IoSlot{vj, sj, zj};
@@ -348,12 +380,11 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
     } else {
       enqueue_fgmres(l + 1, vj, sj, zj, nullptr, s);
     }
-    materialized = true;
   } else if (L.child == 1) {
     Level& R = *lv_[l + 1];
     const TilesDev T = a_->tiles(R.PA);
     PROF(kname("richardson", R.PA, R.W, L.W).c_str(),
-         nnz * (psize(R.PA) + 4) + 4.0 * (n + 1) + (double)n * (psize(L.W) + psize(R.W)),
+         mbytes(R.PA) + (double)n * (psize(L.W) + psize(R.W)),
          launch_richardson(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, vj, sj, zj, n, R.drs, GateH{dead, l + 1}, l + 1,
                            cnt, sync, bar_.get<unsigned>(), bar_.get<unsigned>() + 1, nullptr));
   } else {
@@ -362,16 +393,22 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
   }
   const TilesDev T = a_->tiles(L.PA);
   const int nd = std::min(j + 1, 8);
+  // Deferring the projection reduction to k_cgs (every CTA reduces the partials in
+  // its prologue) measured no better than k_spmv_dots' own last-CTA tail (both
+  // ~6 us on config 2, tools/tile_microbench.cu), so it stays off; the path is kept
+  // for the fused-step kernel.
+  const int defer = 0;
+  int dgrid = 0;
   PROF(kname("spmv_dots", L.PA, L.PZ, L.W).c_str(),
-       nnz * (psize(L.PA) + 4) + 4.0 * (n + 1) + (double)n * (psize(L.PZ) + psize(L.W)) + (double)nd * n * psize(L.W),
-       launch_spmv_dots(L.PA, L.PZ, L.W, Launch{0, s}, a_->csr(), T, zj, L.V.get(), n, j, materialized ? nullptr : sj,
-                        L.dstate, GateH{dead, l + 1}, sync));
+       mbytes(L.PA) + (double)n * (psize(L.PZ) + psize(L.W)) + (double)nd * n * psize(L.W),
+       launch_spmv_dots(L.PA, L.PZ, L.W, Launch{0, s}, a_->csr(), T, zj, L.V.get(), n, j, L.dstate,
+                        GateH{dead, l + 1}, sync, dpartials_.get<double>(), defer, &dgrid));
   for (int k0 = 8; k0 <= j; k0 += 8)
     PROF(kname("multi_dot", L.W, L.W, L.W).c_str(), (double)n * psize(L.W) * (1 + std::min(8, j + 1 - k0)),
          launch_multi_dot(L.W, Launch{0, s}, L.V.get(), n, j, k0, L.dstate, GateH{dead, l + 1}, sync));
   PROF(kname("cgs", L.W, L.W, L.W).c_str(), (double)n * psize(L.W) * (j + 3),
        launch_cgs(L.W, Launch{0, s}, L.V.get(), n, j, L.dstate, dead, GateH{dead, l + 1}, l, top ? 1 : 0, top ? 1 : 0,
-                  top ? info_.get<StepInfo>() : nullptr, sync));
+                  top ? info_.get<StepInfo>() : nullptr, sync, defer ? dpartials_.get<double>() : nullptr, dgrid));
 }
 
 void Solver::enqueue_fgmres(int l, void* src, const double* src_scale, void* dst, const IoSlot* io, cudaStream_t s) {
@@ -382,7 +419,7 @@ void Solver::enqueue_fgmres(int l, void* src, const double* src_scale, void* dst
   auto* cnt = cnt_.get<unsigned long long>();
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
   PROF(kname("level_start", P.W, L.W, L.W).c_str(), (double)n * (2 * psize(P.W) + psize(L.W)),
-       launch_level_start(P.W, L.W, Launch{0, s}, src, src_scale, 1, L.V.get(), n, L.dstate, dead, GateH{dead, l}, l,
+       launch_level_start(P.W, L.W, Launch{0, s}, src, src_scale, 0, L.V.get(), n, L.dstate, dead, GateH{dead, l}, l,
                           cnt, sync, io));
   for (int j = 0; j < L.spec.m; ++j) enqueue_child_step(l, j, s, false);
   PROF(kname("level_finish", L.PZ, L.W, L.W).c_str(), (double)n * (L.spec.m * psize(L.PZ) + psize(L.W)),
@@ -421,7 +458,7 @@ double Solver::true_rel(const double* b, double bnorm, cudaStream_t s) {
   Level& top = *lv_[0];
   const double nnz = (double)a_->nnz();
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
-  PROF(kname("residual", 2, top.spec.pv, 2).c_str(), nnz * 12 + 4.0 * (n_ + 1) + (double)n_ * (psize(top.spec.pv) + 16),
+  PROF(kname("residual", 2, top.spec.pv, 2).c_str(), mbytes(2) + (double)n_ * (psize(top.spec.pv) + 16),
        launch_residual(2, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(2), xbuf_.get(), b, rbuf_.get(), nullptr,
                        norm_.get<double>(), sync));
   return read_double(norm_.get<double>(), s) / bnorm;
@@ -498,7 +535,7 @@ Report Solver::run_fgmres_top(const double* b, const RunOptions& opts, cudaStrea
                               GateH{dead, 0}, 0, cnt, sync, nullptr));
     } else {  // r = b - A x
       PROF(kname("residual", top.PA, top.spec.pv, 2).c_str(),
-           nnz * (psize(top.PA) + 4) + 4.0 * (n + 1) + (double)n * (psize(top.spec.pv) + 16),
+           mbytes(top.PA) + (double)n * (psize(top.spec.pv) + 16),
            launch_residual(top.PA, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(top.PA), xbuf_.get(), b,
                            top.V.get(), top.dstate, nullptr, sync));
     }
@@ -580,13 +617,13 @@ Report Solver::run_richardson_top(const double* b, const RunOptions& opts, cudaS
       rep.flag = "capped";
       break;
     }
-    PROF(kname("richardson", top.PA, pv, pv).c_str(), nnz * (psize(top.PA) + 4) + 4.0 * (n + 1) + 2.0 * n * psize(pv),
+    PROF(kname("richardson", top.PA, pv, pv).c_str(), mbytes(top.PA) + 2.0 * n * psize(pv),
          launch_richardson(top.PA, pv, pv, Launch{0, s}, a_->csr(), a_->tiles(top.PA), rbuf_.get(), nullptr,
                            zbuf_.get(), n, top.drs, GateH{dead, 0}, 0, cnt, sync, bar_.get<unsigned>(),
                            bar_.get<unsigned>() + 1, nullptr));
     F3RG_CUDA(launch_axpy(pv, pv, Launch{0, s}, 1.0, zbuf_.get(), xbuf_.get(), n));
     rep.outer_iterations += 1;
-    PROF(kname("residual", top.PA, pv, pv).c_str(), nnz * (psize(top.PA) + 4) + 4.0 * (n + 1) + (double)n * (2 * psize(pv) + 8),
+    PROF(kname("residual", top.PA, pv, pv).c_str(), mbytes(top.PA) + (double)n * (2 * psize(pv) + 8),
          launch_residual(top.PA, pv, pv, Launch{0, s}, a_->csr(), a_->tiles(top.PA), xbuf_.get(), b, rbuf_.get(),
                          nullptr, norm_.get<double>(), sync));
     const double rel = read_double(norm_.get<double>(), s) / bnorm;

@@ -120,10 +120,11 @@ class DeviceMatrix {
   CsrDev csr() const;
   TilesDev tiles(int p) const;
   const void* values(int p) const { return val_[p].get(); }
+  bool d16() const { return dcol_.get() != nullptr; }  // 16-bit delta column stream in use
 
  private:
   uint64_t n_ = 0, nnz_ = 0;
-  DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3];
+  DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_;
   uint32_t ntiles_[3] = {0, 0, 0};
 };
 
@@ -187,6 +188,7 @@ class Solver {
   Report run_fgmres_top(const double* b, const RunOptions& opts, cudaStream_t s, double bnorm, Report rep);
   Report run_richardson_top(const double* b, const RunOptions& opts, cudaStream_t s, double bnorm, Report rep);
   double true_rel(const double* b, double bnorm, cudaStream_t s);
+  double mbytes(int pa) const;
   void prof_begin(cudaStream_t s);
   void prof_end(cudaStream_t s, const char* name, double bytes);
 
@@ -195,7 +197,7 @@ class Solver {
   std::shared_ptr<DeviceMatrix> a_;
   std::vector<std::unique_ptr<Level>> lv_;
   uint64_t n_ = 0;
-  DevBuf dead_, cnt_, partials_, counter_, bar_, info_, io_, norm_, xbuf_, rbuf_, zbuf_;
+  DevBuf dead_, cnt_, partials_, dpartials_, counter_, bar_, info_, io_, norm_, xbuf_, rbuf_, zbuf_;
   StepInfo* info_host_ = nullptr;
   IoSlot* io_host_ = nullptr;
   double* stage_host_ = nullptr;

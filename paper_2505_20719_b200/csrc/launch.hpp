@@ -32,8 +32,6 @@ struct Launch {
 // grid used for streaming (BLAS-1 style) kernels and for tile kernels (per value
 // precision and whether the kernel is the cooperative Richardson one)
 int stream_grid();
-int tile_grid(int pa, uint32_t ntiles);
-int richardson_grid(int pa, int pw, int pv, uint32_t ntiles);
 int max_partial_blocks();
 int sm_count();
 
@@ -43,13 +41,14 @@ cudaError_t launch_level_start(int ps, int pw, Launch l, void* src, const double
                                SyncH sync, const IoSlot* io);
 cudaError_t launch_copy_scaled(int pw, Launch l, void* v, const double* scale, void* z, uint64_t n, GateH gate,
                                unsigned long long* cnt);
+// dots: per-CTA partials (grid x 16 doubles); defer: leave their reduction to k_cgs
 cudaError_t launch_spmv_dots(int pa, int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z,
-                             void* V, uint64_t n, int j, const double* scale_j, LevelState* L, GateH gate,
-                             SyncH sync);
+                             void* V, uint64_t n, int j, LevelState* L, GateH gate, SyncH sync, double* dots,
+                             int defer, int* grid_out);
 cudaError_t launch_multi_dot(int pw, Launch l, const void* V, uint64_t n, int j, int k0, LevelState* L, GateH gate,
                              SyncH sync);
 cudaError_t launch_cgs(int pw, Launch l, void* V, uint64_t n, int j, LevelState* L, int* dead, GateH gate, int level,
-                       int outer, int use_tol, StepInfo* info, SyncH sync);
+                       int outer, int use_tol, StepInfo* info, SyncH sync, const double* dots, int dots_grid);
 cudaError_t launch_level_finish(int pz, int pw, int px, Launch l, const void* Z, uint64_t n, LevelState* L, void* x,
                                 int x_is_zero, GateH gate, int level, unsigned long long* cnt, int count_iterations,
                                 const IoSlot* io);

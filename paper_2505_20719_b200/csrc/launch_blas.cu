@@ -73,20 +73,4 @@ cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* ou
   return cudaGetLastError();
 }
 
-cudaError_t launch_spmv(int pa, int px, int py, Launch l, const CsrDev& A, const TilesDev& T, const void* x, void* y) {
-  with_p(pa, [&](auto PA_) {
-    constexpr int PA = decltype(PA_)::value;
-    with_p(px, [&](auto X) {
-      with_p(py, [&](auto Y) {
-        auto kern = k_spmv<PA, decltype(X)::value, decltype(Y)::value>;
-        static const int occ = occupancy_blocks(kern, TileCfg<PA>::SMEM_BYTES);
-        (void)occ;
-        const int g = l.grid ? l.grid : tile_grid(PA, T.ntiles);
-        kern<<<g, kThreads, TileCfg<PA>::SMEM_BYTES, l.stream>>>(A, T, x, y);
-      });
-    });
-  });
-  return cudaGetLastError();
-}
-
 }  // namespace f3rg

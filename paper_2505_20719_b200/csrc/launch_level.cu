@@ -16,20 +16,6 @@ int sm_count() {
 int stream_grid() { return sm_count() * 8; }
 int max_partial_blocks() { return sm_count() * 8; }
 
-int tile_grid(int pa, uint32_t ntiles) {
-  int occ = 1;
-  with_p(pa, [&](auto A) {
-    constexpr int PA = decltype(A)::value;
-    // all tile kernels of one value precision share the smem footprint; the
-    // plain SpMV instantiation stands in for the family
-    static const int o = occupancy_blocks(k_spmv_dots<PA, PA, PA>, TileCfg<PA>::SMEM_BYTES);
-    occ = o;
-  });
-  long g = (long)occ * sm_count();
-  if (g > (long)ntiles) g = ntiles;
-  return g < 1 ? 1 : (int)g;
-}
-
 cudaError_t launch_level_start(int ps, int pw, Launch l, void* src, const double* src_scale, int writeback, void* dst,
                                uint64_t n, LevelState* L, int* dead, GateH gate, int level, unsigned long long* cnt,
                                SyncH sync, const IoSlot* io) {
@@ -52,25 +38,6 @@ cudaError_t launch_copy_scaled(int pw, Launch l, void* v, const double* scale, v
   return cudaGetLastError();
 }
 
-cudaError_t launch_spmv_dots(int pa, int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z,
-                             void* V, uint64_t n, int j, const double* scale_j, LevelState* L, GateH gate,
-                             SyncH sync) {
-  with_p(pa, [&](auto PA_) {
-    constexpr int PA = decltype(PA_)::value;
-    with_p(pz, [&](auto Z) {
-      with_p(pw, [&](auto W) {
-        auto kern = k_spmv_dots<PA, decltype(Z)::value, decltype(W)::value>;
-        static const int occ = occupancy_blocks(kern, TileCfg<PA>::SMEM_BYTES);
-        (void)occ;
-        const int g = l.grid ? l.grid : tile_grid(PA, T.ntiles);
-        kern<<<g, kThreads, TileCfg<PA>::SMEM_BYTES, l.stream>>>(A, T, z, V, n, j, scale_j, L, to_gate(gate),
-                                                                 to_sync(sync));
-      });
-    });
-  });
-  return cudaGetLastError();
-}
-
 cudaError_t launch_multi_dot(int pw, Launch l, const void* V, uint64_t n, int j, int k0, LevelState* L, GateH gate,
                              SyncH sync) {
   const int g = l.grid ? l.grid : stream_grid();
@@ -81,11 +48,12 @@ cudaError_t launch_multi_dot(int pw, Launch l, const void* V, uint64_t n, int j,
 }
 
 cudaError_t launch_cgs(int pw, Launch l, void* V, uint64_t n, int j, LevelState* L, int* dead, GateH gate, int level,
-                       int outer, int use_tol, StepInfo* info, SyncH sync) {
-  const int g = l.grid ? l.grid : stream_grid();
+                       int outer, int use_tol, StepInfo* info, SyncH sync, const double* dots, int dots_grid) {
+  // 2 CTAs per SM with 16-byte loads measured fastest (tools/tile_microbench.cu)
+  const int g = l.grid ? l.grid : sm_count() * 2;
   with_p(pw, [&](auto W) {
     k_cgs<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(V, n, j, L, dead, to_gate(gate), level, outer, use_tol,
-                                                            info, to_sync(sync));
+                                                            info, to_sync(sync), dots, dots_grid);
   });
   return cudaGetLastError();
 }
@@ -99,23 +67,6 @@ cudaError_t launch_level_finish(int pz, int pw, int px, Launch l, const void* Z,
       with_p(px, [&](auto X) {
         k_level_finish<decltype(PZ)::value, decltype(W)::value, decltype(X)::value><<<g, kThreads, 0, l.stream>>>(
             Z, n, L, x, x_is_zero, to_gate(gate), level, cnt, count_iterations, io);
-      });
-    });
-  });
-  return cudaGetLastError();
-}
-
-cudaError_t launch_residual(int pa, int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
-                            const double* b, void* r, LevelState* L, double* out_norm, SyncH sync) {
-  with_p(pa, [&](auto PA_) {
-    constexpr int PA = decltype(PA_)::value;
-    with_p(px, [&](auto X) {
-      with_p(pw, [&](auto W) {
-        auto kern = k_residual<PA, decltype(X)::value, decltype(W)::value>;
-        static const int occ = occupancy_blocks(kern, TileCfg<PA>::SMEM_BYTES);
-        (void)occ;
-        const int g = l.grid ? l.grid : tile_grid(PA, T.ntiles);
-        kern<<<g, kThreads, TileCfg<PA>::SMEM_BYTES, l.stream>>>(A, T, x, b, r, L, out_norm, to_sync(sync));
       });
     });
   });

@@ -1,0 +1,149 @@
+// launch_tile.cuh -- launchers of every TMA-tiled kernel (SpMV + fused epilogues)
+// for ONE matrix precision PA, instantiated in launch_t16.cu / launch_t32.cu /
+// launch_t64.cu so the heavy template bodies compile in parallel. Only
+// combinations the engine can produce are instantiated (a child level's vector
+// precision never exceeds its parent's); the column format (u32 or D16) follows
+// the matrix.
+#pragma once
+
+#include "blas1.cuh"
+#include "dispatch.cuh"
+#include "levels.cuh"
+#include "richardson.cuh"
+
+namespace f3rg {
+
+template <class K>
+inline int tile_kernel_grid(K kern, int smem, uint32_t ntiles, bool cap_by_tiles) {
+  const int occ = occupancy_blocks(kern, smem);
+  long g = (long)occ * sm_count();
+  if (cap_by_tiles && g > (long)ntiles) g = ntiles;
+  return g < 1 ? 1 : (int)g;
+}
+
+template <int PA>
+cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z, void* V,
+                               uint64_t n, int j, LevelState* L, GateH gate, SyncH sync, double* dots, int defer,
+                               int* grid_out) {
+  cudaError_t err = cudaErrorInvalidValue;
+  auto go = [&](auto IDX_) {
+    constexpr int IDX = decltype(IDX_)::value;
+    constexpr int SM = TileCfg<PA, IDX>::SMEM_BYTES;
+    with_p(pw, [&](auto W) {
+      constexpr int PW = decltype(W)::value;
+      with_p(pz, [&](auto Z) {
+        constexpr int PZ = decltype(Z)::value;
+        if constexpr (PZ <= PW) {
+          auto kern = k_spmv_dots<PA, PZ, PW, IDX>;
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
+          const int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          if (grid_out) *grid_out = g;
+          kern<<<g, kThreads, SM, l.stream>>>(A, T, z, V, n, j, L, to_gate(gate), to_sync(sync), dots, defer);
+          err = cudaGetLastError();
+        }
+      });
+    });
+  };
+  if (A.dcol) go(std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 0>{});
+  return err;
+}
+
+template <int PA>
+cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
+                              const double* b, void* r, LevelState* L, double* out_norm, SyncH sync) {
+  cudaError_t err = cudaErrorInvalidValue;
+  auto go = [&](auto IDX_) {
+    constexpr int IDX = decltype(IDX_)::value;
+    constexpr int SM = TileCfg<PA, IDX>::SMEM_BYTES;
+    with_p(px, [&](auto X) {
+      constexpr int PX = decltype(X)::value;
+      with_p(pw, [&](auto W) {
+        constexpr int PW = decltype(W)::value;
+        if constexpr (PW >= PX) {
+          auto kern = k_residual<PA, PX, PW, IDX>;
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
+          const int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          kern<<<g, kThreads, SM, l.stream>>>(A, T, x, b, r, L, out_norm, to_sync(sync));
+          err = cudaGetLastError();
+        }
+      });
+    });
+  };
+  if (A.dcol) go(std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 0>{});
+  return err;
+}
+
+template <int PA>
+cudaError_t launch_spmv_t(int px, int py, Launch l, const CsrDev& A, const TilesDev& T, const void* x, void* y) {
+  cudaError_t err = cudaErrorInvalidValue;
+  auto go = [&](auto IDX_) {
+    constexpr int IDX = decltype(IDX_)::value;
+    constexpr int SM = TileCfg<PA, IDX>::SMEM_BYTES;
+    with_p(px, [&](auto X) {
+      with_p(py, [&](auto Y) {
+        auto kern = k_spmv<PA, decltype(X)::value, decltype(Y)::value, IDX>;
+        static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
+        const int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+        kern<<<g, kThreads, SM, l.stream>>>(A, T, x, y);
+        err = cudaGetLastError();
+      });
+    });
+  };
+  if (A.dcol) go(std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 0>{});
+  return err;
+}
+
+// cooperative: grid = co-resident capacity (grid barriers on update calls)
+template <int PA>
+cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, const void* v,
+                                const double* v_scale, void* out, uint64_t n, RichState* RS, GateH gate, int level,
+                                unsigned long long* cnt, SyncH sync, unsigned* bar_count, unsigned* bar_gen,
+                                const IoSlot* io) {
+  cudaError_t err = cudaErrorInvalidValue;
+  auto go = [&](auto IDX_) {
+    constexpr int IDX = decltype(IDX_)::value;
+    constexpr int SM = TileCfg<PA, IDX>::SMEM_BYTES;
+    with_p(pv, [&](auto V) {
+      constexpr int PV = decltype(V)::value;
+      with_p(pw, [&](auto W) {
+        constexpr int PW = decltype(W)::value;
+        if constexpr (PW <= PV) {
+          auto kern = k_richardson<PA, PW, PV, IDX>;
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
+          const int g = l.grid ? l.grid : g0;
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(g);
+          cfg.blockDim = dim3(kThreads);
+          cfg.dynamicSmemBytes = SM;
+          cfg.stream = l.stream;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeCooperative;
+          attr[0].val.cooperative = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          err = cudaLaunchKernelEx(&cfg, kern, A, T, v, v_scale, out, n, RS, to_gate(gate), level, cnt, to_sync(sync),
+                                   bar_count, bar_gen, io);
+          if (err == cudaSuccess) err = cudaGetLastError();
+        }
+      });
+    });
+  };
+  if (A.dcol) go(std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 0>{});
+  return err;
+}
+
+#define F3RG_TILE_INSTANTIATE(PA)                                                                                  \
+  template cudaError_t launch_spmv_dots_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*, void*, \
+                                              uint64_t, int, LevelState*, GateH, SyncH, double*, int, int*);       \
+  template cudaError_t launch_residual_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*,         \
+                                             const double*, void*, LevelState*, double*, SyncH);                   \
+  template cudaError_t launch_spmv_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*, void*);     \
+  template cudaError_t launch_richardson_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*,       \
+                                               const double*, void*, uint64_t, RichState*, GateH, int,             \
+                                               unsigned long long*, SyncH, unsigned*, unsigned*, const IoSlot*);
+
+}  // namespace f3rg

@@ -1,0 +1,25 @@
+// launch_tile_decl.hpp -- declarations of the per-precision tiled-kernel launchers
+// (defined in launch_tile.cuh, instantiated in launch_t16/32/64.cu).
+#pragma once
+
+#include "launch.hpp"
+#include "state.hpp"
+
+namespace f3rg {
+
+template <int PA>
+cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z, void* V,
+                               uint64_t n, int j, LevelState* L, GateH gate, SyncH sync, double* dots, int defer,
+                               int* grid_out);
+template <int PA>
+cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
+                              const double* b, void* r, LevelState* L, double* out_norm, SyncH sync);
+template <int PA>
+cudaError_t launch_spmv_t(int px, int py, Launch l, const CsrDev& A, const TilesDev& T, const void* x, void* y);
+template <int PA>
+cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, const void* v,
+                                const double* v_scale, void* out, uint64_t n, RichState* RS, GateH gate, int level,
+                                unsigned long long* cnt, SyncH sync, unsigned* bar_count, unsigned* bar_gen,
+                                const IoSlot* io);
+
+}  // namespace f3rg

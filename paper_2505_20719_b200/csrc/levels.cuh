@@ -138,73 +138,77 @@ __device__ __forceinline__ void static_for(F&& f) {
   }
 }
 
-template <int C, int PW>
+// Basis slots hold UN-normalised vectors; slot k's normalisation factor
+// s_k = fl_W(1/||w_k||) (reference scale_in_place, src/fgmres.cpp:88-92) lives in
+// L->scale[k] and every consumer forms v_k(i) = fl_W(s_k * w_k(i)) in registers --
+// bit-identical to the reference's materialised v_k, without a write-back pass.
+template <int C, int PW, int ND>
 struct EpiDots {
   void* w;
   void* V;
   uint64_t n;
-  int nd;          // number of projections computed here
-  int j;           // v_j may need normalising + write-back
-  T_<PW> sj;       // its scale
-  bool scale_j;
-  Reg8<T_<PW>> d;
-  Reg8<T_<PW>> vk;  // prefetched v_k(i), k < nd
-  T_<PW> vjr;       // prefetched raw v_j(i) when j >= 8
+  T_<PW> sk[ND];  // s_k
+  T_<PW> d[ND];   // partial (w, v_k)
+  T_<PW> vk[ND];  // prefetched raw w_k(i)
   __device__ __forceinline__ void prefetch(uint32_t i) {
-    static_for<0, 8>([&](auto K) {
-      vk.template at<K>() = K < nd ? ld<PW>(V, (uint64_t)K * n + i) : Ar<PW>::zero();
-    });
-    if (scale_j && j >= 8) vjr = ld<PW>(V, (uint64_t)j * n + i);
+#pragma unroll
+    for (int k = 0; k < ND; ++k) vk[k] = ld<PW>(V, (uint64_t)k * n + i);
   }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> wi = cvt<PW>(acc);
-    static_for<0, 8>([&](auto K) {
-      if (K < nd) {
-        const bool sk = scale_j && K == j;  // normalise v_j row-locally, write it back
-        T_<PW> v = vk.template at<K>();
-        if (sk) {
-          v = Ar<PW>::mul(sj, v);
-          st<PW>(V, (uint64_t)j * n + i, v);
-        }
-        d.template at<K>() = Ar<PW>::add(d.template at<K>(), Ar<PW>::mul(wi, v));
-      }
-    });
-    if (scale_j && j >= 8) st<PW>(V, (uint64_t)j * n + i, Ar<PW>::mul(sj, vjr));
+#pragma unroll
+    for (int k = 0; k < ND; ++k) d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, Ar<PW>::mul(sk[k], vk[k])));
     st<PW>(w, i, wi);
   }
 };
 
-template <int PA, int PZ, int PW>
-__global__ void __launch_bounds__(256, 2) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t n, int j,
-                                                   const double* scale_j, LevelState* L, Gate gate, Sync sync) {
+template <int PA, int PZ, int PW, int ND, int IDX>
+__device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& T, const void* z, void* V, uint64_t n,
+                                               int j, LevelState* L, Sync& sync, double* dots, int defer,
+                                               uint8_t* smem, double* scratch, double* res) {
+  constexpr int C = pmax(PA, PW);
+  GatherPlain<PZ, C> g{z};
+  EpiDots<C, PW, ND> e;
+  e.w = static_cast<uint8_t*>(V) + (size_t)(j + 1) * n * sizeof(T_<PW>);
+  e.V = V;
+  e.n = n;
+#pragma unroll
+  for (int k = 0; k < ND; ++k) e.d[k] = Ar<PW>::zero(), e.sk[k] = cvt<PW>(L->scale[k]);
+  spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
+  T_<PW> dd[ND];
+#pragma unroll
+  for (int k = 0; k < ND; ++k) dd[k] = e.d[k];
+  block_sum<PW, ND>(dd, scratch);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 8; ++k) dots[(size_t)blockIdx.x * kMaxPart + k] = k < ND ? Ar<PW>::wide(dd[k]) : 0.0;
+  if (defer) return;
+  if (!last_block(sync.counter)) return;
+  reduce_partials<PW, ND>(dots, gridDim.x, kMaxPart, res, scratch);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < ND; ++k) L->H[(size_t)j * (L->m + 1) + k] = res[k];
+}
+
+// w = A z (rounded to W) fused with the projections h_k = (w, v_k), k < min(j+1, 8)
+// (the projection count is a compile-time parameter of the epilogue: runtime
+// predication there cost ~140 instructions per row). defer != 0: only per-CTA
+// partials are written (to `dots`); the following k_cgs reduces them.
+template <int PA, int PZ, int PW, int IDX>
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t n, int j,
+                                                   LevelState* L, Gate gate, Sync sync, double* dots, int defer) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double res[8];
   if (gate.closed()) return;
-  constexpr int C = pmax(PA, PW);
-  GatherPlain<PZ, C> g{z};
-  EpiDots<C, PW> e;
-  e.w = static_cast<uint8_t*>(V) + (size_t)(j + 1) * n * sizeof(T_<PW>);
-  e.V = V;
-  e.n = n;
-  e.nd = j + 1 < 8 ? j + 1 : 8;
-  e.j = j;
-  e.scale_j = scale_j != nullptr;
-  e.sj = scale_j ? cvt<PW>(*scale_j) : Ar<PW>::one();
-  static_for<0, 8>([&](auto K) { e.d.template at<K>() = Ar<PW>::zero(); });
-  spmv_tiles<PA, C>(A, T, g, e, smem);
-  T_<PW> dd[8];
-  static_for<0, 8>([&](auto K) { dd[K] = e.d.template at<K>(); });
-  block_sum<PW, 8>(dd, scratch);
-  if (threadIdx.x == 0)
-    for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(dd[k]);
-  if (!last_block(sync.counter)) return;
-  reduce_partials<PW, 8>(sync.partials, gridDim.x, kMaxPart, res, scratch);
-  if (threadIdx.x == 0)
-    for (int k = 0; k < e.nd; ++k) L->H[(size_t)j * (L->m + 1) + k] = res[k];
+  switch (j + 1 < 8 ? j + 1 : 8) {
+#define F3RG_ND(K) \
+  case K: spmv_dots_body<PA, PZ, PW, K, IDX>(A, T, z, V, n, j, L, sync, dots, defer, smem, scratch, res); break;
+    F3RG_ND(1) F3RG_ND(2) F3RG_ND(3) F3RG_ND(4) F3RG_ND(5) F3RG_ND(6) F3RG_ND(7)
+    default: spmv_dots_body<PA, PZ, PW, 8, IDX>(A, T, z, V, n, j, L, sync, dots, defer, smem, scratch, res);
+#undef F3RG_ND
+  }
 }
 
-// remaining projections h_i, i in [k0, min(k0+8, j+1)), for long outer cycles
+// remaining projections h_k, k in [k0, min(k0+8, j+1)), for long outer cycles
 template <int PW>
 __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, int j, int k0, LevelState* L,
                                                    Gate gate, Sync sync) {
@@ -212,15 +216,19 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, in
   __shared__ double res[8];
   if (gate.closed()) return;
   const int nd = (j + 1 - k0) < 8 ? (j + 1 - k0) : 8;
-  T_<PW> d[8];
+  T_<PW> d[8], s[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) d[k] = Ar<PW>::zero();
+  for (int k = 0; k < 8; ++k) {
+    d[k] = Ar<PW>::zero();
+    s[k] = k < nd ? cvt<PW>(L->scale[k0 + k]) : Ar<PW>::zero();
+  }
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const T_<PW> wi = ld<PW>(V, (uint64_t)(j + 1) * n + i);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (k < nd) d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, ld<PW>(V, (uint64_t)(k0 + k) * n + i)));
+      if (k < nd)
+        d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, Ar<PW>::mul(s[k], ld<PW>(V, (uint64_t)(k0 + k) * n + i))));
   }
   block_sum<PW, 8>(d, scratch);
   if (threadIdx.x == 0)
@@ -231,44 +239,102 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, in
     for (int k = 0; k < nd; ++k) L->H[(size_t)j * (L->m + 1) + k0 + k] = res[k];
 }
 
-
 // ------------------------------------------------------------------------------
-// CGS subtraction + norm + Givens (src/fgmres.cpp:74-129). `outer` levels never set
-// their dead flag (the host decides) and report through `info`.
+// CGS subtraction + norm + Givens (src/fgmres.cpp:74-129). With dots != nullptr the
+// projections are first reduced from k_spmv_dots' per-CTA partials (every CTA in
+// the same fixed order -> identical h in all CTAs; CTA 0 records the H column).
+// `outer` levels never set their dead flag (the host decides) and report through
+// `info`.
 template <int PW>
 __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelState* L, int* dead, Gate gate,
-                                             int level, int outer, int use_tol, StepInfo* info, Sync sync) {
+                                             int level, int outer, int use_tol, StepInfo* info, Sync sync,
+                                             const double* dots, int dots_G) {
   __shared__ double scratch[64];
   __shared__ double hs[128];
-  __shared__ double tot[1];
+  __shared__ double tot[8];
   if (gate.closed()) return;
   using A = Ar<PW>;
   const int m1 = L->m + 1;
   double* h = L->H + (size_t)j * m1;
   const int nh = j + 1 <= 128 ? j + 1 : 128;
-  for (int k = threadIdx.x; k < nh; k += blockDim.x) hs[k] = -h[k];
-  __syncthreads();
+  // the projections: reduced here from k_spmv_dots' partials (deferred) or read
+  // from H; called after each thread has issued its first streaming loads so the
+  // reduction's latency hides under them
+  auto get_h = [&]() {
+    if (dots) {  // j + 1 <= 8 here
+      reduce_partials<PW, 8>(dots, dots_G, kMaxPart, tot, scratch);
+      for (int k = threadIdx.x; k < nh; k += blockDim.x) hs[k] = -tot[k];
+      if (blockIdx.x == 0 && threadIdx.x < nh) h[threadIdx.x] = tot[threadIdx.x];
+    } else {
+      for (int k = threadIdx.x; k < nh; k += blockDim.x) hs[k] = -h[k];
+    }
+    __syncthreads();
+  };
   T_<PW> acc[1] = {A::zero()};
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   T_<PW>* w = static_cast<T_<PW>*>(V) + (size_t)(j + 1) * n;
-  // the first <= 8 coefficients live in registers and the loop is specialised on
-  // their count (uniform per launch): no per-element predicates or conversions
+  // the first <= 8 coefficients and scales live in registers and the loop is
+  // specialised on their count (uniform per launch); 16-byte vector loads when the
+  // slots are 16-byte aligned (n a multiple of the vector width)
   auto body = [&](auto NJ_) {
     constexpr int NJ = decltype(NJ_)::value;
-    T_<PW> a[NJ];
+    constexpr int VE = 16 / (int)sizeof(T_<PW>);
+    T_<PW> a[NJ], sc[NJ];
+    auto update = [&](uint64_t i, T_<PW> wi, const T_<PW>* vv) {
 #pragma unroll
-    for (int u = 0; u < NJ; ++u) a[u] = cvt<PW>(hs[u]);
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-      T_<PW> vv[NJ];
-#pragma unroll
-      for (int u = 0; u < NJ; ++u) vv[u] = ld<PW>(V, (uint64_t)u * n + i);
-      T_<PW> wi = w[i];
-#pragma unroll
-      for (int u = 0; u < NJ; ++u) wi = A::add(A::mul(a[u], vv[u]), wi);
-      for (int k = NJ; k <= j; ++k)  // long outer cycles only
-        wi = A::add(A::mul(k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]), ld<PW>(V, (uint64_t)k * n + i)), wi);
-      w[i] = wi;
+      for (int u = 0; u < NJ; ++u) wi = A::add(A::mul(a[u], A::mul(sc[u], vv[u])), wi);
+      for (int k = NJ; k <= j; ++k) {  // long outer cycles only
+        const T_<PW> v = A::mul(cvt<PW>(L->scale[k]), ld<PW>(V, (uint64_t)k * n + i));
+        wi = A::add(A::mul(k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]), v), wi);
+      }
       acc[0] = A::add(acc[0], A::mul(wi, wi));
+      return wi;
+    };
+    auto coefficients = [&]() {
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) a[u] = cvt<PW>(hs[u]), sc[u] = cvt<PW>(L->scale[u]);
+    };
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (n % VE == 0) {
+      const uint64_t nv = n / VE;
+      const uint4* w4 = reinterpret_cast<const uint4*>(w);
+      uint4 raw[NJ], wr = {0u, 0u, 0u, 0u};
+      auto load = [&](uint64_t e) {
+#pragma unroll
+        for (int u = 0; u < NJ; ++u)
+          raw[u] = reinterpret_cast<const uint4*>(static_cast<const T_<PW>*>(V) + (uint64_t)u * n)[e];
+        wr = w4[e];
+      };
+      uint64_t e = tid;
+      if (e < nv) load(e);
+      get_h();
+      coefficients();
+      for (; e < nv;) {
+        T_<PW> wv[VE];
+        memcpy(wv, &wr, 16);
+#pragma unroll
+        for (int l = 0; l < VE; ++l) {
+          T_<PW> vv[NJ];
+#pragma unroll
+          for (int u = 0; u < NJ; ++u)
+            memcpy(&vv[u], reinterpret_cast<const char*>(&raw[u]) + l * sizeof(T_<PW>), sizeof(T_<PW>));
+          wv[l] = update(e * VE + l, wv[l], vv);
+        }
+        uint4 out;
+        memcpy(&out, wv, 16);
+        reinterpret_cast<uint4*>(w)[e] = out;
+        e += stride;
+        if (e < nv) load(e);
+      }
+    } else {
+      get_h();
+      coefficients();
+      for (uint64_t i = tid; i < n; i += stride) {
+        T_<PW> vv[NJ];
+#pragma unroll
+        for (int u = 0; u < NJ; ++u) vv[u] = ld<PW>(V, (uint64_t)u * n + i);
+        w[i] = update(i, w[i], vv);
+      }
     }
   };
   switch (j + 1 < 8 ? j + 1 : 8) {
@@ -428,8 +494,8 @@ struct EpiResidual {
 
 // result: L (if non-null) gets the Arnoldi start like k_level_start; norm2 (W) is
 // also written to *out_norm.
-template <int PA, int PX, int PW>
-__global__ void __launch_bounds__(256, 2) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
+template <int PA, int PX, int PW, int IDX>
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
                                                   LevelState* L, double* out_norm, Sync sync) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
@@ -437,7 +503,7 @@ __global__ void __launch_bounds__(256, 2) k_residual(CsrDev A, TilesDev T, const
   constexpr int C = pmax(PA, PX);
   GatherPlain<PX, C> g{x};
   EpiResidual<C, PW> e{b, r, Ar<PW>::zero(), 0.0};
-  spmv_tiles<PA, C>(A, T, g, e, smem);
+  spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
   T_<PW> acc[1] = {e.acc};
   block_sum<PW, 1>(acc, scratch);
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);

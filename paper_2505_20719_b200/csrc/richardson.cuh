@@ -105,8 +105,8 @@ struct EpiResid {
   }
 };
 
-template <int PA, int PW, int PV>
-__global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
+template <int PA, int PW, int PV, int IDX>
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
                                                     void* out, uint64_t n, RichState* RS, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, unsigned* bar_count,
                                                     unsigned* bar_gen, const IoSlot* io) {
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, con
       {
         GatherZ1<PV, PW, C> g{rhs, w0};
         EpiStep<PV, PW, C, true> e{rhs, w0, cvt<PW>(RS->omegas[1]), nullptr, m == 2 ? out : RS->Za, {}, {}};
-        spmv_tiles<PA, C>(A, T, g, e, smem);
+        spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
       }
       for (int k = 2; k < m; ++k) {
         grid_barrier(bar_count, bar_gen);
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, con
         void* zn = (k + 1 == m) ? out : ((k % 2 == 0) ? RS->Zb : RS->Za);
         GatherCG<PW, C> g{zk};
         EpiStep<PV, PW, C, false> e{rhs, w0, cvt<PW>(RS->omegas[k]), zk, zn, {}, {}};
-        spmv_tiles<PA, C>(A, T, g, e, smem);
+        spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
       }
     }
   } else {
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, con
       if (k > 0) {
         GatherCG<PW, C> g{RS->Za};
         EpiResid<PV, PW, C> e{rhs, RS->R, {}};
-        spmv_tiles<PA, C>(A, T, g, e, smem);
+        spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
         grid_barrier(bar_count, bar_gen);
       }
       {
@@ -168,10 +168,10 @@ __global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, con
             __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
             __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
           } g{rhs};
-          spmv_tiles<PA, C>(A, T, g, e, smem);
+          spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
         } else {
           GatherCG<PW, C> g{RS->R};
-          spmv_tiles<PA, C>(A, T, g, e, smem);
+          spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
         }
         T_<CD> acc[2] = {e.num, e.den};
         block_sum<CD, 2>(acc, scratch);
@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(256, 2) k_richardson(CsrDev A, TilesDev T, con
     }
   }
   // bookkeeping once every CTA is done reading the state
-  if (!last_block(sync.counter)) return;
+  // update calls publish wused/wupd across CTAs (full fence); plain calls only count
+  if (!(update ? last_block(sync.counter) : last_block_light(sync.counter))) return;
   if (threadIdx.x == 0) {
     if (update) {
       const double l = (double)(call / RS->cycle - 1ull);

@@ -210,7 +210,7 @@ uint32_t tile_max_rows() { return 256; }
 #define F3RG_TILE_SCALE 8
 #endif
 // = TileCfg<PA>::TNNZ (spmv.cuh)
-uint32_t tile_max_nnz(int pa) { return (pa == 0 ? 1024u : pa == 1 ? 768u : 512u) * F3RG_TILE_SCALE; }
+uint32_t tile_max_nnz(int pa) { return pa == 0 ? 7168u : pa == 1 ? 6912u : 4096u; }
 
 void build_tiles(uint64_t n, const uint32_t* rp, uint32_t max_rows, uint32_t max_nnz, std::vector<uint32_t>& r0,
                  std::vector<uint32_t>& k0) {

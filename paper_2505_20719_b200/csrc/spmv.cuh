@@ -11,59 +11,70 @@
 // coalesced (the naive one-thread-per-row load pattern would be L1-wavefront bound
 // on B200).
 //
+// Column stream, IDX = 0: u32 indices (4 B/nnz). IDX = 1 ("D16"): u16 in-row
+// deltas + one u32 first column per row (2 B/nnz + 4 B/row), decoded by a running
+// sum during the (already sequential) row walk -- same columns, same order, a
+// third fewer bytes for an fp16 matrix.
+//
 // Tiles: contiguous row ranges with <= NT rows and <= TNNZ nonzeros (built on the
-// host, tiles.cpp). A row longer than TNNZ gets a tile of its own and is summed
-// straight from global memory by one thread (same order, slow, never hit by the
-// benchmark matrices).
+// host, spec.cpp build_tiles). A row longer than TNNZ gets a tile of its own and is
+// summed straight from global memory by one thread (same order, slow, never hit by
+// the benchmark matrices).
 #pragma once
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "state.hpp"
 
+#ifndef F3RG_TILE_MINB  // tile kernels: min CTAs per SM (register budget)
+#define F3RG_TILE_MINB 3
+#endif
+#ifndef F3RG_D16_STAGES  // pipeline depth of fp16 D16 tiles
+#define F3RG_D16_STAGES 2
+#endif
+#ifndef F3RG_CHUNK
+#define F3RG_CHUNK 16
+#endif
+
 namespace f3rg {
 
-
-template <int PA>
+template <int PA, int IDX = 0>
 struct TileCfg {
-#ifndef F3RG_TILE_SCALE
-#define F3RG_TILE_SCALE 8
-#endif
-#ifndef F3RG_STAGES
-#define F3RG_STAGES 2
-#endif
-  static constexpr int NT = 256;                                      // threads = max rows per tile
+  static constexpr int NT = 256;  // threads = max rows per tile
   static constexpr int SA = (int)sizeof(T_<PA>);
-  // ~48 KB of (val, col) per stage at scale 8 (TNNZ multiples of 1024)
-  static constexpr int TNNZ = (PA == P16 ? 1024 : PA == P32 ? 768 : 512) * F3RG_TILE_SCALE;
-  static constexpr int VAL = 16 / SA;                                 // elements per 16 B
-  static constexpr int STAGES = F3RG_STAGES;
+  // Two CTAs per SM (<= ~113 KB of shared memory each). The tile table is shared by
+  // both column formats, so TNNZ depends on PA only: fp16 / fp32 tiles hold 256
+  // rows of a 27-point stencil, fp64 ones 151. The smaller D16 fp16 tiles afford a
+  // third stage -- with 2 the next tile's load gets only one compute period to land,
+  // which bounded the kernel below HBM bandwidth once the column bytes shrank.
+  static constexpr int TNNZ = PA == P16 ? 7168 : PA == P32 ? 6912 : 4096;
+  static constexpr int VAL = 16 / SA;  // value elements per 16 B
+  static constexpr int CS = IDX ? 2 : 4;
+  static constexpr int CAL = 16 / CS;  // column elements per 16 B
+  static constexpr int STAGES = (PA == P16 && IDX == 1) ? F3RG_D16_STAGES : 2;
   static constexpr int VAL_BYTES = ((TNNZ + 2 * VAL) * SA + 15) / 16 * 16;
-  static constexpr int COL_BYTES = (TNNZ + 8) * 4;
+  static constexpr int COL_BYTES = ((TNNZ + 2 * CAL) * CS + 15) / 16 * 16;
   static constexpr int RP_BYTES = (NT + 12) * 4;
-  static constexpr int STAGE_BYTES = VAL_BYTES + COL_BYTES + RP_BYTES;
+  static constexpr int FIRST_BYTES = IDX ? (NT + 12) * 4 : 0;
+  static constexpr int STAGE_BYTES = VAL_BYTES + COL_BYTES + RP_BYTES + FIRST_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 64;
 };
-
-// N consecutive entries of one row: issue the N gathers, then accumulate in order.
-template <int C, int N, class TA, class Gather>
-__device__ __forceinline__ void row_chunk(T_<C>& acc, const TA* pv, const uint32_t* pc, const Gather& g) {
-  typename Gather::Raw xs[N];
-#pragma unroll
-  for (int u = 0; u < N; ++u) xs[u] = g.load(pc[u]);
-#pragma unroll
-  for (int u = 0; u < N; ++u) acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[u]), g.value(xs[u])));
-}
 
 // Streams all tiles owned by this CTA (tile t = blockIdx.x + i*gridDim.x) through
 // shared memory and calls epi.row(row, acc) for every row with acc at
 // C = promote(PA, gather precision).
-template <int PA, int C, class Gather, class Epi>
+template <int PA, int C, int IDX, class Gather, class Epi>
 __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
-  using Cfg = TileCfg<PA>;
+  using Cfg = TileCfg<PA, IDX>;
   using TA = T_<PA>;
-  constexpr int NT = Cfg::NT, ST = Cfg::STAGES, VAL = Cfg::VAL;
+  using TC = typename std::conditional<IDX == 1, uint16_t, uint32_t>::type;
+  constexpr int ST = Cfg::STAGES, VAL = Cfg::VAL, CAL = Cfg::CAL;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * Cfg::STAGE_BYTES);
   const TA* vals = static_cast<const TA*>(A.val[PA]);
+  const TC* cols;
+  if constexpr (IDX == 1) cols = A.dcol;
+  else cols = A.ci;
   const uint32_t G = gridDim.x, tid = threadIdx.x;
 
   if (tid == 0) {
@@ -82,14 +93,16 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
       return;
     }
     const uint32_t k0v = k0 & ~(uint32_t)(VAL - 1), k1v = (k1 + VAL - 1) & ~(uint32_t)(VAL - 1);
-    const uint32_t k0c = k0 & ~3u, k1c = (k1 + 3) & ~3u;
+    const uint32_t k0c = k0 & ~(uint32_t)(CAL - 1), k1c = (k1 + CAL - 1) & ~(uint32_t)(CAL - 1);
     const uint32_t r0a = r0 & ~3u, r1a = (r1 + 1 + 3) & ~3u;
-    const uint32_t vb = (k1v - k0v) * Cfg::SA, cb = (k1c - k0c) * 4u, rb = (r1a - r0a) * 4u;
-    mbar_arrive_expect_tx(bar, vb + cb + rb);
+    const uint32_t vb = (k1v - k0v) * Cfg::SA, cb = (k1c - k0c) * Cfg::CS, rb = (r1a - r0a) * 4u;
+    const uint32_t fb = IDX ? (((r1 + 3) & ~3u) - r0a) * 4u : 0u;
+    mbar_arrive_expect_tx(bar, vb + cb + rb + fb);
     uint8_t* sp = stage_ptr(s);
     if (vb) bulk_g2s(sp, vals + k0v, vb, bar);
-    if (cb) bulk_g2s(sp + Cfg::VAL_BYTES, A.ci + k0c, cb, bar);
+    if (cb) bulk_g2s(sp + Cfg::VAL_BYTES, cols + k0c, cb, bar);
     bulk_g2s(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES, A.rp + r0a, rb, bar);
+    if (IDX && fb) bulk_g2s(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES + Cfg::RP_BYTES, A.first + r0a, fb, bar);
   };
 
   if (tid == 0) {
@@ -98,11 +111,9 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
       if (t < T.ntiles) issue(t, s);
     }
   }
-  // gathers are issued CHUNK at a time (independent loads in flight per thread)
-  // before the sequential, order-preserving accumulation consumes them
-#ifndef F3RG_CHUNK
-#define F3RG_CHUNK 8
-#endif
+  // up to CHUNK gathers of a row are issued before the first is consumed (one
+  // latency round per CHUNK entries); groups of 8 are unpredicated, only the last
+  // partial group is predicated
   constexpr int CHUNK = F3RG_CHUNK;
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < T.ntiles; t += G, ++it) {
@@ -118,35 +129,70 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
     if (!longrow) {
       const uint8_t* sp = stage_ptr(s);
       const TA* sv = reinterpret_cast<const TA*>(sp);
-      const uint32_t* sc = reinterpret_cast<const uint32_t*>(sp + Cfg::VAL_BYTES);
+      const TC* sc = reinterpret_cast<const TC*>(sp + Cfg::VAL_BYTES);
       const uint32_t* sr = reinterpret_cast<const uint32_t*>(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES);
-      const uint32_t k0v = k0 & ~(uint32_t)(VAL - 1), k0c = k0 & ~3u, r0a = r0 & ~3u;
+      const uint32_t k0v = k0 & ~(uint32_t)(VAL - 1), k0c = k0 & ~(uint32_t)(CAL - 1), r0a = r0 & ~3u;
       if (row < r1) {
         const uint32_t kb = sr[row - r0a], ke = sr[row + 1 - r0a];
         T_<C> acc = Ar<C>::zero();
         const TA* pv = sv + (kb - k0v);
-        const uint32_t* pc = sc + (kb - k0c);
+        const TC* pc = sc + (kb - k0c);
         const uint32_t len = ke - kb;
-        // unpredicated chunks of 8 then 4 (raw loads first: all in flight, few live
-        // registers), then a predicated tail of <= 3
-        uint32_t q = 0;
-        for (; q + CHUNK <= len; q += CHUNK) row_chunk<C, CHUNK>(acc, pv + q, pc + q, g);
-        for (; q + 4 <= len; q += 4) row_chunk<C, 4>(acc, pv + q, pc + q, g);
-        {
-          typename Gather::Raw xs[3];
+        uint32_t col = 0;  // D16: running column
+        if constexpr (IDX == 1)
+          col = reinterpret_cast<const uint32_t*>(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES + Cfg::RP_BYTES)[row - r0a];
+        auto column = [&](uint32_t q) -> uint32_t {
+          if constexpr (IDX == 1) {
+            if (q > 0) col += pc[q];
+            return col;
+          } else {
+            return pc[q];
+          }
+        };
+        for (uint32_t q = 0; q < len; q += CHUNK) {
+          const uint32_t cnt = len - q < (uint32_t)CHUNK ? len - q : (uint32_t)CHUNK;
+          typename Gather::Raw xs[CHUNK];
 #pragma unroll
-          for (int u = 0; u < 3; ++u)
-            if (q + u < len) xs[u] = g.load(pc[q + u]);
+          for (int b = 0; b < CHUNK / 8; ++b) {
+            if ((uint32_t)(8 * b + 8) <= cnt) {
 #pragma unroll
-          for (int u = 0; u < 3; ++u)
-            if (q + u < len) acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[q + u]), g.value(xs[u])));
+              for (int u = 0; u < 8; ++u) xs[8 * b + u] = g.load(column(q + 8 * b + u));
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if ((uint32_t)(8 * b + u) < cnt) xs[8 * b + u] = g.load(column(q + 8 * b + u));
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < CHUNK / 8; ++b) {
+            if ((uint32_t)(8 * b + 8) <= cnt) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[q + 8 * b + u]), g.value(xs[8 * b + u])));
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if ((uint32_t)(8 * b + u) < cnt)
+                  acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[q + 8 * b + u]), g.value(xs[8 * b + u])));
+            }
+          }
         }
         e.row(row, acc);
       }
     } else if (tid == 0) {
       T_<C> acc = Ar<C>::zero();
-      for (uint32_t k = k0; k < k1; ++k)
-        acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vals[k]), g.value(g.load(A.ci[k]))));
+      uint32_t col = 0;
+      if constexpr (IDX == 1) col = A.first[r0];
+      for (uint32_t k = k0; k < k1; ++k) {
+        uint32_t c;
+        if constexpr (IDX == 1) {
+          if (k > k0) col += A.dcol[k];
+          c = col;
+        } else {
+          c = A.ci[k];
+        }
+        acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vals[k]), g.value(g.load(c))));
+      }
       e.row(r0, acc);
     }
     __syncthreads();
@@ -160,7 +206,6 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   __syncthreads();
   if (tid == 0)
     for (int s = 0; s < ST; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
-  (void)NT;
 }
 
 // ---- gathers ----------------------------------------------------------------------

@@ -12,6 +12,12 @@ struct CsrDev {
   const uint32_t* rp = nullptr;  // n+1 (+pad)
   const uint32_t* ci = nullptr;  // nnz (+pad)
   const void* val[3] = {nullptr, nullptr, nullptr};
+  // "D16" column stream (same columns, fewer bytes): first[i] = column of row i's
+  // first entry, dcol[k] = col[k] - col[k-1] inside a row (dcol[rp[i]] unused).
+  // Present only when every in-row gap fits 16 bits; kernels then stream 2-byte
+  // deltas instead of 4-byte indices.
+  const uint16_t* dcol = nullptr;   // nnz (+pad)
+  const uint32_t* first = nullptr;  // n (+pad)
 };
 
 struct TilesDev {

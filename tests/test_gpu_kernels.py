@@ -49,6 +49,23 @@ def test_spmv_bit_exact_all_precisions(probs, oracle, pa):
                 assert np.array_equal(got, want), (name, pa, px, py, np.abs(got - want).max())
 
 
+@pytest.mark.parametrize("columns", ["u32", "d16"])
+def test_spmv_both_column_streams(cuda, oracle, columns, monkeypatch):
+    """the u32 index stream and the 16-bit delta stream (D16) give identical bits"""
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+    if columns == "u32":
+        monkeypatch.setenv("F3RG_COLUMNS", "u32")
+    p = problems.problem(4, grid=20)
+    reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
+    a = (p.n, p.row_ptr, p.col_idx)
+    for pa, px, py in [(0, 0, 0), (0, 1, 1), (1, 1, 1), (2, 2, 2), (2, 1, 2), (0, 2, 0)]:
+        x = rand_vec(oracle, px, p.n, 3 + pa)
+        y = f.DenseVector(p.n, py)
+        f.spmv(reps.at(pa), f.DenseVector(x, px), y)
+        assert np.array_equal(y.numpy(), oracle.spmv(a, oracle.round_vec(pa, p.values), pa, x, px, py)), (pa, px, py)
+
+
 def test_spmv_long_rows_and_empty_rows(cuda, oracle):
     """rows longer than a shared-memory tile and empty rows (CSR edge cases)."""
     import paper_2505_20719_b200 as f

@@ -74,6 +74,18 @@ def test_config1_full_vs_reference(cuda, reference):
     assert run.report.precond_invocations == ref.precond_invocations
 
 
+def test_u32_and_d16_column_streams_solve_identically(probs, monkeypatch):
+    import paper_2505_20719_b200 as f
+    name, p = probs[3]
+    s1, _ = _solver(p, F3R16)
+    r1 = s1.run(p.b, f.RunOptions(tol=TOL))
+    monkeypatch.setenv("F3RG_COLUMNS", "u32")
+    s2, _ = _solver(p, F3R16)
+    r2 = s2.run(p.b, f.RunOptions(tol=TOL))
+    assert r1.report.residual_history == r2.report.residual_history
+    assert np.array_equal(r1.x, r2.x)
+
+
 def test_determinism_bitwise(probs):
     import paper_2505_20719_b200 as f
     name, p = probs[0]

@@ -13,13 +13,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 VARIANTS = {
-    "s2x8_c8": ["F3RG_STAGES=2", "F3RG_TILE_SCALE=8", "F3RG_CHUNK=8"],
-    "s3x5_c8": ["F3RG_STAGES=3", "F3RG_TILE_SCALE=5", "F3RG_CHUNK=8"],
-    "s4x4_c8": ["F3RG_STAGES=4", "F3RG_TILE_SCALE=4", "F3RG_CHUNK=8"],
-    "s2x8_c16": ["F3RG_STAGES=2", "F3RG_TILE_SCALE=8", "F3RG_CHUNK=16"],
-    "s3x5_c16": ["F3RG_STAGES=3", "F3RG_TILE_SCALE=5", "F3RG_CHUNK=16"],
-    "s2x4_c8": ["F3RG_STAGES=2", "F3RG_TILE_SCALE=4", "F3RG_CHUNK=8"],
+    "m2_s3_c32": ["F3RG_TILE_MINB=2", "F3RG_D16_STAGES=3", "F3RG_CHUNK=32"],
+    "m2_s3_c16": ["F3RG_TILE_MINB=2", "F3RG_D16_STAGES=3", "F3RG_CHUNK=16"],
+    "m3_s2_c16": ["F3RG_TILE_MINB=3", "F3RG_D16_STAGES=2", "F3RG_CHUNK=16"],
+    "m3_s2_c8": ["F3RG_TILE_MINB=3", "F3RG_D16_STAGES=2", "F3RG_CHUNK=8"],
+    "m4_s1_c8": ["F3RG_TILE_MINB=4", "F3RG_D16_STAGES=1", "F3RG_CHUNK=8"],
 }
+if os.environ.get("SWEEP"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP"].split(",")}
 
 CHILD = r"""
 import sys, time, json, torch
