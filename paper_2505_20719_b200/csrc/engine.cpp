@@ -174,6 +174,7 @@ Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_ki
   for (const auto& L : spec_.levels)
     if (L.kind == LK_FGMRES && L.m > 1000) throw Error(ERR_UNSUPPORTED, "FGMRES cycle length above 1000");
   id_ = spec_.to_string();
+  if (const char* e = std::getenv("F3RG_NO_REVERSE")) reverse_off_ = e[0] == '1';
   n_ = a_->rows();
   build_levels();
   capture_inner_graph();
@@ -391,7 +392,10 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
     PROF(kname("copy_scaled", L.W, L.W, L.W).c_str(), 2.0 * n * psize(L.W),
          launch_copy_scaled(L.W, Launch{0, s}, vj, sj, zj, n, GateH{dead, l + 1}, cnt));
   }
-  const TilesDev T = a_->tiles(L.PA);
+  TilesDev T = a_->tiles(L.PA);
+  // right after a Richardson pass over the same replica: walk the tiles backwards
+  // so the pass starts on the tail end that is still in L2
+  if (L.child == 1 && lv_[l + 1]->PA == L.PA && !reverse_off_) T.reverse = 1;
   const int nd = std::min(j + 1, 8);
   // Deferring the projection reduction to k_cgs (every CTA reduces the partials in
   // its prologue) measured no better than k_spmv_dots' own last-CTA tail (both

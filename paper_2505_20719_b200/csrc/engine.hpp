@@ -207,6 +207,7 @@ class Solver {
   bool has_inner_graph_ = false;
   bool profile_ = false;
   bool profiling_now_ = false;
+  bool reverse_off_ = false;  // F3RG_NO_REVERSE=1: no reversed tile walks (A/B tests)
   struct ProfRec;
   std::vector<std::unique_ptr<ProfRec>> prof_;
 };

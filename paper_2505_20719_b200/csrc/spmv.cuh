@@ -84,7 +84,9 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   __syncthreads();
 
   auto stage_ptr = [&](int s) { return smem + s * Cfg::STAGE_BYTES; };
-  auto issue = [&](uint32_t t, int s) {
+  auto phys = [&](uint32_t t) { return T.reverse ? T.ntiles - 1u - t : t; };
+  auto issue = [&](uint32_t tl, int s) {
+    const uint32_t t = phys(tl);
     const uint32_t r0 = T.r0[t], r1 = T.r0[t + 1], k0 = T.k0[t], k1 = T.k0[t + 1];
     uint64_t* bar = &bars[s];
     fence_proxy_async();
@@ -119,7 +121,8 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   for (uint32_t t = blockIdx.x; t < T.ntiles; t += G, ++it) {
     const int s = (int)(it % ST);
     const uint32_t par = (it / ST) & 1u;
-    const uint32_t r0 = T.r0[t], r1 = T.r0[t + 1], k0 = T.k0[t], k1 = T.k0[t + 1];
+    const uint32_t tp = phys(t);
+    const uint32_t r0 = T.r0[tp], r1 = T.r0[tp + 1], k0 = T.k0[tp], k1 = T.k0[tp + 1];
     const bool longrow = k1 - k0 > (uint32_t)Cfg::TNNZ;
     const uint32_t row = r0 + tid;
     // row-local epilogue operands do not depend on the tile: start them now so

@@ -24,6 +24,10 @@ struct TilesDev {
   const uint32_t* r0 = nullptr;  // ntiles+1 row starts
   const uint32_t* k0 = nullptr;  // ntiles+1 nnz starts (= rp[r0])
   uint32_t ntiles = 0;
+  // walk the tiles last-to-first: a pass that follows another pass over the same
+  // replica then starts on the part the L2 still holds (set per launch site, so
+  // every solve is still bitwise reproducible)
+  uint32_t reverse = 0;
 };
 
 // Device-resident state of one FGMRES level. H is column-major: column j holds
