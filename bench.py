@@ -91,6 +91,29 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
 
 
+# DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
+# committed `ncu --set full` capture of config 2 (profiles/r01_ncu_full.md)
+TRAFFIC = {}
+
+
+def streams_matrix(kernel):
+    return kernel.split("[")[0] in ("richardson", "spmv_dots", "spmv", "residual")
+
+
+def column_stream_saving(p):
+    """u32 column bytes minus D16 bytes (u16 deltas + u32 first column per row) when
+    the engine uses the D16 stream (every in-row gap < 2^16, F3RG_COLUMNS unset)."""
+    if os.environ.get("F3RG_COLUMNS") == "u32" or p.nnz == 0:
+        return 0.0
+    rp = p.row_ptr.astype(np.int64)
+    gaps = np.diff(p.col_idx.astype(np.int64))
+    inrow = np.ones(len(gaps), dtype=bool)
+    inrow[rp[1:-1][(rp[1:-1] > 0) & (rp[1:-1] < p.nnz)] - 1] = False
+    if len(gaps) and gaps[inrow].max(initial=0) > 0xFFFF:
+        return 0.0
+    return 4.0 * p.nnz - (2.0 * p.nnz + 4.0 * p.n)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
@@ -235,8 +258,12 @@ def run_ours(args):
     top = max(prof, key=lambda k: k[1])
     peak, peak_kind = _peaks()
     per_launch_ms = top[1] / top[2]
+    # profile bytes are what the kernel streams (D16 column stream when in use);
+    # SURVEY.md 8(d)'s algorithmic unit counts the reference's u32 CSR instead
     per_launch_bytes = top[3] / top[2]
-    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    algo_bytes = per_launch_bytes + (column_stream_saving(p) if streams_matrix(top[0]) else 0.0)
+    achieved = algo_bytes / (per_launch_ms * 1e-3) / 1e9
+    streamed = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
     breakdown = sorted(prof, key=lambda k: -k[1])
     kernels = [{"kernel": k[0], "share": round(k[1] / total_ms, 4), "launches": k[2],
                 "avg_us": round(1e3 * k[1] / k[2], 2),
@@ -248,8 +275,10 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "mixed f64/f32/f16", "data": "synthetic", "config": _config(args, p),
         "outer_iterations": outer, "final_true_residual": run.report.final_true_residual,
         "roofline": {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "bytes_per_launch": per_launch_bytes, "avg_launch_us": per_launch_ms * 1e3},
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": TRAFFIC.get(top[0]), "algorithmic_bytes_per_launch": algo_bytes,
+                     "streamed_bytes_per_launch": per_launch_bytes, "achieved_streamed": round(streamed, 1),
+                     "frac_streamed": round(streamed / peak, 4), "avg_launch_us": per_launch_ms * 1e3},
         "kernels": kernels,
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(p.n * 8), "d2h_bytes_per_step": int(p.n * 8)},
         "gpu_launches": launches * args.steps,

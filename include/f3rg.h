@@ -117,6 +117,7 @@ int f3rg_solver_reset_state(f3rg_solver* s, uintptr_t stream);
 int f3rg_solver_history(const f3rg_solver* s, double* out, uint64_t cap);
 int f3rg_solver_level_iterations(const f3rg_solver* s, uint64_t* out, uint64_t cap);
 int f3rg_solver_omegas(f3rg_solver* s, double* out, uint64_t cap); /* innermost_omegas() */
+uint64_t f3rg_solver_omega_count(const f3rg_solver* s);           /* its length (0: no Richardson level) */
 /* per-kernel timing of the next solve (CUDA events around each launch; the solve
  * runs eagerly instead of through the captured graph) */
 int f3rg_solver_set_profile(f3rg_solver* s, int on);

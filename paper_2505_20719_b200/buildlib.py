@@ -121,6 +121,7 @@ def build_oracle(verbose: bool = False) -> None:
     _run(["make", "-C", odir, "liboracle"])
     if os.path.isdir("/root/reference/proj/src"):
         _run(["make", "-C", odir, "ref"])
+        _run(["make", "-C", odir, "dropin"])  # after build_lib(): links libf3rg.so
     elif verbose:
         print("reference sources absent: using prebuilt oracle/_ref if present")
 

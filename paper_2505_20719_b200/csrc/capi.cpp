@@ -196,6 +196,12 @@ int f3rg_solver_omegas(f3rg_solver* s, double* out, uint64_t cap) {
   });
 }
 
+uint64_t f3rg_solver_omega_count(const f3rg_solver* s) {
+  uint64_t n = 0;
+  guarded([&] { n = s->s->innermost_omegas().size(); });
+  return n;
+}
+
 int f3rg_solver_set_profile(f3rg_solver* s, int on) {
   s->s->set_profile(on != 0);
   return F3RG_OK;

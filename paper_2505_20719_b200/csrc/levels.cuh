@@ -28,6 +28,7 @@
 namespace f3rg {
 
 constexpr int kMaxPart = 16;  // partial slots per block
+constexpr int kStageMax = 128;  // Hessenberg columns up to this length are staged in shared memory
 
 
 struct Gate {
@@ -350,13 +351,27 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
   block_sum<PW, 1>(acc, scratch);
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = A::wide(acc[0]);
   if (!last_block(sync.counter)) return;
-  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+  // Givens tail: one parallel round trip stages the small state (column j of H,
+  // the previous rotations, g_j) in shared memory, overlapped with the partials
+  // reduction; thread 0 then runs the serial recurrence out of shared memory
+  // instead of a chain of dependent global loads
+  __shared__ double hc[kStageMax + 1], cs[kStageMax], sn[kStageMax], gj_tol[3];
+  const bool staged = j < kStageMax;
+  if (staged) {
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) hc[i] = __ldcg(h + i);
+    for (int i = threadIdx.x; i < j; i += blockDim.x) cs[i] = __ldcg(L->cs + i), sn[i] = __ldcg(L->sn + i);
+    if (threadIdx.x == 0) gj_tol[0] = __ldcg(L->g + j), gj_tol[1] = L->tol, gj_tol[2] = L->bnorm;
+  }
+  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);  // ends with __syncthreads
   if (threadIdx.x != 0) return;
+  double* hh = staged ? hc : h;
+  const double* csr = staged ? cs : L->cs;
+  const double* snr = staged ? sn : L->sn;
 
   const T_<PW> wnorm = A::sqrt(cvt<PW>(tot[0]));
-  h[j + 1] = A::wide(wnorm);
+  hh[j + 1] = A::wide(wnorm);
   bool bad = !A::finite(wnorm);
-  for (int i = 0; i <= j + 1; ++i) bad = bad || !isfinite(h[i]);
+  for (int i = 0; i <= j + 1; ++i) bad = bad || !isfinite(hh[i]);
   bool stop = false;
   if (bad) {
     L->diverged = 1;
@@ -367,13 +382,13 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
     if (!happy) L->scale[j + 1] = A::wide(A::div(A::one(), wnorm));
     // apply the accumulated rotations to column j, then generate the new one
     for (int i = 0; i < j; ++i) {
-      const T_<PW> c = cvt<PW>(L->cs[i]), s = cvt<PW>(L->sn[i]);
-      const T_<PW> hi = cvt<PW>(h[i]), hi1 = cvt<PW>(h[i + 1]);
+      const T_<PW> c = cvt<PW>(csr[i]), s = cvt<PW>(snr[i]);
+      const T_<PW> hi = cvt<PW>(hh[i]), hi1 = cvt<PW>(hh[i + 1]);
       const T_<PW> t = A::add(A::mul(c, hi), A::mul(s, hi1));
-      h[i + 1] = A::wide(A::add(A::mul(A::neg(s), hi), A::mul(c, hi1)));
-      h[i] = A::wide(t);
+      hh[i + 1] = A::wide(A::add(A::mul(A::neg(s), hi), A::mul(c, hi1)));
+      hh[i] = A::wide(t);
     }
-    const T_<PW> hj = cvt<PW>(h[j]), hj1 = cvt<PW>(h[j + 1]);
+    const T_<PW> hj = cvt<PW>(hh[j]), hj1 = cvt<PW>(hh[j + 1]);
     const T_<PW> rho = A::hypot(hj, hj1);
     T_<PW> c, s;
     if (A::wide(rho) == 0.0) {
@@ -385,22 +400,25 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
     }
     L->cs[j] = A::wide(c);
     L->sn[j] = A::wide(s);
-    h[j] = A::wide(rho);
-    h[j + 1] = 0.0;
-    const T_<PW> gj = cvt<PW>(L->g[j]);
-    L->g[j + 1] = A::wide(A::mul(A::neg(s), gj));
+    hh[j] = A::wide(rho);
+    hh[j + 1] = 0.0;
+    const T_<PW> gj = cvt<PW>(staged ? gj_tol[0] : L->g[j]);
+    const double gj1 = A::wide(A::mul(A::neg(s), gj));
+    L->g[j + 1] = gj1;
     L->g[j] = A::wide(A::mul(c, gj));
     L->k = j + 1;
-    const double est = fabs(L->g[j + 1]);
+    const double est = fabs(gj1);
     L->estimate = est;
     if (happy) {
       L->happy = 1;
       stop = true;
-    } else if (use_tol && est < L->tol * L->bnorm) {
+    } else if (use_tol && est < (staged ? gj_tol[1] * gj_tol[2] : L->tol * L->bnorm)) {
       L->tol_hit = 1;
       stop = true;
     }
   }
+  if (staged)
+    for (int i = 0; i <= j + 1; ++i) h[i] = hc[i];
   if (!outer && stop) dead[level] = 1;
   if (info) {
     info->estimate = L->estimate;
@@ -425,12 +443,26 @@ __global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n,
   using A = Ar<PW>;
   const int k = L->k;
   const int m1 = L->m + 1;
+  // inner levels (k <= 16): stage the triangle of H and g in shared memory with one
+  // parallel round trip, so thread 0's back-substitution never waits on global loads
+  constexpr int KS = 16;
+  __shared__ double Hs[KS * KS], gs[KS];
+  const bool staged = k <= KS;
+  if (staged) {
+    const double* H = L->H;
+    for (int t = threadIdx.x; t < k * k; t += blockDim.x) {
+      const int l = t / k, i = t - l * k;
+      if (l >= i) Hs[l * KS + i] = H[(size_t)l * m1 + i];
+    }
+    if (threadIdx.x < k) gs[threadIdx.x] = L->g[threadIdx.x];
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     for (int i = k - 1; i >= 0; --i) {
-      T_<PW> acc = cvt<PW>(L->g[i]);
+      T_<PW> acc = cvt<PW>(staged ? gs[i] : L->g[i]);
       for (int l = i + 1; l < k; ++l)
-        acc = A::sub(acc, A::mul(cvt<PW>(L->H[(size_t)l * m1 + i]), cvt<PW>(ys[l])));
-      ys[i] = A::wide(A::div(acc, cvt<PW>(L->H[(size_t)i * m1 + i])));
+        acc = A::sub(acc, A::mul(cvt<PW>(staged ? Hs[l * KS + i] : L->H[(size_t)l * m1 + i]), cvt<PW>(ys[l])));
+      ys[i] = A::wide(A::div(acc, cvt<PW>(staged ? Hs[i * KS + i] : L->H[(size_t)i * m1 + i])));
     }
     if (blockIdx.x == 0) {
       for (int i = 0; i < k; ++i) L->y[i] = ys[i];
