@@ -93,7 +93,7 @@ class Clocks:
 
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
 # committed `ncu --set full` capture of config 2 (profiles/r01_ncu_full.md)
-TRAFFIC = {}
+TRAFFIC = {"richardson[f16,f16,f32]": 255257088.0, "spmv_dots[f16,f16,f32]": 273912064.0}
 
 
 def streams_matrix(kernel):
@@ -236,13 +236,13 @@ def run_ours(args):
         raise SystemExit(f"timed solve did not converge: {run.report}")
 
     # ---- e2e: through the C ABI with host buffers (pinned b in, x out) ----
-    b_pin = torch.from_numpy(p.b).pin_memory()
-    b_host = b_pin.numpy()
+    b_host = torch.from_numpy(p.b).pin_memory().numpy()
+    x_host = torch.empty(p.n, dtype=torch.float64).pin_memory().numpy()
     e2e_t = []
     for _ in range(max(1, min(args.steps, 5))):
         t0 = time.perf_counter()
         solver.reset()
-        r2 = solver.run(b_host, opts)
+        r2 = solver.run(b_host, opts, out=x_host)
         e2e_t.append(time.perf_counter() - t0)
     e2e = float(np.mean(e2e_t))
     assert r2.report.converged

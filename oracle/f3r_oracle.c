@@ -111,19 +111,36 @@ void or_spmv(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* v
   }
 }
 
-double or_dot(const double* x, int px, const double* y, int py, uint64_t n, int floor_p) {
-  const int c = maxp(floor_p, maxp(px, py));
+/* Summation order of the dots (experiments only): 0 = the reference's sequential
+ * index order (src/vector_ops.cpp:20-28, the default), 1 = pairwise (blocks of 256
+ * summed sequentially, then a balanced tree), at the same precision C. Used to show
+ * that outer-count differences at large n come from the order alone. */
+static int g_pairwise = 0;
+void or_set_pairwise_dots(int on) { g_pairwise = on; }
+
+static double dot_seq(int c, const double* x, const double* y, uint64_t lo, uint64_t hi) {
   double acc = 0.0;
   if (c == OR_P64) {
-    for (uint64_t i = 0; i < n; ++i) acc = acc + x[i] * y[i];
+    for (uint64_t i = lo; i < hi; ++i) acc = acc + x[i] * y[i];
   } else if (c == OR_P32) {
     float a = 0.0f;
-    for (uint64_t i = 0; i < n; ++i) a = a + (float)x[i] * (float)y[i];
+    for (uint64_t i = lo; i < hi; ++i) a = a + (float)x[i] * (float)y[i];
     acc = a;
   } else {
-    for (uint64_t i = 0; i < n; ++i) acc = add_c(OR_P16, acc, mul_c(OR_P16, x[i], y[i]));
+    for (uint64_t i = lo; i < hi; ++i) acc = add_c(OR_P16, acc, mul_c(OR_P16, x[i], y[i]));
   }
   return acc;
+}
+
+static double dot_pairwise(int c, const double* x, const double* y, uint64_t lo, uint64_t hi) {
+  if (hi - lo <= 256) return dot_seq(c, x, y, lo, hi);
+  const uint64_t mid = lo + (hi - lo) / 2;
+  return add_c(c, dot_pairwise(c, x, y, lo, mid), dot_pairwise(c, x, y, mid, hi));
+}
+
+double or_dot(const double* x, int px, const double* y, int py, uint64_t n, int floor_p) {
+  const int c = maxp(floor_p, maxp(px, py));
+  return g_pairwise ? dot_pairwise(c, x, y, 0, n) : dot_seq(c, x, y, 0, n);
 }
 
 double or_norm2(const double* x, int px, uint64_t n) {

@@ -34,6 +34,7 @@ double or_round(int p, double x); /* demote(x, p) of include/f3r/precision.hpp:6
 void or_spmv(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals, int pa, const double* x,
              int px, double* y, int py);
 double or_dot(const double* x, int px, const double* y, int py, uint64_t n, int floor_p);
+void or_set_pairwise_dots(int on); /* experiments: pairwise instead of sequential dots */
 double or_norm2(const double* x, int px, uint64_t n);
 void or_axpy(double alpha, const double* x, int px, double* y, int py, uint64_t n);
 void or_add_scaled(const double* x, int px, double alpha, const double* y, int py, double* out, int po,

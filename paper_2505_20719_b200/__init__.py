@@ -112,6 +112,8 @@ def lib():
     L.f3rg_solver_reset_state.argtypes = [vp, C.c_size_t]
     L.f3rg_solver_level_iterations.argtypes = [vp, vp, u64]
     L.f3rg_solver_omegas.argtypes = [vp, vp, u64]
+    L.f3rg_solver_omega_count.restype = u64
+    L.f3rg_solver_omega_count.argtypes = [vp]
     L.f3rg_solver_set_profile.argtypes = [vp, i32]
     L.f3rg_solver_profile_entry.argtypes = [vp, u64, C.c_char_p, C.c_size_t, C.POINTER(dbl), C.POINTER(u64),
                                             C.POINTER(dbl)]
@@ -491,15 +493,18 @@ class ComposedSolver:
                                  r.final_true_residual, r.wall_seconds, list(om[:r.n_omegas]), r.flag.decode(),
                                  self.id())
 
-    def run(self, b, opts: RunOptions = RunOptions(), want_x: bool = True) -> RunResult:
+    def run(self, b, opts: RunOptions = RunOptions(), want_x: bool = True, out=None) -> RunResult:
         """b: host numpy fp64 array (host copies inside the call) or a CUDA fp64
-        tensor (device-resident; x is returned as a CUDA tensor)."""
+        tensor (device-resident; x is returned as a CUDA tensor). With a host b,
+        `out` (fp64 numpy array of length n, ideally in pinned memory) receives x."""
         r = _Report()
         if isinstance(b, np.ndarray):
             b = np.ascontiguousarray(b, dtype=np.float64)
             if b.size != self.n:
                 raise DimensionError("run: rhs length mismatch")
-            x = np.zeros(self.n) if want_x else None
+            if out is not None and (out.dtype != np.float64 or out.size != self.n or not out.flags.c_contiguous):
+                raise DimensionError("run: out must be a contiguous fp64 array of length n")
+            x = (out if out is not None else np.zeros(self.n)) if want_x else None
             _check(lib().f3rg_solve(self.h, b.ctypes.data, x.ctypes.data if x is not None else None,
                                     C.byref(opts._c()), C.byref(r)))
             return RunResult(x, self._report(r))
@@ -518,9 +523,12 @@ class ComposedSolver:
         _check(lib().f3rg_solver_reset_state(self.h, _stream()))
 
     def innermost_omegas(self) -> list:
-        om = np.zeros(64)
-        _check(lib().f3rg_solver_omegas(self.h, om.ctypes.data, 64))
-        return list(om)
+        """weights of the deepest Richardson level; empty when there is none"""
+        cnt = int(lib().f3rg_solver_omega_count(self.h))
+        om = np.zeros(max(1, cnt))
+        if cnt:
+            _check(lib().f3rg_solver_omegas(self.h, om.ctypes.data, cnt))
+        return list(om[:cnt])
 
     def set_profile(self, on: bool = True) -> None:
         lib().f3rg_solver_set_profile(self.h, int(on))

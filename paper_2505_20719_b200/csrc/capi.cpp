@@ -20,6 +20,7 @@ struct f3rg_matrix {
 struct f3rg_solver {
   std::unique_ptr<Solver> s;
   Report last;
+  DevBuf b, x;  // device staging of the host-buffer entry, allocated on first use
 };
 
 struct f3rg_richardson {
@@ -165,10 +166,14 @@ int f3rg_solve_device(f3rg_solver* s, const double* b, double* x, const f3rg_run
 int f3rg_solve(f3rg_solver* s, const double* b_host, double* x_host, const f3rg_run_options* o, f3rg_report* rep) {
   return guarded([&] {
     const uint64_t n = s->s->rows();
-    DevBuf b(n * 8 + 16), x(n * 8 + 16);
-    F3RG_CUDA(cudaMemcpy(b.get(), b_host, n * 8, cudaMemcpyHostToDevice));
-    s->last = s->s->run(b.get<double>(), x_host ? x.get<double>() : nullptr, to_opts(o), nullptr);
-    if (x_host) F3RG_CUDA(cudaMemcpy(x_host, x.get(), n * 8, cudaMemcpyDeviceToHost));
+    if (!s->b.get()) s->b.alloc(n * 8 + 16), s->x.alloc(n * 8 + 16);
+    cudaStream_t st = s->s->stream();
+    F3RG_CUDA(cudaMemcpyAsync(s->b.get(), b_host, n * 8, cudaMemcpyHostToDevice, st));
+    s->last = s->s->run(s->b.get<double>(), x_host ? s->x.get<double>() : nullptr, to_opts(o), st);
+    if (x_host) {
+      F3RG_CUDA(cudaMemcpyAsync(x_host, s->x.get(), n * 8, cudaMemcpyDeviceToHost, st));
+      F3RG_CUDA(cudaStreamSynchronize(st));
+    }
     fill_report(s->last, rep);
   });
 }

@@ -167,6 +167,7 @@ class Solver {
   std::vector<unsigned long long> level_invocations();
   const std::string& id() const { return id_; }
   uint64_t rows() const { return a_->rows(); }
+  cudaStream_t stream() const { return own_stream_; }
   // per-kernel timing of the NEXT run (CUDA events around every launch, eager mode)
   void set_profile(bool on) { profile_ = on; }
   struct KernelTime {

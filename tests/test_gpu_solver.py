@@ -107,6 +107,17 @@ def test_device_and_host_entry_points_agree(probs, cuda):
     r2 = s2.run(bd, f.RunOptions(tol=TOL))
     assert r1.report.residual_history == r2.report.residual_history
     assert np.array_equal(r1.x, r2.x.cpu().numpy())
+    # caller-provided (pinned) output buffer, reused across solves
+    out = cuda.empty(p.n, dtype=cuda.float64).pin_memory().numpy()
+    for _ in range(2):
+        s1.reset()
+        r3 = s1.run(p.b, f.RunOptions(tol=TOL), out=out)
+        assert r3.x is out and np.array_equal(out, r1.x)
+    # innermost_omegas(): the deepest Richardson level's m weights (reference
+    # include/f3r/nesting.hpp:67-68), equal to the report's omegas_final
+    assert s1.innermost_omegas() == r3.report.omegas_final and len(r3.report.omegas_final) == 2
+    with pytest.raises(f.DimensionError):
+        s1.run(p.b, f.RunOptions(tol=TOL), out=np.zeros(p.n + 1))
 
 
 def test_zero_rhs(probs):
