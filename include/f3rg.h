@@ -151,6 +151,53 @@ int f3rg_richardson_state(f3rg_richardson* r, double* omegas_host, uint64_t* cou
 /* v, z: device vectors at the Richardson precision */
 int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t stream);
 
+/* ---- row-block partition over P ranks ---------
+ * Rows split by the reference's rule (src/ilu.cpp:47-54: base = n/P, remainder to the
+ * leading blocks). Each rank keeps its rows of A and of every Krylov vector; SpMV
+ * inputs use the rank's "ext" layout [pad | lo halo | owned | hi halo] (halo = remote
+ * columns referenced by its rows, ascending); dots/norms are rank-local sums combined
+ * in rank order, so every rank holds bitwise-identical Hessenberg/Givens scalars. */
+typedef struct {
+  uint64_t r0, r1;         /* owned rows */
+  uint64_t n_lo, n_hi;     /* halo entries below / above the owned rows */
+  uint64_t pad, off;       /* ext layout: owned rows start at off = pad + n_lo */
+  uint64_t n_ext, ld;      /* ext length; vector stride of a basis */
+  uint64_t nnz_local;      /* nonzeros of the owned rows */
+  uint64_t nnz_begin;      /* global position of the first of them */
+  uint64_t n_send;         /* total entries this rank sends per halo exchange */
+} f3rg_part_info;
+
+/* rank `rank`'s plan (host only, no device work). Optional outputs (NULL to skip):
+ * halo[n_lo + n_hi] global columns; recv_off/recv_cnt/send_cnt[P]; send_idx[n_send]
+ * owned-local indices, peers in rank order; local_rp[r1 - r0 + 1]; local_ci[nnz_local]
+ * (ext columns) */
+int f3rg_part_plan(const f3rg_csr* a, int P, int rank, f3rg_part_info* info, uint32_t* halo, uint64_t* recv_off,
+                   uint64_t* recv_cnt, uint64_t* send_cnt, uint32_t* send_idx, uint32_t* local_rp,
+                   uint32_t* local_ci);
+
+typedef struct f3rg_comm f3rg_comm;
+/* P ranks as host threads of this process, all on the current device, one stream
+ * (the one-GPU test vehicle of the partition; data flow as with NCCL) */
+int f3rg_comm_local(f3rg_comm** out, const f3rg_csr* a, int P);
+/* one rank per process over NCCL (libnccl.so.2 resolved at run time; F3RG_NCCL_LIB
+ * overrides). unique_id: 128 bytes from f3rg_nccl_unique_id on one rank, shared. */
+int f3rg_nccl_unique_id(void* out128);
+int f3rg_comm_nccl(f3rg_comm** out, const f3rg_csr* a, int P, int rank, const void* unique_id);
+void f3rg_comm_destroy(f3rg_comm* c);
+/* a ComposedSolver over rank `rank`'s rows (a: the GLOBAL fp64 CSR, host) */
+int f3rg_solver_create_part(f3rg_solver** out, f3rg_comm* c, const f3rg_csr* a, const char* spec, int precond_kind,
+                            int rank);
+/* local communicator: solve with all P rank solvers (one host thread each); b, x:
+ * global host vectors; reps[P] */
+int f3rg_solve_local(f3rg_comm* c, f3rg_solver** solvers, const double* b_host, double* x_host,
+                     const f3rg_run_options* opts, f3rg_report* reps);
+/* NCCL communicator: this rank's solve; b_own, x_own: device vectors of its rows */
+int f3rg_solve_part_device(f3rg_solver* s, const double* b_own, double* x_own, const f3rg_run_options* opts,
+                           f3rg_report* rep, uintptr_t stream);
+/* y = A x through the partition (P rank-local SpMVs on the current device after a
+ * halo exchange); x, y: global host fp64 vectors, values rounded to px / from py */
+int f3rg_local_spmv(const f3rg_csr* a, int P, int pa, int px, int py, const double* x_host, double* y_host);
+
 #ifdef __cplusplus
 }
 #endif

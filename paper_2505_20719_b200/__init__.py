@@ -114,6 +114,16 @@ def lib():
     L.f3rg_solver_omegas.argtypes = [vp, vp, u64]
     L.f3rg_solver_omega_count.restype = u64
     L.f3rg_solver_omega_count.argtypes = [vp]
+    # row-block partition (partition.py)
+    L.f3rg_part_plan.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.f3rg_comm_local.argtypes = [C.POINTER(vp), vp, i32]
+    L.f3rg_nccl_unique_id.argtypes = [vp]
+    L.f3rg_comm_nccl.argtypes = [C.POINTER(vp), vp, i32, i32, vp]
+    L.f3rg_comm_destroy.argtypes = [vp]
+    L.f3rg_solver_create_part.argtypes = [C.POINTER(vp), vp, vp, C.c_char_p, i32, i32]
+    L.f3rg_solve_local.argtypes = [vp, vp, vp, vp, C.POINTER(_RunOpts), vp]
+    L.f3rg_solve_part_device.argtypes = [vp, vp, vp, C.POINTER(_RunOpts), C.POINTER(_Report), C.c_size_t]
+    L.f3rg_local_spmv.argtypes = [vp, i32, i32, i32, i32, vp, vp]
     L.f3rg_solver_set_profile.argtypes = [vp, i32]
     L.f3rg_solver_profile_entry.argtypes = [vp, u64, C.c_char_p, C.c_size_t, C.POINTER(dbl), C.POINTER(u64),
                                             C.POINTER(dbl)]

@@ -56,17 +56,23 @@ __global__ void __launch_bounds__(256) k_add_scaled(const void* x, double alpha,
 // dot at C = max(floor, px, py); result (a C value) in *out; if SQRT, sqrt at
 // precision PS of the C value rounded to PS (norm2 semantics).
 template <int PX, int PY, int C, bool SQRT, int PS>
-__global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint64_t n, double* out, Sync sync) {
+__global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint64_t n, double* out, Sync sync,
+                                             Dist dist) {
   __shared__ double scratch[64];
   __shared__ double tot[1];
-  T_<C> acc[1] = {Ar<C>::zero()};
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    acc[0] = Ar<C>::add(acc[0], Ar<C>::mul(cvt<C>(ld<PX>(x, i)), cvt<C>(ld<PY>(y, i))));
-  block_sum<C, 1>(acc, scratch);
-  if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<C>::wide(acc[0]);
-  if (!last_block(sync.counter)) return;
-  reduce_partials<C, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+  if (dist.mode != 2) {
+    T_<C> acc[1] = {Ar<C>::zero()};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+      acc[0] = Ar<C>::add(acc[0], Ar<C>::mul(cvt<C>(ld<PX>(x, i)), cvt<C>(ld<PY>(y, i))));
+    block_sum<C, 1>(acc, scratch);
+    if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<C>::wide(acc[0]);
+    if (!last_block(sync.counter)) return;
+    reduce_partials<C, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (publish_local(dist, 1, tot)) return;
+  } else {
+    combine_ranks<C>(dist, 1, tot);
+  }
   if (threadIdx.x == 0) {
     if constexpr (SQRT) {
       *out = Ar<PS>::wide(Ar<PS>::sqrt(cvt<PS>(tot[0])));
@@ -74,6 +80,16 @@ __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint6
       *out = tot[0];
     }
   }
+}
+
+// halo exchange helper (row-block partition): dst[i] = src[idx[i]], element-wise
+// copies at one precision (pack for a send, or a direct gather from a peer's
+// owned rows when the peers share an address space)
+template <int P>
+__global__ void __launch_bounds__(256) k_gather(const void* src, const uint32_t* idx, uint64_t cnt, void* dst) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride)
+    st<P>(dst, i, ld<P>(src, idx[i]));
 }
 
 // plain y = A x (any precision triple), for the kernel-level entry point

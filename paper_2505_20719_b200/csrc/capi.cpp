@@ -5,6 +5,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/f3rg.h"
@@ -366,6 +367,198 @@ int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t 
                                 r->cnt.get<unsigned long long>(),
                                 SyncH{r->partials.get<double>(), r->counter.get<unsigned>()}, r->bar.get<unsigned>(),
                                 r->bar.get<unsigned>() + 1, nullptr));
+  });
+}
+
+}  // extern "C"
+
+// ---- row-block partition ----------------------------------------
+struct f3rg_comm {
+  int P = 1;
+  std::unique_ptr<LocalGroup> local;
+  std::vector<std::unique_ptr<LocalExchange>> lex;
+  std::unique_ptr<NcclExchange> nccl;
+  uint64_t n = 0;
+};
+
+extern "C" {
+
+int f3rg_part_plan(const f3rg_csr* a, int P, int rank, f3rg_part_info* info, uint32_t* halo, uint64_t* recv_off,
+                   uint64_t* recv_cnt, uint64_t* send_cnt, uint32_t* send_idx, uint32_t* local_rp,
+                   uint32_t* local_ci) {
+  return guarded([&] {
+    if (!a || !info) throw Error(ERR_DIMENSION, "null argument");
+    validate_csr(a->n, a->row_ptr, a->col_idx);
+    const PartPlan p = make_plan(a->n, a->row_ptr, a->col_idx, P, rank);
+    info->r0 = p.r0;
+    info->r1 = p.r1;
+    info->n_lo = p.n_lo;
+    info->n_hi = p.n_hi;
+    info->pad = p.pad;
+    info->off = p.off();
+    info->n_ext = p.n_ext();
+    info->ld = p.ld();
+    info->nnz_local = p.ci.size();
+    info->nnz_begin = p.nnz_begin;
+    uint64_t nsend = 0;
+    for (const auto& v : p.send_idx) nsend += v.size();
+    info->n_send = nsend;
+    if (halo) std::memcpy(halo, p.halo.data(), p.halo.size() * 4);
+    for (int q = 0; q < P; ++q) {
+      if (recv_off) recv_off[q] = p.recv_off[q];
+      if (recv_cnt) recv_cnt[q] = p.recv_cnt[q];
+      if (send_cnt) send_cnt[q] = p.send_idx[q].size();
+    }
+    if (send_idx) {
+      uint64_t o = 0;
+      for (const auto& v : p.send_idx) {
+        std::memcpy(send_idx + o, v.data(), v.size() * 4);
+        o += v.size();
+      }
+    }
+    if (local_rp) std::memcpy(local_rp, p.rp.data(), p.rp.size() * 4);
+    if (local_ci) std::memcpy(local_ci, p.ci.data(), p.ci.size() * 4);
+  });
+}
+
+int f3rg_comm_local(f3rg_comm** out, const f3rg_csr* a, int P) {
+  return guarded([&] {
+    if (!out || !a) throw Error(ERR_DIMENSION, "null argument");
+    validate_csr(a->n, a->row_ptr, a->col_idx);
+    auto c = std::make_unique<f3rg_comm>();
+    c->P = P;
+    c->n = a->n;
+    c->local = std::make_unique<LocalGroup>(P);
+    c->local->set_plans(a->n, a->row_ptr, a->col_idx);
+    for (int r = 0; r < P; ++r) c->lex.push_back(std::make_unique<LocalExchange>(c->local.get(), r));
+    *out = c.release();
+  });
+}
+
+int f3rg_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    if (!out128) throw Error(ERR_DIMENSION, "null argument");
+    NcclExchange::unique_id(out128);
+  });
+}
+
+int f3rg_comm_nccl(f3rg_comm** out, const f3rg_csr* a, int P, int rank, const void* unique_id) {
+  return guarded([&] {
+    if (!out || !a || !unique_id) throw Error(ERR_DIMENSION, "null argument");
+    validate_csr(a->n, a->row_ptr, a->col_idx);
+    auto c = std::make_unique<f3rg_comm>();
+    c->P = P;
+    c->n = a->n;
+    c->nccl = std::make_unique<NcclExchange>(P, rank, unique_id, a->n, a->row_ptr, a->col_idx);
+    *out = c.release();
+  });
+}
+
+void f3rg_comm_destroy(f3rg_comm* c) { delete c; }
+
+int f3rg_solver_create_part(f3rg_solver** out, f3rg_comm* c, const f3rg_csr* a, const char* spec, int precond_kind,
+                            int rank) {
+  return guarded([&] {
+    if (!out || !c || !a || !spec) throw Error(ERR_DIMENSION, "null argument");
+    if (a->n != c->n) throw Error(ERR_DIMENSION, "matrix differs from the one the communicator was planned for");
+    Exchange* ex = nullptr;
+    if (c->local) {
+      if (rank < 0 || rank >= c->P) throw Error(ERR_DIMENSION, "rank out of range");
+      ex = c->lex[rank].get();
+    } else {
+      if (rank != c->nccl->rank()) throw Error(ERR_DIMENSION, "rank differs from the communicator's");
+      ex = c->nccl.get();
+    }
+    const PartPlan& p = ex->plan();
+    auto m = std::make_shared<DeviceMatrix>(p.n_own(), p.rp.data(), p.ci.data(), a->values + p.nnz_begin, p.n_ext());
+    auto h = std::make_unique<f3rg_solver>();
+    h->s = std::make_unique<Solver>(parse_spec(spec), m, precond_kind, ex);
+    *out = h.release();
+  });
+}
+
+int f3rg_solve_local(f3rg_comm* c, f3rg_solver** solvers, const double* b_host, double* x_host,
+                     const f3rg_run_options* o, f3rg_report* reps) {
+  return guarded([&] {
+    if (!c || !c->local || !solvers || !b_host) throw Error(ERR_DIMENSION, "local solve needs a local communicator");
+    const int P = c->P;
+    std::vector<int> codes((size_t)P, F3RG_OK);
+    std::vector<std::string> msgs((size_t)P);
+    std::vector<std::thread> th;
+    const RunOptions opts = to_opts(o);
+    for (int r = 0; r < P; ++r) {
+      th.emplace_back([&, r] {
+        try {
+          f3rg_solver* s = solvers[r];
+          const PartPlan& p = c->local->plans[r];
+          const uint64_t n = p.n_own();
+          if (s->s->rows() != n || s->s->exchange() != c->lex[r].get())
+            throw Error(ERR_DIMENSION, "solver " + std::to_string(r) + " is not rank " + std::to_string(r));
+          cudaStream_t st = c->local->stream;
+          if (!s->b.get()) s->b.alloc(n * 8 + 16), s->x.alloc(n * 8 + 16);
+          F3RG_CUDA(cudaMemcpyAsync(s->b.get(), b_host + p.r0, n * 8, cudaMemcpyHostToDevice, st));
+          s->last = s->s->run(s->b.get<double>(), x_host ? s->x.get<double>() : nullptr, opts, st);
+          if (x_host) {
+            F3RG_CUDA(cudaMemcpyAsync(x_host + p.r0, s->x.get(), n * 8, cudaMemcpyDeviceToHost, st));
+            F3RG_CUDA(cudaStreamSynchronize(st));
+          }
+          if (reps) fill_report(s->last, reps + r);
+        } catch (const Error& e) {
+          codes[r] = e.code, msgs[r] = e.what();
+          c->local->fail();
+        } catch (const std::exception& e) {
+          codes[r] = F3RG_EINTERNAL, msgs[r] = e.what();
+          c->local->fail();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int r = 0; r < P; ++r)
+      if (codes[r] != F3RG_OK && msgs[r].find("a peer rank failed") == std::string::npos)
+        throw Error(codes[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+    for (int r = 0; r < P; ++r)
+      if (codes[r] != F3RG_OK) throw Error(codes[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+  });
+}
+
+int f3rg_local_spmv(const f3rg_csr* a, int P, int pa, int px, int py, const double* x_host, double* y_host) {
+  return guarded([&] {
+    check_prec(pa), check_prec(px), check_prec(py);
+    if (!a || !x_host || !y_host) throw Error(ERR_DIMENSION, "null argument");
+    validate_csr(a->n, a->row_ptr, a->col_idx);
+    LocalGroup g(P);
+    g.set_plans(a->n, a->row_ptr, a->col_idx);
+    const size_t esx = px == 0 ? 2 : px == 1 ? 4 : 8, esy = py == 0 ? 2 : py == 1 ? 4 : 8;
+    std::vector<std::shared_ptr<DeviceMatrix>> mats;
+    std::vector<DevBuf> xs((size_t)P), ys((size_t)P);
+    DevBuf tmp(a->n * 8 + 16);
+    for (int r = 0; r < P; ++r) {
+      const PartPlan& p = g.plans[r];
+      mats.push_back(
+          std::make_shared<DeviceMatrix>(p.n_own(), p.rp.data(), p.ci.data(), a->values + p.nnz_begin, p.n_ext()));
+      xs[r].alloc(p.ld() * esx + 16);
+      ys[r].alloc(p.n_own() * esy + 16);
+      F3RG_CUDA(cudaMemset(xs[r].get(), 0, xs[r].bytes()));
+      F3RG_CUDA(cudaMemcpy(tmp.get(), x_host + p.r0, p.n_own() * 8, cudaMemcpyHostToDevice));
+      F3RG_CUDA(launch_copy(2, px, Launch{}, tmp.get(), xs[r].get<char>() + p.off() * esx, p.n_own()));
+      g.ptrs[r] = xs[r].get();
+    }
+    for (int r = 0; r < P; ++r) g.gather_into(r, xs[r].get(), px, nullptr);
+    for (int r = 0; r < P; ++r) {
+      const PartPlan& p = g.plans[r];
+      F3RG_CUDA(launch_spmv(pa, px, py, Launch{}, mats[r]->csr(), mats[r]->tiles(pa), xs[r].get(), ys[r].get()));
+      F3RG_CUDA(launch_copy(py, 2, Launch{}, ys[r].get(), tmp.get(), p.n_own()));
+      F3RG_CUDA(cudaMemcpy(y_host + p.r0, tmp.get(), p.n_own() * 8, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int f3rg_solve_part_device(f3rg_solver* s, const double* b_own, double* x_own, const f3rg_run_options* o,
+                           f3rg_report* rep, uintptr_t stream) {
+  return guarded([&] {
+    if (!s || !s->s->exchange()) throw Error(ERR_DIMENSION, "not a partitioned solver");
+    s->last = s->s->run(b_own, x_own, to_opts(o), as_stream(stream));
+    fill_report(s->last, rep);
   });
 }
 

@@ -26,6 +26,7 @@ inline void with_p(int p, F&& f) {
 
 inline Sync to_sync(SyncH s) { return Sync{s.partials, s.counter}; }
 inline Gate to_gate(GateH g) { return Gate{g.dead, g.n}; }
+inline Dist to_dist(DistH d) { return Dist{d.mode, d.P, d.loc, d.all}; }
 
 constexpr int kThreads = 256;
 

@@ -40,9 +40,10 @@ void DevBuf::release() {
 static size_t psize(int p) { return p == 0 ? 2 : p == 1 ? 4 : 8; }
 
 // ---- DeviceMatrix -------------------------------------------------------------------
-void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci) {
+void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci, uint64_t ncols) {
   const uint64_t lim = uint64_t{1} << 31;
-  if (n >= lim) throw Error(ERR_DIMENSION, "matrix exceeds 32-bit index range");
+  if (ncols == 0) ncols = n;
+  if (n >= lim || ncols >= lim) throw Error(ERR_DIMENSION, "matrix exceeds 32-bit index range");
   if (!rp) throw Error(ERR_DIMENSION, "row_ptr length must be n+1");
   const uint64_t nnz = rp[n];
   if (nnz >= lim) throw Error(ERR_DIMENSION, "matrix exceeds 32-bit index range");
@@ -50,16 +51,17 @@ void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci) {
   for (uint64_t i = 0; i < n; ++i) {
     if (rp[i] > rp[i + 1]) throw Error(ERR_DIMENSION, "row_ptr must be non-decreasing");
     for (uint32_t k = rp[i]; k < rp[i + 1]; ++k) {
-      if (ci[k] >= n) throw Error(ERR_DIMENSION, "column index out of bounds in row " + std::to_string(i));
+      if (ci[k] >= ncols) throw Error(ERR_DIMENSION, "column index out of bounds in row " + std::to_string(i));
       if (k > rp[i] && ci[k] <= ci[k - 1])
         throw Error(ERR_DIMENSION, "columns must be strictly increasing in row " + std::to_string(i));
     }
   }
 }
 
-DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values)
+DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values,
+                           uint64_t ncols)
     : n_(n), nnz_(row_ptr ? row_ptr[n] : 0) {
-  validate_csr(n, row_ptr, col_idx);
+  validate_csr(n, row_ptr, col_idx, ncols);
   // padded so the 16-byte-granular bulk copies never read past an allocation
   rp_.alloc((n_ + 1) * 4 + 32);
   ci_.alloc(nnz_ * 4 + 32);
@@ -153,7 +155,8 @@ struct Solver::ProfRec {
   cudaEvent_t e0, e1;
 };
 
-Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind) : spec_(spec), a_(std::move(a)) {
+Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind, Exchange* ex)
+    : spec_(spec), a_(std::move(a)), ex_(ex) {
   if (spec_.levels.empty()) throw Error(ERR_SOLVER, "composed solver needs at least one level");
   for (const auto& L : spec_.levels)
     if (L.m < 1) throw Error(ERR_SOLVER, "every level needs m >= 1");
@@ -176,13 +179,25 @@ Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_ki
   id_ = spec_.to_string();
   if (const char* e = std::getenv("F3RG_NO_REVERSE")) reverse_off_ = e[0] == '1';
   n_ = a_->rows();
+  ld_ = n_;
+  if (ex_) {
+    const PartPlan& p = ex_->plan();
+    if (p.n_own() != n_) throw Error(ERR_DIMENSION, "partition: matrix rows differ from the rank's plan");
+    off_ = p.off();
+    ld_ = p.ld();
+    if (spec_.levels[0].kind != LK_FGMRES)
+      throw Error(ERR_UNSUPPORTED, "row-block partition: the outermost level must be FGMRES");
+    for (const auto& L : spec_.levels)
+      if (L.kind == LK_RICHARDSON && L.m > 2)
+        throw Error(ERR_UNSUPPORTED, "row-block partition: Richardson levels with m > 2 are not implemented");
+  }
   build_levels();
-  capture_inner_graph();
+  if (!ex_) capture_inner_graph();  // partitioned solves launch eagerly
 }
 
 Solver::~Solver() {
   if (inner_exec_) cudaGraphExecDestroy(inner_exec_);
-  if (own_stream_) cudaStreamDestroy(own_stream_);
+  if (own_stream_ && !(ex_ && ex_->stream())) cudaStreamDestroy(own_stream_);
   if (info_host_) cudaFreeHost(info_host_);
   if (io_host_) cudaFreeHost(io_host_);
   if (stage_host_) cudaFreeHost(stage_host_);
@@ -195,7 +210,8 @@ Solver::~Solver() {
 
 void Solver::build_levels() {
   const int D = (int)spec_.levels.size();
-  F3RG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+  if (ex_ && ex_->stream()) own_stream_ = ex_->stream();
+  else F3RG_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
   dead_.alloc(16 * sizeof(int));
   cnt_.alloc(CNT_N * sizeof(unsigned long long));
   partials_.alloc((size_t)max_partial_blocks() * 16 * sizeof(double));
@@ -229,8 +245,14 @@ void Solver::build_levels() {
     }
     if (L.spec.kind == LK_FGMRES) {
       const int m = L.spec.m;
-      L.V.alloc((size_t)(m + 1) * L.vbytes(n_) + 16);
-      L.Z.alloc((size_t)m * L.zbytes(n_) + 16);
+      // basis vectors at stride ld_ (ext layout when partitioned: the owned rows at
+      // off_, halo entries around them)
+      L.V.alloc((size_t)(m + 1) * L.vbytes(ld_) + 16);
+      L.Z.alloc((size_t)m * L.zbytes(ld_) + 16);
+      if (ex_) {
+        F3RG_CUDA(cudaMemset(L.V.get(), 0, L.V.bytes()));
+        F3RG_CUDA(cudaMemset(L.Z.get(), 0, L.Z.bytes()));
+      }
       L.H.alloc((size_t)(m + 1) * m * 8);
       L.cs.alloc((size_t)m * 8);
       L.sn.alloc((size_t)m * 8);
@@ -257,8 +279,12 @@ void Solver::build_levels() {
       L.wused.alloc((size_t)m * 8);
       L.wupd.alloc((size_t)m * 4);
       L.calls.alloc(4 * 8);
-      L.R.alloc(L.vbytes(n_) + 16);
-      L.Za.alloc(L.vbytes(n_) + 16);
+      L.R.alloc(L.vbytes(ld_) + 16);
+      L.Za.alloc(L.vbytes(ld_) + 16);
+      if (ex_) {
+        F3RG_CUDA(cudaMemset(L.R.get(), 0, L.R.bytes()));
+        F3RG_CUDA(cudaMemset(L.Za.get(), 0, L.Za.bytes()));
+      }
       L.Zb.alloc(m > 2 ? L.vbytes(n_) + 16 : 16);
       RichState h;
       h.m = m;
@@ -287,7 +313,7 @@ void Solver::build_levels() {
     std::memcpy(img + 1000, calls, sizeof calls);
   }
   Level& top = *lv_[0];
-  xbuf_.alloc(n_ * psize(top.spec.pv) + 16);
+  xbuf_.alloc(ld_ * psize(top.spec.pv) + 16);
   rbuf_.alloc(n_ * 8 + 16);
   zbuf_.alloc(n_ * 8 + 16);
   if (top.spec.kind == LK_FGMRES) {
@@ -359,19 +385,77 @@ static std::string kname(const char* base, int a, int b, int c) {
 }
 
 // ---- device level chain ----------------------------------------------------------------
+template <class F>
+void Solver::reduce(cudaStream_t s, F&& launch) {
+  if (!ex_) {
+    launch(DistH{});
+    return;
+  }
+  launch(DistH{1, ex_->size(), ex_->loc_buf(), nullptr});
+  ex_->allgather(ex_->loc_buf(), ex_->all_buf(), s);
+  launch(DistH{2, ex_->size(), ex_->loc_buf(), ex_->all_buf()});
+  ex_->done_reduce(s);
+}
+
+void Solver::enqueue_richardson(int l, int j, void* v_ext, const double* sj, void* z_own, cudaStream_t s) {
+  Level& L = *lv_[l - 1];
+  Level& R = *lv_[l];
+  const uint64_t n = n_;
+  int* dead = dead_.get<int>();
+  auto* cnt = cnt_.get<unsigned long long>();
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  const TilesDev T = a_->tiles(R.PA);
+  const double bytes = mbytes(R.PA) + (double)n * (psize(L.W) + psize(R.W));
+  if (!ex_) {
+    PROF(kname("richardson", R.PA, R.W, L.W).c_str(), bytes,
+         launch_richardson(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, v_ext, sj, z_own, n, R.drs, GateH{dead, l}, l,
+                           cnt, sync, bar_.get<unsigned>(), bar_.get<unsigned>() + 1, nullptr));
+    (void)j;
+    return;
+  }
+  // partitioned: halo of v, the plain sweep, then the update-call phases with their
+  // exchanges (every call; the phases return at once unless call_count % c == 0)
+  halo(v_ext, L.W, s);
+  PROF(kname("richardson", R.PA, R.W, L.W).c_str(), bytes,
+       launch_richardson(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, v_ext, sj, z_own, n, R.drs, GateH{dead, l}, l,
+                         cnt, sync, bar_.get<unsigned>(), bar_.get<unsigned>() + 1, nullptr, off_, 1));
+  const int m = R.spec.m;
+  for (int k = 0; k < m; ++k) {
+    if (k > 0) {
+      halo(R.Za.get(), R.W, s);
+      F3RG_CUDA(launch_rich_phase(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, PH_RESID_H, k, v_ext, sj, off_, z_own, n,
+                                  R.drs, R.R.get(), R.Za.get(), GateH{dead, l}, l, cnt, sync, DistH{}));
+      halo(R.R.get(), R.W, s);
+    }
+    F3RG_CUDA(launch_rich_phase(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, PH_DOTS_H, k, v_ext, sj, off_, z_own, n,
+                                R.drs, R.R.get(), R.Za.get(), GateH{dead, l}, l, cnt, sync,
+                                DistH{1, ex_->size(), ex_->loc_buf(), nullptr}));
+    ex_->allgather(ex_->loc_buf(), ex_->all_buf(), s);
+    F3RG_CUDA(launch_rich_phase(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, PH_UPDATE_H, k, v_ext, sj, off_, z_own, n,
+                                R.drs, R.R.get(), R.Za.get(), GateH{dead, l}, l, cnt, sync,
+                                DistH{2, ex_->size(), ex_->loc_buf(), ex_->all_buf()}));
+    ex_->done_reduce(s);
+  }
+  F3RG_CUDA(launch_rich_phase(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, PH_BOOK_H, 0, v_ext, sj, off_, z_own, n,
+                              R.drs, R.R.get(), R.Za.get(), GateH{dead, l}, l, cnt, sync, DistH{}));
+}
+
 void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
   Level& L = *lv_[l];
   const uint64_t n = n_;
-  const double nnz = (double)a_->nnz();
-  void* vj = L.V.get<char>() + (size_t)j * L.vbytes(n);
+  // slot j of V / Z in the ext layout (ld_ stride); *_own: its owned rows
+  char* vj = L.V.get<char>() + (size_t)j * L.vbytes(ld_);
+  char* vj_own = vj + own(L.W);
   const double* sj = L.scale.get<double>() + j;
-  void* zj = L.Z.get<char>() + (size_t)j * L.zbytes(n);
+  char* zj = L.Z.get<char>() + (size_t)j * L.zbytes(ld_);
+  char* zj_own = zj + own(L.PZ);
+  void* V_own = L.V.get<char>() + own(L.W);
   int* dead = dead_.get<int>();
   auto* cnt = cnt_.get<unsigned long long>();
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
   if (L.child == 0) {
     if (top) {
-      io_host_[j] = IoSlot{vj, sj, zj};
+      io_host_[j] = IoSlot{vj_own, sj, zj_own};
       F3RG_CUDA(cudaMemcpyAsync(io_.get(), &io_host_[j], sizeof(IoSlot), cudaMemcpyHostToDevice, s));
       if (has_inner_graph_ && !profiling_now_) {
         F3RG_CUDA(cudaGraphLaunch(inner_exec_, s));
@@ -379,19 +463,15 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
         enqueue_fgmres(l + 1, nullptr, nullptr, nullptr, io_.get<IoSlot>(), s);
       }
     } else {
-      enqueue_fgmres(l + 1, vj, sj, zj, nullptr, s);
+      enqueue_fgmres(l + 1, vj_own, sj, zj_own, nullptr, s);
     }
   } else if (L.child == 1) {
-    Level& R = *lv_[l + 1];
-    const TilesDev T = a_->tiles(R.PA);
-    PROF(kname("richardson", R.PA, R.W, L.W).c_str(),
-         mbytes(R.PA) + (double)n * (psize(L.W) + psize(R.W)),
-         launch_richardson(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, vj, sj, zj, n, R.drs, GateH{dead, l + 1}, l + 1,
-                           cnt, sync, bar_.get<unsigned>(), bar_.get<unsigned>() + 1, nullptr));
+    enqueue_richardson(l + 1, j, vj, sj, zj_own, s);
   } else {
     PROF(kname("copy_scaled", L.W, L.W, L.W).c_str(), 2.0 * n * psize(L.W),
-         launch_copy_scaled(L.W, Launch{0, s}, vj, sj, zj, n, GateH{dead, l + 1}, cnt));
+         launch_copy_scaled(L.W, Launch{0, s}, vj_own, sj, zj_own, n, GateH{dead, l + 1}, cnt));
   }
+  halo(zj, L.PZ, s);  // z_j is the SpMV input
   TilesDev T = a_->tiles(L.PA);
   // right after a Richardson pass over the same replica: walk the tiles backwards
   // so the pass starts on the tail end that is still in L2
@@ -403,16 +483,24 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
   // for the fused-step kernel.
   const int defer = 0;
   int dgrid = 0;
-  PROF(kname("spmv_dots", L.PA, L.PZ, L.W).c_str(),
-       mbytes(L.PA) + (double)n * (psize(L.PZ) + psize(L.W)) + (double)nd * n * psize(L.W),
-       launch_spmv_dots(L.PA, L.PZ, L.W, Launch{0, s}, a_->csr(), T, zj, L.V.get(), n, j, L.dstate,
-                        GateH{dead, l + 1}, sync, dpartials_.get<double>(), defer, &dgrid));
+  reduce(s, [&](DistH d) {
+    PROF(kname("spmv_dots", L.PA, L.PZ, L.W).c_str(),
+         d.mode == 2 ? 0.0 : mbytes(L.PA) + (double)n * (psize(L.PZ) + psize(L.W)) + (double)nd * n * psize(L.W),
+         launch_spmv_dots(L.PA, L.PZ, L.W, Launch{0, s}, a_->csr(), T, zj, V_own, ld_, j, L.dstate,
+                          GateH{dead, l + 1}, sync, dpartials_.get<double>(), defer, &dgrid, d));
+  });
   for (int k0 = 8; k0 <= j; k0 += 8)
-    PROF(kname("multi_dot", L.W, L.W, L.W).c_str(), (double)n * psize(L.W) * (1 + std::min(8, j + 1 - k0)),
-         launch_multi_dot(L.W, Launch{0, s}, L.V.get(), n, j, k0, L.dstate, GateH{dead, l + 1}, sync));
-  PROF(kname("cgs", L.W, L.W, L.W).c_str(), (double)n * psize(L.W) * (j + 3),
-       launch_cgs(L.W, Launch{0, s}, L.V.get(), n, j, L.dstate, dead, GateH{dead, l + 1}, l, top ? 1 : 0, top ? 1 : 0,
-                  top ? info_.get<StepInfo>() : nullptr, sync, defer ? dpartials_.get<double>() : nullptr, dgrid));
+    reduce(s, [&](DistH d) {
+      PROF(kname("multi_dot", L.W, L.W, L.W).c_str(),
+           d.mode == 2 ? 0.0 : (double)n * psize(L.W) * (1 + std::min(8, j + 1 - k0)),
+           launch_multi_dot(L.W, Launch{0, s}, V_own, n, j, k0, L.dstate, GateH{dead, l + 1}, sync, ld_, d));
+    });
+  reduce(s, [&](DistH d) {
+    PROF(kname("cgs", L.W, L.W, L.W).c_str(), d.mode == 2 ? 0.0 : (double)n * psize(L.W) * (j + 3),
+         launch_cgs(L.W, Launch{0, s}, V_own, n, j, L.dstate, dead, GateH{dead, l + 1}, l, top ? 1 : 0, top ? 1 : 0,
+                    top ? info_.get<StepInfo>() : nullptr, sync, defer ? dpartials_.get<double>() : nullptr, dgrid,
+                    ld_, d));
+  });
 }
 
 void Solver::enqueue_fgmres(int l, void* src, const double* src_scale, void* dst, const IoSlot* io, cudaStream_t s) {
@@ -422,12 +510,15 @@ void Solver::enqueue_fgmres(int l, void* src, const double* src_scale, void* dst
   int* dead = dead_.get<int>();
   auto* cnt = cnt_.get<unsigned long long>();
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
-  PROF(kname("level_start", P.W, L.W, L.W).c_str(), (double)n * (2 * psize(P.W) + psize(L.W)),
-       launch_level_start(P.W, L.W, Launch{0, s}, src, src_scale, 0, L.V.get(), n, L.dstate, dead, GateH{dead, l}, l,
-                          cnt, sync, io));
+  reduce(s, [&](DistH d) {
+    PROF(kname("level_start", P.W, L.W, L.W).c_str(), d.mode == 2 ? 0.0 : (double)n * (2 * psize(P.W) + psize(L.W)),
+         launch_level_start(P.W, L.W, Launch{0, s}, src, src_scale, 0, L.V.get<char>() + own(L.W), n, L.dstate, dead,
+                            GateH{dead, l}, l, cnt, sync, io, d));
+  });
   for (int j = 0; j < L.spec.m; ++j) enqueue_child_step(l, j, s, false);
   PROF(kname("level_finish", L.PZ, L.W, L.W).c_str(), (double)n * (L.spec.m * psize(L.PZ) + psize(L.W)),
-       launch_level_finish(L.PZ, L.W, L.W, Launch{0, s}, L.Z.get(), n, L.dstate, dst, 1, GateH{dead, l}, l, cnt, 1, io));
+       launch_level_finish(L.PZ, L.W, L.W, Launch{0, s}, L.Z.get<char>() + own(L.PZ), n, L.dstate, dst, 1,
+                           GateH{dead, l}, l, cnt, 1, io, ld_));
 }
 
 void Solver::capture_inner_graph() {
@@ -460,11 +551,13 @@ double Solver::read_double(const double* dev, cudaStream_t s) {
 
 double Solver::true_rel(const double* b, double bnorm, cudaStream_t s) {
   Level& top = *lv_[0];
-  const double nnz = (double)a_->nnz();
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
-  PROF(kname("residual", 2, top.spec.pv, 2).c_str(), mbytes(2) + (double)n_ * (psize(top.spec.pv) + 16),
-       launch_residual(2, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(2), xbuf_.get(), b, rbuf_.get(), nullptr,
-                       norm_.get<double>(), sync));
+  halo(xbuf_.get(), top.spec.pv, s);
+  reduce(s, [&](DistH d) {
+    PROF(kname("residual", 2, top.spec.pv, 2).c_str(), d.mode == 2 ? 0.0 : mbytes(2) + (double)n_ * (psize(top.spec.pv) + 16),
+         launch_residual(2, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(2), xbuf_.get(), b, rbuf_.get(),
+                         nullptr, norm_.get<double>(), sync, d));
+  });
   return read_double(norm_.get<double>(), s) / bnorm;
 }
 
@@ -486,7 +579,9 @@ Report Solver::run(const double* b, double* x_out, const RunOptions& opts, cudaS
   F3RG_CUDA(cudaMemsetAsync(dead_.get(), 0, dead_.bytes(), s));
   F3RG_CUDA(cudaMemsetAsync(xbuf_.get(), 0, xbuf_.bytes(), s));
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
-  PROF("norm2[b]", 8.0 * n_, launch_norm2(2, Launch{0, s}, b, n_, norm_.get<double>(), sync));
+  reduce(s, [&](DistH d) {
+    PROF("norm2[b]", d.mode == 2 ? 0.0 : 8.0 * n_, launch_norm2(2, Launch{0, s}, b, n_, norm_.get<double>(), sync, d));
+  });
   const double bnorm = read_double(norm_.get<double>(), s);
   if (bnorm == 0.0) {
     rep.converged = true;
@@ -507,7 +602,7 @@ Report Solver::run(const double* b, double* x_out, const RunOptions& opts, cudaS
   for (int d = 1; d < D; ++d) rep.level_iterations[d] = cnt[CNT_IT + d];
   rep.level_iterations[0] = lv_[0]->spec.kind == LK_FGMRES ? rep.outer_iterations : cnt[CNT_IT + 0];
   rep.omegas_final = innermost_omegas();
-  if (x_out) F3RG_CUDA(launch_copy(lv_[0]->spec.pv, 2, Launch{0, s}, xbuf_.get(), x_out, n_));
+  if (x_out) F3RG_CUDA(launch_copy(lv_[0]->spec.pv, 2, Launch{0, s}, xbuf_.get<char>() + own(lv_[0]->spec.pv), x_out, n_));
   F3RG_CUDA(cudaStreamSynchronize(s));
   profiling_now_ = false;
   rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -534,14 +629,19 @@ Report Solver::run_fgmres_top(const double* b, const RunOptions& opts, cudaStrea
     // ---- one cycle (src/fgmres.cpp:21-148) ----
     const bool first = executions == 0;
     if (first) {  // r = b
-      PROF("level_start[f64,f64,f64]", 16.0 * n,
-           launch_level_start(2, 2, Launch{0, s}, const_cast<double*>(b), nullptr, 0, top.V.get(), n, top.dstate, dead,
-                              GateH{dead, 0}, 0, cnt, sync, nullptr));
+      reduce(s, [&](DistH d) {
+        PROF("level_start[f64,f64,f64]", d.mode == 2 ? 0.0 : 16.0 * n,
+             launch_level_start(2, 2, Launch{0, s}, const_cast<double*>(b), nullptr, 0, top.V.get<char>() + own(2), n,
+                                top.dstate, dead, GateH{dead, 0}, 0, cnt, sync, nullptr, d));
+      });
     } else {  // r = b - A x
-      PROF(kname("residual", top.PA, top.spec.pv, 2).c_str(),
-           mbytes(top.PA) + (double)n * (psize(top.spec.pv) + 16),
-           launch_residual(top.PA, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(top.PA), xbuf_.get(), b,
-                           top.V.get(), top.dstate, nullptr, sync));
+      halo(xbuf_.get(), top.spec.pv, s);
+      reduce(s, [&](DistH d) {
+        PROF(kname("residual", top.PA, top.spec.pv, 2).c_str(),
+             d.mode == 2 ? 0.0 : mbytes(top.PA) + (double)n * (psize(top.spec.pv) + 16),
+             launch_residual(top.PA, top.spec.pv, 2, Launch{0, s}, a_->csr(), a_->tiles(top.PA), xbuf_.get(), b,
+                             top.V.get<char>() + own(2), top.dstate, nullptr, sync, d));
+      });
     }
     F3RG_CUDA(cudaMemsetAsync(dead, 0, sizeof(int), s));
     F3RG_CUDA(cudaMemcpyAsync(stage_host_, top.dstate, sizeof(LevelState), cudaMemcpyDeviceToHost, s));
@@ -583,8 +683,8 @@ Report Solver::run_fgmres_top(const double* b, const RunOptions& opts, cudaStrea
       // back-substitution + x += Z y
       PROF(kname("level_finish", top.PZ, top.W, top.spec.pv).c_str(),
            (double)n * (iterations * psize(top.PZ) + 2 * psize(top.spec.pv)),
-           launch_level_finish(top.PZ, top.W, top.spec.pv, Launch{0, s}, top.Z.get(), n, top.dstate, xbuf_.get(), 0,
-                               GateH{dead, 0}, 0, cnt, 0, nullptr));
+           launch_level_finish(top.PZ, top.W, top.spec.pv, Launch{0, s}, top.Z.get<char>() + own(top.PZ), n, top.dstate,
+                               xbuf_.get<char>() + own(top.spec.pv), 0, GateH{dead, 0}, 0, cnt, 0, nullptr, ld_));
     }
     rep.outer_iterations += (unsigned long long)iterations;
     if (diverged) {

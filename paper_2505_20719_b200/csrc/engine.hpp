@@ -6,12 +6,15 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "partition.hpp"
 #include "state.hpp"
 
 namespace f3rg {
@@ -113,8 +116,10 @@ uint32_t tile_max_rows();
 class DeviceMatrix {
  public:
   // validates like SparseCsr::validate (src/csr.cpp:51-69) and uploads one shared
-  // index copy plus the fp64 / fp32 / fp16 value replicas (RNE demotions, :83-92)
-  DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values);
+  // index copy plus the fp64 / fp32 / fp16 value replicas (RNE demotions, :83-92).
+  // ncols > n: a rank's rows of a partitioned matrix, columns in its ext layout
+  DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values,
+               uint64_t ncols = 0);
   uint64_t rows() const { return n_; }
   uint64_t nnz() const { return nnz_; }
   CsrDev csr() const;
@@ -128,7 +133,100 @@ class DeviceMatrix {
   uint32_t ntiles_[3] = {0, 0, 0};
 };
 
-void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci);
+void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci, uint64_t ncols = 0);
+
+// ---- cross-rank exchange of the row-block partition ------------
+// Every rank calls the same sequence of halo()/allgather() (its host control flow
+// depends only on replicated scalars), so the exchanges always pair up.
+class Exchange {
+ public:
+  virtual ~Exchange() = default;
+  virtual int size() const = 0;
+  virtual int rank() const = 0;
+  virtual const PartPlan& plan() const = 0;
+  // fill the halo entries of an ext-layout vector (precision prec) from the peers
+  virtual void halo(void* ext, int prec, cudaStream_t s) = 0;
+  // loc[0..16) of every rank -> all[r * 16 + k]; then the caller launches the tail;
+  // then done_reduce()
+  virtual void allgather(double* loc, double* all, cudaStream_t s) = 0;
+  virtual void done_reduce(cudaStream_t) {}
+  // where this rank's kernels publish their totals (allgather's loc) and read all
+  virtual double* loc_buf() = 0;
+  virtual double* all_buf() = 0;
+  // stream the rank's solver must use (nullptr: its own)
+  virtual cudaStream_t stream() const { return nullptr; }
+};
+
+// P ranks of one process sharing the current device and ONE stream (each rank's
+// solver runs on its own host thread). Halo entries are gathered straight from the
+// peers' owned rows. Test vehicle for the partition on a one-GPU box: the data flow
+// and arithmetic are those of the multi-process NCCL backend.
+class LocalGroup {
+ public:
+  LocalGroup(int P);
+  ~LocalGroup();
+  int P;
+  cudaStream_t stream = nullptr;
+  std::vector<PartPlan> plans;
+  // sidx[q][p]: device copy of plans[q].send_idx[p]
+  std::vector<std::vector<DevBuf>> sidx;
+  std::vector<void*> ptrs;  // ext pointers published at a halo exchange
+  DevBuf all;               // P x 16 doubles: row r is rank r's loc
+  void barrier();
+  void fail();              // a rank failed: release everyone (barrier() then throws)
+  // rank r's halo entries of an ext vector, gathered from the owned rows the peers
+  // published in ptrs[] (precision prec)
+  void gather_into(int r, void* ext, int prec, cudaStream_t s);
+  void set_plans(uint64_t n, const uint32_t* rp, const uint32_t* ci);
+
+ private:
+  std::mutex mu_;
+  std::condition_variable cv_;
+  int arrived_ = 0;
+  unsigned long long gen_ = 0;
+  bool failed_ = false;
+};
+
+class LocalExchange : public Exchange {
+ public:
+  LocalExchange(LocalGroup* g, int r) : g_(g), r_(r) {}
+  int size() const override { return g_->P; }
+  int rank() const override { return r_; }
+  const PartPlan& plan() const override { return g_->plans[r_]; }
+  void halo(void* ext, int prec, cudaStream_t s) override;
+  void allgather(double* loc, double* all, cudaStream_t s) override;
+  void done_reduce(cudaStream_t s) override;
+  double* loc_buf() override { return g_->all.get<double>() + (size_t)r_ * 16; }
+  double* all_buf() override { return g_->all.get<double>(); }
+  cudaStream_t stream() const override { return g_->stream; }
+
+ private:
+  LocalGroup* g_;
+  int r_;
+};
+
+// one rank per process (torch.distributed launch), NCCL point-to-point halos and
+// allgather, loaded at run time from the libnccl.so.2 the process already maps
+class NcclExchange : public Exchange {
+ public:
+  NcclExchange(int P, int rank, const void* unique_id, uint64_t n, const uint32_t* rp, const uint32_t* ci);
+  ~NcclExchange() override;
+  int size() const override { return plan_.P; }
+  int rank() const override { return plan_.rank; }
+  const PartPlan& plan() const override { return plan_; }
+  void halo(void* ext, int prec, cudaStream_t s) override;
+  void allgather(double* loc, double* all, cudaStream_t s) override;
+  double* loc_buf() override { return loc_.get<double>(); }
+  double* all_buf() override { return all_.get<double>(); }
+  static void unique_id(void* out128);
+
+ private:
+  PartPlan plan_;
+  void* comm_ = nullptr;
+  std::vector<DevBuf> sidx_;  // per peer: owned indices to send
+  std::vector<uint64_t> soff_;
+  DevBuf sendbuf_, loc_, all_;
+};
 
 // ---- composed solver (reference include/f3r/nesting.hpp:55-77) ------------------------
 struct RunOptions {
@@ -153,7 +251,9 @@ struct Report {
 
 class Solver {
  public:
-  Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind);
+  // ex != nullptr: this solver is one rank of a row-block partition; `a` holds the
+  // rank's rows (columns in its ext layout) and every vector is the rank's slice
+  Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind, Exchange* ex = nullptr);
   ~Solver();
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
@@ -168,6 +268,7 @@ class Solver {
   const std::string& id() const { return id_; }
   uint64_t rows() const { return a_->rows(); }
   cudaStream_t stream() const { return own_stream_; }
+  Exchange* exchange() const { return ex_; }
   // per-kernel timing of the NEXT run (CUDA events around every launch, eager mode)
   void set_profile(bool on) { profile_ = on; }
   struct KernelTime {
@@ -192,12 +293,23 @@ class Solver {
   double mbytes(int pa) const;
   void prof_begin(cudaStream_t s);
   void prof_end(cudaStream_t s, const char* name, double bytes);
+  void halo(void* ext, int prec, cudaStream_t s) {
+    if (ex_) ex_->halo(ext, prec, s);
+  }
+  // P == 1: launch(DistH{}) once. P > 1: rank-local launch, allgather, tail launch.
+  template <class F>
+  void reduce(cudaStream_t s, F&& launch);
+  void enqueue_richardson(int l, int j, void* v_ext, const double* sj, void* z_own, cudaStream_t s);
+  size_t own(int p) const { return off_ * (p == 0 ? 2 : p == 1 ? 4 : 8); }  // byte offset of the owned rows
 
   Spec spec_;
   std::string id_;
   std::shared_ptr<DeviceMatrix> a_;
   std::vector<std::unique_ptr<Level>> lv_;
-  uint64_t n_ = 0;
+  uint64_t n_ = 0;    // rows of this rank (all rows on one rank)
+  uint64_t ld_ = 0;   // vector stride of a basis (ext layout; = n_ on one rank)
+  uint64_t off_ = 0;  // owned rows start here in an ext-layout vector
+  Exchange* ex_ = nullptr;
   DevBuf dead_, cnt_, partials_, dpartials_, counter_, bar_, info_, io_, norm_, xbuf_, rbuf_, zbuf_;
   StepInfo* info_host_ = nullptr;
   IoSlot* io_host_ = nullptr;

@@ -24,6 +24,14 @@ struct SyncH {
   unsigned* counter;
 };
 
+// cross-rank reduction stage (levels.cuh Dist); mode 0 = single rank
+struct DistH {
+  int mode = 0;
+  int P = 1;
+  double* loc = nullptr;
+  const double* all = nullptr;
+};
+
 struct Launch {
   int grid = 0;  // 0: launcher picks (persistent, occupancy-sized)
   cudaStream_t stream = nullptr;
@@ -38,29 +46,37 @@ int sm_count();
 // ---- FGMRES level ------------------------------------------------------------------
 cudaError_t launch_level_start(int ps, int pw, Launch l, void* src, const double* src_scale, int writeback, void* dst,
                                uint64_t n, LevelState* L, int* dead, GateH gate, int level, unsigned long long* cnt,
-                               SyncH sync, const IoSlot* io);
+                               SyncH sync, const IoSlot* io, DistH dist = {});
 cudaError_t launch_copy_scaled(int pw, Launch l, void* v, const double* scale, void* z, uint64_t n, GateH gate,
                                unsigned long long* cnt);
-// dots: per-CTA partials (grid x 16 doubles); defer: leave their reduction to k_cgs
+// dots: per-CTA partials (grid x 16 doubles); defer: leave their reduction to k_cgs.
+// V: slot 0 of the basis (owned rows), ld: slot stride; z: the SpMV input (ext layout)
 cudaError_t launch_spmv_dots(int pa, int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z,
-                             void* V, uint64_t n, int j, LevelState* L, GateH gate, SyncH sync, double* dots,
-                             int defer, int* grid_out);
+                             void* V, uint64_t ld, int j, LevelState* L, GateH gate, SyncH sync, double* dots,
+                             int defer, int* grid_out, DistH dist = {});
 cudaError_t launch_multi_dot(int pw, Launch l, const void* V, uint64_t n, int j, int k0, LevelState* L, GateH gate,
-                             SyncH sync);
+                             SyncH sync, uint64_t ldv = 0, DistH dist = {});
 cudaError_t launch_cgs(int pw, Launch l, void* V, uint64_t n, int j, LevelState* L, int* dead, GateH gate, int level,
-                       int outer, int use_tol, StepInfo* info, SyncH sync, const double* dots, int dots_grid);
+                       int outer, int use_tol, StepInfo* info, SyncH sync, const double* dots, int dots_grid,
+                       uint64_t ldv = 0, DistH dist = {});
 cudaError_t launch_level_finish(int pz, int pw, int px, Launch l, const void* Z, uint64_t n, LevelState* L, void* x,
                                 int x_is_zero, GateH gate, int level, unsigned long long* cnt, int count_iterations,
-                                const IoSlot* io);
+                                const IoSlot* io, uint64_t ldz = 0);
 cudaError_t launch_residual(int pa, int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
-                            const double* b, void* r, LevelState* L, double* out_norm, SyncH sync);
+                            const double* b, void* r, LevelState* L, double* out_norm, SyncH sync, DistH dist = {});
 cudaError_t launch_set_outer(Launch l, LevelState* L, double bnorm, double tol);
 
 // ---- Richardson (cooperative) ----------------------------------------------------
 cudaError_t launch_richardson(int pa, int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, const void* v,
                               const double* v_scale, void* out, uint64_t n, RichState* RS, GateH gate, int level,
                               unsigned long long* cnt, SyncH sync, unsigned* bar_count, unsigned* bar_gen,
-                              const IoSlot* io);
+                              const IoSlot* io, uint64_t voff = 0, int flags = 0);
+// one phase of a partitioned Richardson call (richardson.cuh k_rich_phase, PH_*)
+enum { PH_RESID_H = 0, PH_DOTS_H = 1, PH_UPDATE_H = 2, PH_BOOK_H = 3 };
+cudaError_t launch_rich_phase(int pa, int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, int phase, int k,
+                              const void* v, const double* v_scale, uint64_t off, void* out, uint64_t n,
+                              RichState* RS, void* R, void* Za, GateH gate, int level, unsigned long long* cnt,
+                              SyncH sync, DistH dist);
 
 // ---- BLAS-1 / SpMV (kernel-level entry points) ----------------------------------
 cudaError_t launch_fill(int p, Launch l, void* x, uint64_t n, double value);
@@ -72,8 +88,10 @@ cudaError_t launch_add_scaled(int px, int py, int po, Launch l, const void* x, d
 // dot at C = max(floor, px, py) -> *out (device); norm: sqrt at precision px of the
 // result rounded to px (norm2 semantics, x == y)
 cudaError_t launch_dot(int px, int py, int floor_p, Launch l, const void* x, const void* y, uint64_t n, double* out,
-                       SyncH sync);
-cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* out, SyncH sync);
+                       SyncH sync, DistH dist = {});
+cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* out, SyncH sync, DistH dist = {});
+// dst[i] = src[idx[i]], i < cnt, at precision p (halo pack / gather)
+cudaError_t launch_gather(int p, Launch l, const void* src, const uint32_t* idx, uint64_t cnt, void* dst);
 cudaError_t launch_spmv(int pa, int px, int py, Launch l, const CsrDev& A, const TilesDev& T, const void* x, void* y);
 
 }  // namespace f3rg

@@ -49,27 +49,35 @@ cudaError_t launch_add_scaled(int px, int py, int po, Launch l, const void* x, d
 }
 
 cudaError_t launch_dot(int px, int py, int floor_p, Launch l, const void* x, const void* y, uint64_t n, double* out,
-                       SyncH sync) {
-  const int g = l.grid ? l.grid : stream_grid();
+                       SyncH sync, DistH dist) {
+  const int g = dist.mode == 2 ? 1 : l.grid ? l.grid : stream_grid();
   const int c = floor_p > px ? (floor_p > py ? floor_p : py) : (px > py ? px : py);
   with_p(px, [&](auto X) {
     with_p(py, [&](auto Y) {
       with_p(c, [&](auto C) {
         constexpr int CX = decltype(C)::value, PX = decltype(X)::value, PY = decltype(Y)::value;
         if constexpr (CX >= PX && CX >= PY)
-          k_dot<PX, PY, CX, false, CX><<<g, kThreads, 0, l.stream>>>(x, y, n, out, to_sync(sync));
+          k_dot<PX, PY, CX, false, CX><<<g, kThreads, 0, l.stream>>>(x, y, n, out, to_sync(sync), to_dist(dist));
       });
     });
   });
   return cudaGetLastError();
 }
 
-cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* out, SyncH sync) {
-  const int g = l.grid ? l.grid : stream_grid();
+cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* out, SyncH sync, DistH dist) {
+  const int g = dist.mode == 2 ? 1 : l.grid ? l.grid : stream_grid();
   with_p(px, [&](auto X) {
     constexpr int PX = decltype(X)::value;
-    k_dot<PX, PX, PX, true, PX><<<g, kThreads, 0, l.stream>>>(x, x, n, out, to_sync(sync));
+    k_dot<PX, PX, PX, true, PX><<<g, kThreads, 0, l.stream>>>(x, x, n, out, to_sync(sync), to_dist(dist));
   });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(int p, Launch l, const void* src, const uint32_t* idx, uint64_t cnt, void* dst) {
+  if (cnt == 0) return cudaSuccess;
+  const uint64_t want = (cnt + kThreads - 1) / kThreads;
+  const int g = l.grid ? l.grid : (int)(want < (uint64_t)stream_grid() ? want : (uint64_t)stream_grid());
+  with_p(p, [&](auto P) { k_gather<decltype(P)::value><<<g, kThreads, 0, l.stream>>>(src, idx, cnt, dst); });
   return cudaGetLastError();
 }
 

@@ -18,12 +18,12 @@ int max_partial_blocks() { return sm_count() * 8; }
 
 cudaError_t launch_level_start(int ps, int pw, Launch l, void* src, const double* src_scale, int writeback, void* dst,
                                uint64_t n, LevelState* L, int* dead, GateH gate, int level, unsigned long long* cnt,
-                               SyncH sync, const IoSlot* io) {
-  const int g = l.grid ? l.grid : stream_grid();
+                               SyncH sync, const IoSlot* io, DistH dist) {
+  const int g = dist.mode == 2 ? 1 : l.grid ? l.grid : stream_grid();
   with_p(ps, [&](auto S) {
     with_p(pw, [&](auto W) {
       k_level_start<decltype(S)::value, decltype(W)::value><<<g, kThreads, 0, l.stream>>>(
-          src, src_scale, writeback, dst, n, L, dead, to_gate(gate), level, cnt, to_sync(sync), io);
+          src, src_scale, writeback, dst, n, L, dead, to_gate(gate), level, cnt, to_sync(sync), io, to_dist(dist));
     });
   });
   return cudaGetLastError();
@@ -39,34 +39,37 @@ cudaError_t launch_copy_scaled(int pw, Launch l, void* v, const double* scale, v
 }
 
 cudaError_t launch_multi_dot(int pw, Launch l, const void* V, uint64_t n, int j, int k0, LevelState* L, GateH gate,
-                             SyncH sync) {
-  const int g = l.grid ? l.grid : stream_grid();
+                             SyncH sync, uint64_t ldv, DistH dist) {
+  const int g = dist.mode == 2 ? 1 : l.grid ? l.grid : stream_grid();
   with_p(pw, [&](auto W) {
-    k_multi_dot<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(V, n, j, k0, L, to_gate(gate), to_sync(sync));
+    k_multi_dot<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(V, n, ldv ? ldv : n, j, k0, L, to_gate(gate),
+                                                                  to_sync(sync), to_dist(dist));
   });
   return cudaGetLastError();
 }
 
 cudaError_t launch_cgs(int pw, Launch l, void* V, uint64_t n, int j, LevelState* L, int* dead, GateH gate, int level,
-                       int outer, int use_tol, StepInfo* info, SyncH sync, const double* dots, int dots_grid) {
+                       int outer, int use_tol, StepInfo* info, SyncH sync, const double* dots, int dots_grid,
+                       uint64_t ldv, DistH dist) {
   // 2 CTAs per SM with 16-byte loads measured fastest (tools/tile_microbench.cu)
-  const int g = l.grid ? l.grid : sm_count() * 2;
+  const int g = dist.mode == 2 ? 1 : l.grid ? l.grid : sm_count() * 2;
   with_p(pw, [&](auto W) {
-    k_cgs<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(V, n, j, L, dead, to_gate(gate), level, outer, use_tol,
-                                                            info, to_sync(sync), dots, dots_grid);
+    k_cgs<decltype(W)::value><<<g, kThreads, 0, l.stream>>>(V, n, ldv ? ldv : n, j, L, dead, to_gate(gate), level,
+                                                            outer, use_tol, info, to_sync(sync), dots, dots_grid,
+                                                            to_dist(dist));
   });
   return cudaGetLastError();
 }
 
 cudaError_t launch_level_finish(int pz, int pw, int px, Launch l, const void* Z, uint64_t n, LevelState* L, void* x,
                                 int x_is_zero, GateH gate, int level, unsigned long long* cnt, int count_iterations,
-                                const IoSlot* io) {
+                                const IoSlot* io, uint64_t ldz) {
   const int g = l.grid ? l.grid : stream_grid();
   with_p(pz, [&](auto PZ) {
     with_p(pw, [&](auto W) {
       with_p(px, [&](auto X) {
         k_level_finish<decltype(PZ)::value, decltype(W)::value, decltype(X)::value><<<g, kThreads, 0, l.stream>>>(
-            Z, n, L, x, x_is_zero, to_gate(gate), level, cnt, count_iterations, io);
+            Z, n, ldz ? ldz : n, L, x, x_is_zero, to_gate(gate), level, cnt, count_iterations, io);
       });
     });
   });

@@ -13,16 +13,16 @@ namespace f3rg {
   }
 
 cudaError_t launch_spmv_dots(int pa, int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z,
-                             void* V, uint64_t n, int j, LevelState* L, GateH gate, SyncH sync, double* dots,
-                             int defer, int* grid_out) {
-#define C_(P) launch_spmv_dots_t<P>(pz, pw, l, A, T, z, V, n, j, L, gate, sync, dots, defer, grid_out)
+                             void* V, uint64_t ld, int j, LevelState* L, GateH gate, SyncH sync, double* dots,
+                             int defer, int* grid_out, DistH dist) {
+#define C_(P) launch_spmv_dots_t<P>(pz, pw, l, A, T, z, V, ld, j, L, gate, sync, dots, defer, grid_out, dist)
   F3RG_BY_PA(pa, C_)
 #undef C_
 }
 
 cudaError_t launch_residual(int pa, int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
-                            const double* b, void* r, LevelState* L, double* out_norm, SyncH sync) {
-#define C_(P) launch_residual_t<P>(px, pw, l, A, T, x, b, r, L, out_norm, sync)
+                            const double* b, void* r, LevelState* L, double* out_norm, SyncH sync, DistH dist) {
+#define C_(P) launch_residual_t<P>(px, pw, l, A, T, x, b, r, L, out_norm, sync, dist)
   F3RG_BY_PA(pa, C_)
 #undef C_
 }
@@ -36,8 +36,19 @@ cudaError_t launch_spmv(int pa, int px, int py, Launch l, const CsrDev& A, const
 cudaError_t launch_richardson(int pa, int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, const void* v,
                               const double* v_scale, void* out, uint64_t n, RichState* RS, GateH gate, int level,
                               unsigned long long* cnt, SyncH sync, unsigned* bar_count, unsigned* bar_gen,
-                              const IoSlot* io) {
-#define C_(P) launch_richardson_t<P>(pw, pv, l, A, T, v, v_scale, out, n, RS, gate, level, cnt, sync, bar_count, bar_gen, io)
+                              const IoSlot* io, uint64_t voff, int flags) {
+#define C_(P) \
+  launch_richardson_t<P>(pw, pv, l, A, T, v, v_scale, out, n, RS, gate, level, cnt, sync, bar_count, bar_gen, io, voff, flags)
+  F3RG_BY_PA(pa, C_)
+#undef C_
+}
+
+cudaError_t launch_rich_phase(int pa, int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, int phase, int k,
+                              const void* v, const double* v_scale, uint64_t off, void* out, uint64_t n,
+                              RichState* RS, void* R, void* Za, GateH gate, int level, unsigned long long* cnt,
+                              SyncH sync, DistH dist) {
+#define C_(P) \
+  launch_rich_phase_t<P>(pw, pv, l, A, T, phase, k, v, v_scale, off, out, n, RS, R, Za, gate, level, cnt, sync, dist)
   F3RG_BY_PA(pa, C_)
 #undef C_
 }

@@ -23,8 +23,8 @@ inline int tile_kernel_grid(K kern, int smem, uint32_t ntiles, bool cap_by_tiles
 
 template <int PA>
 cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* z, void* V,
-                               uint64_t n, int j, LevelState* L, GateH gate, SyncH sync, double* dots, int defer,
-                               int* grid_out) {
+                               uint64_t ld, int j, LevelState* L, GateH gate, SyncH sync, double* dots, int defer,
+                               int* grid_out, DistH dist) {
   cudaError_t err = cudaErrorInvalidValue;
   auto go = [&](auto IDX_) {
     constexpr int IDX = decltype(IDX_)::value;
@@ -36,9 +36,12 @@ cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const 
         if constexpr (PZ <= PW) {
           auto kern = k_spmv_dots<PA, PZ, PW, IDX>;
           static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-          const int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          if (dist.mode == 2) g = 1;
+          if (g < 1) g = 1;
           if (grid_out) *grid_out = g;
-          kern<<<g, kThreads, SM, l.stream>>>(A, T, z, V, n, j, L, to_gate(gate), to_sync(sync), dots, defer);
+          kern<<<g, kThreads, SM, l.stream>>>(A, T, z, V, ld, j, L, to_gate(gate), to_sync(sync), dots, defer,
+                                              to_dist(dist));
           err = cudaGetLastError();
         }
       });
@@ -51,7 +54,7 @@ cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const 
 
 template <int PA>
 cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const TilesDev& T, const void* x,
-                              const double* b, void* r, LevelState* L, double* out_norm, SyncH sync) {
+                              const double* b, void* r, LevelState* L, double* out_norm, SyncH sync, DistH dist) {
   cudaError_t err = cudaErrorInvalidValue;
   auto go = [&](auto IDX_) {
     constexpr int IDX = decltype(IDX_)::value;
@@ -63,8 +66,10 @@ cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const T
         if constexpr (PW >= PX) {
           auto kern = k_residual<PA, PX, PW, IDX>;
           static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-          const int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
-          kern<<<g, kThreads, SM, l.stream>>>(A, T, x, b, r, L, out_norm, to_sync(sync));
+          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          if (dist.mode == 2) g = 1;
+          if (g < 1) g = 1;
+          kern<<<g, kThreads, SM, l.stream>>>(A, T, x, b, r, L, out_norm, to_sync(sync), to_dist(dist));
           err = cudaGetLastError();
         }
       });
@@ -101,7 +106,7 @@ template <int PA>
 cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, const void* v,
                                 const double* v_scale, void* out, uint64_t n, RichState* RS, GateH gate, int level,
                                 unsigned long long* cnt, SyncH sync, unsigned* bar_count, unsigned* bar_gen,
-                                const IoSlot* io) {
+                                const IoSlot* io, uint64_t voff, int flags) {
   cudaError_t err = cudaErrorInvalidValue;
   auto go = [&](auto IDX_) {
     constexpr int IDX = decltype(IDX_)::value;
@@ -125,8 +130,39 @@ cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const
           cfg.attrs = attr;
           cfg.numAttrs = 1;
           err = cudaLaunchKernelEx(&cfg, kern, A, T, v, v_scale, out, n, RS, to_gate(gate), level, cnt, to_sync(sync),
-                                   bar_count, bar_gen, io);
+                                   bar_count, bar_gen, io, voff, flags);
           if (err == cudaSuccess) err = cudaGetLastError();
+        }
+      });
+    });
+  };
+  if (A.dcol) go(std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 0>{});
+  return err;
+}
+
+template <int PA>
+cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, int phase, int k,
+                                const void* v, const double* v_scale, uint64_t off, void* out, uint64_t n,
+                                RichState* RS, void* R, void* Za, GateH gate, int level, unsigned long long* cnt,
+                                SyncH sync, DistH dist) {
+  cudaError_t err = cudaErrorInvalidValue;
+  auto go = [&](auto IDX_) {
+    constexpr int IDX = decltype(IDX_)::value;
+    constexpr int SM = TileCfg<PA, IDX>::SMEM_BYTES;
+    with_p(pv, [&](auto V) {
+      constexpr int PV = decltype(V)::value;
+      with_p(pw, [&](auto W) {
+        constexpr int PW = decltype(W)::value;
+        if constexpr (PW <= PV) {
+          auto kern = k_rich_phase<PA, PW, PV, IDX>;
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
+          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          if (phase == PH_BOOK) g = 1;
+          if (g < 1) g = 1;
+          kern<<<g, kThreads, SM, l.stream>>>(A, T, phase, k, v, v_scale, off, out, n, RS, R, Za, to_gate(gate), level,
+                                              cnt, to_sync(sync), to_dist(dist));
+          err = cudaGetLastError();
         }
       });
     });
@@ -138,12 +174,16 @@ cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const
 
 #define F3RG_TILE_INSTANTIATE(PA)                                                                                  \
   template cudaError_t launch_spmv_dots_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*, void*, \
-                                              uint64_t, int, LevelState*, GateH, SyncH, double*, int, int*);       \
+                                              uint64_t, int, LevelState*, GateH, SyncH, double*, int, int*, DistH); \
   template cudaError_t launch_residual_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*,         \
-                                             const double*, void*, LevelState*, double*, SyncH);                   \
+                                             const double*, void*, LevelState*, double*, SyncH, DistH);            \
   template cudaError_t launch_spmv_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*, void*);     \
   template cudaError_t launch_richardson_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*,       \
                                                const double*, void*, uint64_t, RichState*, GateH, int,             \
-                                               unsigned long long*, SyncH, unsigned*, unsigned*, const IoSlot*);
+                                               unsigned long long*, SyncH, unsigned*, unsigned*, const IoSlot*,    \
+                                               uint64_t, int);                                                     \
+  template cudaError_t launch_rich_phase_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, int, int,          \
+                                               const void*, const double*, uint64_t, void*, uint64_t, RichState*,  \
+                                               void*, void*, GateH, int, unsigned long long*, SyncH, DistH);
 
 }  // namespace f3rg

@@ -48,37 +48,76 @@ struct Sync {
   unsigned* counter;  // last-block counter
 };
 
+// Cross-rank completion of a reduction under the row-block partition (P > 1,
+// SURVEY.md 8(e)); DESIGN.md section 6.
+//   mode 0: one rank -- the last CTA runs the tail on its own totals
+//   mode 1: the last CTA publishes its rank-local totals to loc[0..NV) and stops
+//   mode 2: one CTA combines all[r * kMaxPart + k], r = 0..P-1, in rank order at
+//           the reduction precision, then runs the tail (the body is skipped)
+// Every rank combines the same P values in the same order, so the replicated
+// scalars (Hessenberg column, norms, Givens state) are bitwise equal on all ranks.
+struct Dist {
+  int mode;
+  int P;
+  double* loc;
+  const double* all;
+};
+
+template <int C>
+__device__ void combine_ranks(const Dist& d, int nv, double* out) {
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nv; ++k) {
+      T_<C> acc = Ar<C>::zero();
+      for (int r = 0; r < d.P; ++r) acc = Ar<C>::add(acc, cvt<C>(d.all[(size_t)r * kMaxPart + k]));
+      out[k] = Ar<C>::wide(acc);
+    }
+  __syncthreads();
+}
+
+// mode 1: hand the rank-local totals over and report "stop here"
+__device__ __forceinline__ bool publish_local(const Dist& d, int nv, const double* tot) {
+  if (d.mode != 1) return false;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < nv; ++k) d.loc[k] = tot[k];
+  return true;
+}
+
 // ------------------------------------------------------------------------------
 // v_0 of an invocation: dst = demote(src * s) (s optional); optionally write the
 // scaled source back (materialising the parent's normalised basis vector); norm.
 template <int PS, int PW>
 __global__ void __launch_bounds__(256) k_level_start(void* src, const double* src_scale, int writeback, void* dst,
                                                      uint64_t n, LevelState* L, int* dead, Gate gate, int level,
-                                                     unsigned long long* cnt, Sync sync, const IoSlot* io) {
+                                                     unsigned long long* cnt, Sync sync, const IoSlot* io, Dist dist) {
   __shared__ double scratch[64];
-  if (gate.closed()) return;
-  if (io) {
-    src = io->src;
-    src_scale = io->src_scale;
-  }
-  const T_<PS> s = src_scale ? cvt<PS>(*src_scale) : Ar<PS>::one();
-  T_<PW> acc[1] = {Ar<PW>::zero()};
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    T_<PS> v = ld<PS>(src, i);
-    if (src_scale) {
-      v = Ar<PS>::mul(s, v);
-      if (writeback) st<PS>(src, i, v);
-    }
-    const T_<PW> d = cvt<PW>(v);
-    st<PW>(dst, i, d);
-    acc[0] = Ar<PW>::add(acc[0], Ar<PW>::mul(d, d));
-  }
-  block_sum<PW, 1>(acc, scratch);
-  if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
-  if (!last_block(sync.counter)) return;
   __shared__ double tot[1];
-  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+  if (gate.closed()) return;
+  if (dist.mode != 2) {
+    if (io) {
+      src = io->src;
+      src_scale = io->src_scale;
+    }
+    const T_<PS> s = src_scale ? cvt<PS>(*src_scale) : Ar<PS>::one();
+    T_<PW> acc[1] = {Ar<PW>::zero()};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      T_<PS> v = ld<PS>(src, i);
+      if (src_scale) {
+        v = Ar<PS>::mul(s, v);
+        if (writeback) st<PS>(src, i, v);
+      }
+      const T_<PW> d = cvt<PW>(v);
+      st<PW>(dst, i, d);
+      acc[0] = Ar<PW>::add(acc[0], Ar<PW>::mul(d, d));
+    }
+    block_sum<PW, 1>(acc, scratch);
+    if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
+    if (!last_block(sync.counter)) return;
+    reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (publish_local(dist, 1, tot)) return;
+  } else {
+    combine_ranks<PW>(dist, 1, tot);
+  }
   if (threadIdx.x == 0) {
     using A = Ar<PW>;
     const T_<PW> beta = A::sqrt(cvt<PW>(tot[0]));  // norm2 at the storage precision
@@ -147,13 +186,13 @@ template <int C, int PW, int ND>
 struct EpiDots {
   void* w;
   void* V;
-  uint64_t n;
+  uint64_t ld;  // slot stride
   T_<PW> sk[ND];  // s_k
   T_<PW> d[ND];   // partial (w, v_k)
   T_<PW> vk[ND];  // prefetched raw w_k(i)
   __device__ __forceinline__ void prefetch(uint32_t i) {
 #pragma unroll
-    for (int k = 0; k < ND; ++k) vk[k] = ld<PW>(V, (uint64_t)k * n + i);
+    for (int k = 0; k < ND; ++k) vk[k] = ::f3rg::ld<PW>(V, (uint64_t)k * ld + i);
   }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> wi = cvt<PW>(acc);
@@ -164,15 +203,15 @@ struct EpiDots {
 };
 
 template <int PA, int PZ, int PW, int ND, int IDX>
-__device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& T, const void* z, void* V, uint64_t n,
+__device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& T, const void* z, void* V, uint64_t ld,
                                                int j, LevelState* L, Sync& sync, double* dots, int defer,
-                                               uint8_t* smem, double* scratch, double* res) {
+                                               uint8_t* smem, double* scratch, double* res, const Dist& dist) {
   constexpr int C = pmax(PA, PW);
   GatherPlain<PZ, C> g{z};
   EpiDots<C, PW, ND> e;
-  e.w = static_cast<uint8_t*>(V) + (size_t)(j + 1) * n * sizeof(T_<PW>);
+  e.w = static_cast<uint8_t*>(V) + (size_t)(j + 1) * ld * sizeof(T_<PW>);
   e.V = V;
-  e.n = n;
+  e.ld = ld;
 #pragma unroll
   for (int k = 0; k < ND; ++k) e.d[k] = Ar<PW>::zero(), e.sk[k] = cvt<PW>(L->scale[k]);
   spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
@@ -185,6 +224,7 @@ __device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& 
   if (defer) return;
   if (!last_block(sync.counter)) return;
   reduce_partials<PW, ND>(dots, gridDim.x, kMaxPart, res, scratch);
+  if (publish_local(dist, ND, res)) return;
   if (threadIdx.x == 0)
     for (int k = 0; k < ND; ++k) L->H[(size_t)j * (L->m + 1) + k] = res[k];
 }
@@ -193,30 +233,45 @@ __device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& 
 // (the projection count is a compile-time parameter of the epilogue: runtime
 // predication there cost ~140 instructions per row). defer != 0: only per-CTA
 // partials are written (to `dots`); the following k_cgs reduces them.
+// V: slot 0 of the basis (owned rows); ld: slot stride; z: the SpMV input (ext layout)
 template <int PA, int PZ, int PW, int IDX>
-__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t n, int j,
-                                                   LevelState* L, Gate gate, Sync sync, double* dots, int defer) {
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t ld, int j,
+                                                   LevelState* L, Gate gate, Sync sync, double* dots, int defer,
+                                                   Dist dist) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double res[8];
   if (gate.closed()) return;
+  if (dist.mode == 2) {
+    const int nd = j + 1 < 8 ? j + 1 : 8;
+    combine_ranks<PW>(dist, nd, res);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < nd; ++k) L->H[(size_t)j * (L->m + 1) + k] = res[k];
+    return;
+  }
   switch (j + 1 < 8 ? j + 1 : 8) {
 #define F3RG_ND(K) \
-  case K: spmv_dots_body<PA, PZ, PW, K, IDX>(A, T, z, V, n, j, L, sync, dots, defer, smem, scratch, res); break;
+  case K: spmv_dots_body<PA, PZ, PW, K, IDX>(A, T, z, V, ld, j, L, sync, dots, defer, smem, scratch, res, dist); break;
     F3RG_ND(1) F3RG_ND(2) F3RG_ND(3) F3RG_ND(4) F3RG_ND(5) F3RG_ND(6) F3RG_ND(7)
-    default: spmv_dots_body<PA, PZ, PW, 8, IDX>(A, T, z, V, n, j, L, sync, dots, defer, smem, scratch, res);
+    default: spmv_dots_body<PA, PZ, PW, 8, IDX>(A, T, z, V, ld, j, L, sync, dots, defer, smem, scratch, res, dist);
 #undef F3RG_ND
   }
 }
 
 // remaining projections h_k, k in [k0, min(k0+8, j+1)), for long outer cycles
 template <int PW>
-__global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, int j, int k0, LevelState* L,
-                                                   Gate gate, Sync sync) {
+__global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, uint64_t ldv, int j, int k0,
+                                                   LevelState* L, Gate gate, Sync sync, Dist dist) {
   __shared__ double scratch[8 * 8];
   __shared__ double res[8];
   if (gate.closed()) return;
   const int nd = (j + 1 - k0) < 8 ? (j + 1 - k0) : 8;
+  if (dist.mode == 2) {
+    combine_ranks<PW>(dist, nd, res);
+    if (threadIdx.x == 0)
+      for (int k = 0; k < nd; ++k) L->H[(size_t)j * (L->m + 1) + k0 + k] = res[k];
+    return;
+  }
   T_<PW> d[8], s[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -225,17 +280,18 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, in
   }
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const T_<PW> wi = ld<PW>(V, (uint64_t)(j + 1) * n + i);
+    const T_<PW> wi = ld<PW>(V, (uint64_t)(j + 1) * ldv + i);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       if (k < nd)
-        d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, Ar<PW>::mul(s[k], ld<PW>(V, (uint64_t)(k0 + k) * n + i))));
+        d[k] = Ar<PW>::add(d[k], Ar<PW>::mul(wi, Ar<PW>::mul(s[k], ld<PW>(V, (uint64_t)(k0 + k) * ldv + i))));
   }
   block_sum<PW, 8>(d, scratch);
   if (threadIdx.x == 0)
     for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(d[k]);
   if (!last_block(sync.counter)) return;
   reduce_partials<PW, 8>(sync.partials, gridDim.x, kMaxPart, res, scratch);
+  if (publish_local(dist, nd, res)) return;
   if (threadIdx.x == 0)
     for (int k = 0; k < nd; ++k) L->H[(size_t)j * (L->m + 1) + k0 + k] = res[k];
 }
@@ -247,9 +303,9 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, in
 // `outer` levels never set their dead flag (the host decides) and report through
 // `info`.
 template <int PW>
-__global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelState* L, int* dead, Gate gate,
-                                             int level, int outer, int use_tol, StepInfo* info, Sync sync,
-                                             const double* dots, int dots_G) {
+__global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, uint64_t ldv, int j, LevelState* L, int* dead,
+                                             Gate gate, int level, int outer, int use_tol, StepInfo* info, Sync sync,
+                                             const double* dots, int dots_G, Dist dist) {
   __shared__ double scratch[64];
   __shared__ double hs[128];
   __shared__ double tot[8];
@@ -258,6 +314,7 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
   const int m1 = L->m + 1;
   double* h = L->H + (size_t)j * m1;
   const int nh = j + 1 <= 128 ? j + 1 : 128;
+  if (dist.mode != 2) {
   // the projections: reduced here from k_spmv_dots' partials (deferred) or read
   // from H; called after each thread has issued its first streaming loads so the
   // reduction's latency hides under them
@@ -272,7 +329,7 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
     __syncthreads();
   };
   T_<PW> acc[1] = {A::zero()};
-  T_<PW>* w = static_cast<T_<PW>*>(V) + (size_t)(j + 1) * n;
+  T_<PW>* w = static_cast<T_<PW>*>(V) + (size_t)(j + 1) * ldv;
   // the first <= 8 coefficients and scales live in registers and the loop is
   // specialised on their count (uniform per launch); 16-byte vector loads when the
   // slots are 16-byte aligned (n a multiple of the vector width)
@@ -284,7 +341,7 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
 #pragma unroll
       for (int u = 0; u < NJ; ++u) wi = A::add(A::mul(a[u], A::mul(sc[u], vv[u])), wi);
       for (int k = NJ; k <= j; ++k) {  // long outer cycles only
-        const T_<PW> v = A::mul(cvt<PW>(L->scale[k]), ld<PW>(V, (uint64_t)k * n + i));
+        const T_<PW> v = A::mul(cvt<PW>(L->scale[k]), ld<PW>(V, (uint64_t)k * ldv + i));
         wi = A::add(A::mul(k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]), v), wi);
       }
       acc[0] = A::add(acc[0], A::mul(wi, wi));
@@ -296,14 +353,14 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
     };
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    if (n % VE == 0) {
+    if (n % VE == 0 && ldv % VE == 0) {
       const uint64_t nv = n / VE;
       const uint4* w4 = reinterpret_cast<const uint4*>(w);
       uint4 raw[NJ], wr = {0u, 0u, 0u, 0u};
       auto load = [&](uint64_t e) {
 #pragma unroll
         for (int u = 0; u < NJ; ++u)
-          raw[u] = reinterpret_cast<const uint4*>(static_cast<const T_<PW>*>(V) + (uint64_t)u * n)[e];
+          raw[u] = reinterpret_cast<const uint4*>(static_cast<const T_<PW>*>(V) + (uint64_t)u * ldv)[e];
         wr = w4[e];
       };
       uint64_t e = tid;
@@ -333,7 +390,7 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
       for (uint64_t i = tid; i < n; i += stride) {
         T_<PW> vv[NJ];
 #pragma unroll
-        for (int u = 0; u < NJ; ++u) vv[u] = ld<PW>(V, (uint64_t)u * n + i);
+        for (int u = 0; u < NJ; ++u) vv[u] = ld<PW>(V, (uint64_t)u * ldv + i);
         w[i] = update(i, w[i], vv);
       }
     }
@@ -351,6 +408,7 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
   block_sum<PW, 1>(acc, scratch);
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = A::wide(acc[0]);
   if (!last_block(sync.counter)) return;
+  }  // dist.mode != 2
   // Givens tail: one parallel round trip stages the small state (column j of H,
   // the previous rotations, g_j) in shared memory, overlapped with the partials
   // reduction; thread 0 then runs the serial recurrence out of shared memory
@@ -362,7 +420,12 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
     for (int i = threadIdx.x; i < j; i += blockDim.x) cs[i] = __ldcg(L->cs + i), sn[i] = __ldcg(L->sn + i);
     if (threadIdx.x == 0) gj_tol[0] = __ldcg(L->g + j), gj_tol[1] = L->tol, gj_tol[2] = L->bnorm;
   }
-  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);  // ends with __syncthreads
+  if (dist.mode != 2) {
+    reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);  // ends with __syncthreads
+    if (publish_local(dist, 1, tot)) return;
+  } else {
+    combine_ranks<PW>(dist, 1, tot);
+  }
   if (threadIdx.x != 0) return;
   double* hh = staged ? hc : h;
   const double* csr = staged ? cs : L->cs;
@@ -434,7 +497,7 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, int j, LevelSt
 // Back-substitution (in W) + x (+)= sum_l y_l z_l, sequential axpys per element
 // (src/fgmres.cpp:133-146). x_is_zero: inner levels start from fill(out, 0).
 template <int PZ, int PW, int PX>
-__global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n, LevelState* L, void* x,
+__global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n, uint64_t ldz, LevelState* L, void* x,
                                                       int x_is_zero, Gate gate, int level, unsigned long long* cnt,
                                                       int count_iterations, const IoSlot* io) {
   __shared__ double ys[1024];
@@ -482,12 +545,12 @@ __global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n,
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
       T_<PZ> zz[K > 0 ? K : 1];
 #pragma unroll
-      for (int u = 0; u < K; ++u) zz[u] = ld<PZ>(Z, (uint64_t)u * n + i);
+      for (int u = 0; u < K; ++u) zz[u] = ld<PZ>(Z, (uint64_t)u * ldz + i);
       T_<PX> xi = x_is_zero ? cvt<PX>(0.0) : ld<PX>(x, i);
 #pragma unroll
       for (int u = 0; u < K; ++u) xi = cvt<PX>(AC::add(AC::mul(yy[u], cvt<C>(zz[u])), cvt<C>(xi)));
       for (int l = K; l < k; ++l)  // long outer cycles only
-        xi = cvt<PX>(AC::add(AC::mul(cvt<C>(ys[l]), cvt<C>(ld<PZ>(Z, (uint64_t)l * n + i))), cvt<C>(xi)));
+        xi = cvt<PX>(AC::add(AC::mul(cvt<C>(ys[l]), cvt<C>(ld<PZ>(Z, (uint64_t)l * ldz + i))), cvt<C>(xi)));
       st<PX>(x, i, xi);
     }
   };
@@ -526,21 +589,27 @@ struct EpiResidual {
 
 // result: L (if non-null) gets the Arnoldi start like k_level_start; norm2 (W) is
 // also written to *out_norm.
+// x: ext layout (gathered); b, r: owned rows
 template <int PA, int PX, int PW, int IDX>
 __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
-                                                  LevelState* L, double* out_norm, Sync sync) {
+                                                  LevelState* L, double* out_norm, Sync sync, Dist dist) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double tot[1];
-  constexpr int C = pmax(PA, PX);
-  GatherPlain<PX, C> g{x};
-  EpiResidual<C, PW> e{b, r, Ar<PW>::zero(), 0.0};
-  spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
-  T_<PW> acc[1] = {e.acc};
-  block_sum<PW, 1>(acc, scratch);
-  if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
-  if (!last_block(sync.counter)) return;
-  reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+  if (dist.mode != 2) {
+    constexpr int C = pmax(PA, PX);
+    GatherPlain<PX, C> g{x};
+    EpiResidual<C, PW> e{b, r, Ar<PW>::zero(), 0.0};
+    spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
+    T_<PW> acc[1] = {e.acc};
+    block_sum<PW, 1>(acc, scratch);
+    if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
+    if (!last_block(sync.counter)) return;
+    reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (publish_local(dist, 1, tot)) return;
+  } else {
+    combine_ranks<PW>(dist, 1, tot);
+  }
   if (threadIdx.x == 0) {
     using AW = Ar<PW>;
     const T_<PW> beta = AW::sqrt(cvt<PW>(tot[0]));

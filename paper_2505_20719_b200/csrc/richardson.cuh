@@ -23,13 +23,18 @@
 namespace f3rg {
 
 
-// Right-hand side of the call: v_i = demote(s * parent_v_i) (s optional).
+// Right-hand side of the call: v_i = demote(s * parent_v_i) (s optional). v is in
+// the ext layout (row-block partition): gathers index it by ext column, row-local
+// reads by owned row + off (off = 0 on a single rank).
 template <int PV, int PW>
 struct RhsView {
   const void* v;
   T_<PV> s;
   bool scaled;
-  __device__ __forceinline__ T_<PV> raw(uint64_t i) const { return ldg<PV>(v, i); }
+  uint64_t off;
+  __device__ __forceinline__ T_<PV> raw(uint64_t c) const { return ldg<PV>(v, c); }
+  __device__ __forceinline__ T_<PV> raw_row(uint64_t i) const { return ldg<PV>(v, i + off); }
+  __device__ __forceinline__ T_<PW> row(uint64_t i) const { return apply(raw_row(i)); }
   // s = 1 when unscaled: fl(1 * x) == x exactly (no flush-to-zero), so no select
   __device__ __forceinline__ T_<PW> apply(T_<PV> x) const { return cvt<PW>(Ar<PV>::mul(s, x)); }
   __device__ __forceinline__ T_<PW> operator()(uint64_t i) const { return apply(raw(i)); }
@@ -59,7 +64,7 @@ struct EpiStep {
   T_<PV> vraw;  // raw loads only in prefetch: their latency hides behind the row sum
   T_<PW> zi;
   __device__ __forceinline__ void prefetch(uint32_t i) {
-    vraw = rhs.raw(i);
+    vraw = rhs.raw_row(i);
     if constexpr (!Z1_ON_THE_FLY) zi = ldcg<PW>(zk, i);
   }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
@@ -82,7 +87,7 @@ struct EpiDotsRs {
   T_<PV> vraw;
   __device__ __forceinline__ void prefetch(uint32_t i) {
     if (R) rr = ldcg<PW>(R, i);
-    else vraw = rhs.raw(i);
+    else vraw = rhs.raw_row(i);
   }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> s = cvt<PW>(acc);
@@ -98,18 +103,21 @@ struct EpiResid {
   RhsView<PV, PW> rhs;
   void* R;
   T_<PV> vraw;
-  __device__ __forceinline__ void prefetch(uint32_t i) { vraw = rhs.raw(i); }
+  __device__ __forceinline__ void prefetch(uint32_t i) { vraw = rhs.raw_row(i); }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> s = cvt<PW>(acc);
     st<PW>(R, i, Ar<PW>::add(rhs.apply(vraw), Ar<PW>::neg(s)));
   }
 };
 
+// flags & 1 (row-block partition, P > 1): plain calls only, no bookkeeping -- update
+// calls and the per-call bookkeeping run as k_rich_phase launches with the
+// cross-rank exchanges between them
 template <int PA, int PW, int PV, int IDX>
 __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
                                                     void* out, uint64_t n, RichState* RS, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, unsigned* bar_count,
-                                                    unsigned* bar_gen, const IoSlot* io) {
+                                                    unsigned* bar_gen, const IoSlot* io, uint64_t voff, int flags) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double red[2];
@@ -125,14 +133,15 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, Ti
   const int m = RS->m;
   const unsigned long long call = RS->calls[0];
   const bool update = RS->cycle != 0ull && (call % RS->cycle) == 0ull;
-  RhsView<PV, PW> rhs{v, v_scale ? cvt<PV>(*v_scale) : Ar<PV>::one(), v_scale != nullptr};
+  if ((flags & 1) && update) return;
+  RhsView<PV, PW> rhs{v, v_scale ? cvt<PV>(*v_scale) : Ar<PV>::one(), v_scale != nullptr, voff};
   const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
 
   if (!update) {
     const T_<PW> w0 = cvt<PW>(RS->omegas[0]);
     if (m == 1) {
-      for (uint64_t i = gtid; i < n; i += gstride) st<PW>(out, i, AW::add(AW::mul(w0, rhs(i)), AW::zero()));
+      for (uint64_t i = gtid; i < n; i += gstride) st<PW>(out, i, AW::add(AW::mul(w0, rhs.row(i)), AW::zero()));
     } else {
       // step 1 with z1 on the fly, then steps 2..m-1 ping-ponging through scratch
       {
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, Ti
       const T_<PW> wh = cvt<PW>(wk);
       void* zn = (k + 1 == m) ? out : RS->Za;
       for (uint64_t i = gtid; i < n; i += gstride) {
-        const T_<PW> p = k > 0 ? ldcg<PW>(RS->R, i) : rhs(i);
+        const T_<PW> p = k > 0 ? ldcg<PW>(RS->R, i) : rhs.row(i);
         const T_<PW> zi = k > 0 ? ldcg<PW>(RS->Za, i) : AW::zero();
         st<PW>(zn, i, AW::add(AW::mul(wh, p), zi));
       }
@@ -208,6 +217,7 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, Ti
       __syncthreads();
     }
   }
+  if (flags & 1) return;  // bookkeeping: k_rich_phase PHASE_BOOK
   // bookkeeping once every CTA is done reading the state
   // update calls publish wused/wupd across CTAs (full fence); plain calls only count
   if (!(update ? last_block(sync.counter) : last_block_light(sync.counter))) return;
@@ -217,6 +227,107 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, Ti
       for (int k = 0; k < m; ++k) {
         if (RS->wupd[k]) {
           RS->omegas[k] = __ddiv_rn(__dadd_rn(__dmul_rn(l, RS->omegas[k]), RS->wused[k]), __dadd_rn(l, 1.0));
+        } else {
+          RS->calls[2] += 1ull;
+        }
+      }
+      RS->calls[1] += 1ull;
+    }
+    RS->calls[0] = call + 1ull;
+    cnt[CNT_INV + level] += 1ull;
+    cnt[CNT_IT + level] += (unsigned long long)m;
+    cnt[CNT_PRECOND] += (unsigned long long)m;
+  }
+}
+
+
+// ---- row-block partition (P > 1): one Richardson call as a launch sequence ------
+// The cooperative kernel's grid barriers become kernel boundaries, so the halo
+// exchanges (z_k, r) and the cross-rank (r, s), (s, s) reductions can sit between
+// them. The engine enqueues the sequence for EVERY call (the update decision
+// call_count % c == 0 is made here on the device, exactly as in k_richardson);
+// on plain calls every update phase returns at once and k_richardson (flags & 1)
+// did the sweep. Same arithmetic, same per-element order as k_richardson.
+enum { PH_RESID = 0, PH_DOTS = 1, PH_UPDATE = 2, PH_BOOK = 3 };
+
+template <int PA, int PW, int PV, int IDX>
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_rich_phase(CsrDev A, TilesDev T, int phase, int k, const void* v,
+                                                    const double* v_scale, uint64_t off, void* out, uint64_t n,
+                                                    RichState* RS, void* R, void* Za, Gate gate, int level,
+                                                    unsigned long long* cnt, Sync sync, Dist dist) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ double scratch[64];
+  __shared__ double tot[2];
+  if (gate.closed()) return;
+  constexpr int C = pmax(PA, PW);
+  constexpr int CD = pmax(P32, PW);
+  using AW = Ar<PW>;
+  const int m = RS->m;
+  const unsigned long long call = RS->calls[0];
+  const bool update = RS->cycle != 0ull && (call % RS->cycle) == 0ull;
+  RhsView<PV, PW> rhs{v, v_scale ? cvt<PV>(*v_scale) : Ar<PV>::one(), v_scale != nullptr, off};
+  T_<PW>* Rown = static_cast<T_<PW>*>(R) + off;
+  T_<PW>* Zown = static_cast<T_<PW>*>(Za) + off;
+  if (phase == PH_RESID) {  // r = v - A z_k
+    if (!update) return;
+    GatherCG<PW, C> g{Za};
+    EpiResid<PV, PW, C> e{rhs, Rown, {}};
+    spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
+  } else if (phase == PH_DOTS) {  // s = A p, rank-local (r, s), (s, s)
+    if (!update) return;
+    EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? Rown : nullptr, Ar<CD>::zero(), Ar<CD>::zero(), {}, {}};
+    if (k == 0) {
+      struct GatherRhs {
+        using Raw = T_<PV>;
+        RhsView<PV, PW> rhs;
+        __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
+        __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
+      } g{rhs};
+      spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
+    } else {
+      GatherCG<PW, C> g{R};
+      spmv_tiles<PA, C, IDX>(A, T, g, e, smem);
+    }
+    T_<CD> acc[2] = {e.num, e.den};
+    block_sum<CD, 2>(acc, scratch);
+    if (threadIdx.x == 0) {
+      sync.partials[(size_t)blockIdx.x * kMaxPart + 0] = Ar<CD>::wide(acc[0]);
+      sync.partials[(size_t)blockIdx.x * kMaxPart + 1] = Ar<CD>::wide(acc[1]);
+    }
+    if (!last_block(sync.counter)) return;
+    reduce_partials<CD, 2>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    publish_local(dist, 2, tot);
+  } else if (phase == PH_UPDATE) {  // w' from the rank-ordered totals; z += w' p
+    if (!update) return;
+    combine_ranks<CD>(dist, 2, tot);
+    const double num = tot[0], den = tot[1];
+    double wk;
+    int fresh;
+    if (den == 0.0 || !isfinite(num) || !isfinite(den)) {
+      wk = RS->omegas[k];
+      fresh = 0;
+    } else {
+      wk = Ar<CD>::wide(Ar<CD>::div(cvt<CD>(num), cvt<CD>(den)));
+      fresh = 1;
+    }
+    const T_<PW> wh = cvt<PW>(wk);
+    void* zn = (k + 1 == m) ? out : static_cast<void*>(Zown);
+    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gstride) {
+      const T_<PW> p = k > 0 ? ldcg<PW>(Rown, i) : rhs.row(i);
+      const T_<PW> zi = k > 0 ? ldcg<PW>(Zown, i) : AW::zero();
+      st<PW>(zn, i, AW::add(AW::mul(wh, p), zi));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      RS->wused[k] = wk;
+      RS->wupd[k] = fresh;
+    }
+  } else if (blockIdx.x == 0 && threadIdx.x == 0) {  // PH_BOOK, one thread: as k_richardson's tail
+    if (update) {
+      const double l = (double)(call / RS->cycle - 1ull);
+      for (int q = 0; q < m; ++q) {
+        if (RS->wupd[q]) {
+          RS->omegas[q] = __ddiv_rn(__dadd_rn(__dmul_rn(l, RS->omegas[q]), RS->wused[q]), __dadd_rn(l, 1.0));
         } else {
           RS->calls[2] += 1ull;
         }
