@@ -186,6 +186,85 @@ def _config(args, p):
             "parallelism": f"dp{args.gpus}" if args.gpus > 1 else "single GPU"}
 
 
+def run_partitioned(args):
+    """N > 1 (or --partition): ONE config-2 system row-block partitioned over the
+    ranks: NCCL point-to-point halos + allgather of rank-local totals
+    inside the solve; strong scaling (total work fixed). Timed as the max over ranks
+    of CUDA-event time per solve."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import partition, problems
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("cpu:gloo,cuda:nccl", rank=rank, world_size=world)
+    p = problems.problem(args.config)
+    a = f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values)
+    uid = [partition.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    part = partition.NcclPartition(a, SPEC, world, rank, uid[0])
+    pl = part.plan
+    opts = f.RunOptions(tol=TOL)
+    b_own = torch.from_numpy(p.b[pl.r0:pl.r1].copy()).cuda()
+    x_own = torch.zeros(pl.r1 - pl.r0, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    for _ in range(max(args.warmup, 0)):
+        part.reset()
+        rep = part.run(b_own, x_own, opts, sp)
+    assert rep.converged and rep.final_true_residual <= TOL, rep
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            part.reset()
+            rep = part.run(b_own, x_own, opts, sp)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    dist.barrier()
+    # e2e: host b slice in, host x slice out, every step
+    b_host = torch.from_numpy(p.b[pl.r0:pl.r1].copy()).pin_memory()
+    x_host = torch.empty(pl.r1 - pl.r0, dtype=torch.float64).pin_memory()
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 5))):
+        dist.barrier()
+        t0 = time.perf_counter()
+        part.reset()
+        b_own.copy_(b_host, non_blocking=True)
+        rep = part.run(b_own, x_own, opts, sp)
+        x_host.copy_(x_own, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    e2 = torch.tensor([float(np.mean(e2e_t))], device="cuda")
+    dist.all_reduce(e2, op=dist.ReduceOp.MAX)
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "mixed f64/f32/f16", "data": "synthetic",
+        "config": dict(_config(args, p), parallelism=f"row-block partition over {world} GPU(s), NCCL halos"),
+        "outer_iterations": rep.outer_iterations, "final_true_residual": rep.final_true_residual,
+        "e2e": {"value": float(e2.item()), "unit": "s", "h2d_bytes_per_step": int(p.n * 8),
+                "d2h_bytes_per_step": int(p.n * 8)},
+        "gpu_launches": None, "clocks": clk.summary(),
+        "partition": {"rows_rank0": pl.r1 - pl.r0, "halo_rank0": pl.n_lo + pl.n_hi},
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    del part
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
 
@@ -193,9 +272,8 @@ def run_ours(args):
     from paper_2505_20719_b200 import problems
 
     rank, local, world = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
+    if world > 1 or args.partition:
+        return run_partitioned(args)
     torch.cuda.set_device(local)
     p = problems.problem(args.config)
     reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
@@ -215,8 +293,6 @@ def run_ours(args):
     assert run.report.converged and run.report.final_true_residual <= TOL, run.report
 
     # ---- timed region: K full solves, device-resident inputs ----
-    if world > 1:
-        torch.distributed.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -227,11 +303,6 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        torch.distributed.barrier()
     if not (run.report.converged and run.report.final_true_residual <= TOL):
         raise SystemExit(f"timed solve did not converge: {run.report}")
 
@@ -284,7 +355,7 @@ def run_ours(args):
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         try:
             threads = os.cpu_count()
             per_outer, extrap, rep = cpu_reference_sample(p, outer, threads)
@@ -294,10 +365,7 @@ def run_ours(args):
         except Exception as e:  # keep the GPU line even if the CPU leg fails
             line["cpu_baseline"] = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"failed: {e}"}
-    if rank == 0:
-        print(json.dumps(line))
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    print(json.dumps(line))
 
 
 def main():
@@ -308,6 +376,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", action="store_true",
+                    help="use the row-block partitioned NCCL path even on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
