@@ -12,6 +12,7 @@ namespace f3rg {
 
 template <int P>
 __global__ void __launch_bounds__(256) k_fill(void* x, uint64_t n, double value) {
+  pdl_wait();
   const T_<P> v = cvt<P>(value);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) st<P>(x, i, v);
@@ -19,6 +20,7 @@ __global__ void __launch_bounds__(256) k_fill(void* x, uint64_t n, double value)
 
 template <int PX, int PY>
 __global__ void __launch_bounds__(256) k_copy(const void* x, void* y, uint64_t n) {
+  pdl_wait();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     st<PY>(y, i, cvt<PY>(ld<PX>(x, i)));
@@ -26,6 +28,7 @@ __global__ void __launch_bounds__(256) k_copy(const void* x, void* y, uint64_t n
 
 template <int P>
 __global__ void __launch_bounds__(256) k_scale(double alpha, void* x, uint64_t n) {
+  pdl_wait();
   const T_<P> a = cvt<P>(alpha);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -35,6 +38,7 @@ __global__ void __launch_bounds__(256) k_scale(double alpha, void* x, uint64_t n
 // y = fl_C(fl_C(a * x) + y), C = promote(x, y)
 template <int PX, int PY>
 __global__ void __launch_bounds__(256) k_axpy(double alpha, const void* x, void* y, uint64_t n) {
+  pdl_wait();
   constexpr int C = pmax(PX, PY);
   const T_<C> a = cvt<C>(alpha);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -46,6 +50,7 @@ __global__ void __launch_bounds__(256) k_axpy(double alpha, const void* x, void*
 template <int PX, int PY, int PO>
 __global__ void __launch_bounds__(256) k_add_scaled(const void* x, double alpha, const void* y, void* out,
                                                     uint64_t n) {
+  pdl_wait();
   constexpr int C = pmax(pmax(PX, PY), PO);
   const T_<C> a = cvt<C>(alpha);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -58,6 +63,7 @@ __global__ void __launch_bounds__(256) k_add_scaled(const void* x, double alpha,
 template <int PX, int PY, int C, bool SQRT, int PS>
 __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint64_t n, double* out, Sync sync,
                                              Dist dist) {
+  pdl_wait();
   __shared__ double scratch[64];
   __shared__ double tot[1];
   if (dist.mode != 2) {
@@ -65,6 +71,7 @@ __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint6
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
       acc[0] = Ar<C>::add(acc[0], Ar<C>::mul(cvt<C>(ld<PX>(x, i)), cvt<C>(ld<PY>(y, i))));
+    pdl_trigger();
     block_sum<C, 1>(acc, scratch);
     if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<C>::wide(acc[0]);
     if (!last_block(sync.counter)) return;
@@ -87,6 +94,7 @@ __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint6
 // owned rows when the peers share an address space)
 template <int P>
 __global__ void __launch_bounds__(256) k_gather(const void* src, const uint32_t* idx, uint64_t cnt, void* dst) {
+  pdl_wait();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += stride)
     st<P>(dst, i, ld<P>(src, idx[i]));
@@ -95,6 +103,7 @@ __global__ void __launch_bounds__(256) k_gather(const void* src, const uint32_t*
 // plain y = A x (any precision triple), for the kernel-level entry point
 template <int PA, int PX, int PY, int IDX>
 __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int C = pmax(PA, PX);
   GatherPlain<PX, C> g{x};

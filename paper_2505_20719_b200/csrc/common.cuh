@@ -120,6 +120,37 @@ __device__ __forceinline__ void st(void* p, uint64_t i, T_<P> v) {
   static_cast<T_<P>*>(p)[i] = v;
 }
 
+// 8 consecutive elements (group g) of a precision-tagged array as 16-byte
+// transactions (1, 2 or 4 of them); the array must be 16-byte aligned
+constexpr int kGroup = 8;
+template <int P>
+__device__ __forceinline__ void ld8(const void* p, uint64_t g, T_<P> (&out)[kGroup]) {
+  constexpr int NQ = kGroup * (int)sizeof(T_<P>) / 16;
+  const uint4* q = reinterpret_cast<const uint4*>(p) + g * NQ;
+  uint4 t[NQ];
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) t[k] = q[k];
+  memcpy(out, t, sizeof t);
+}
+template <int P>
+__device__ __forceinline__ void st8(void* p, uint64_t g, const T_<P> (&v)[kGroup]) {
+  constexpr int NQ = kGroup * (int)sizeof(T_<P>) / 16;
+  uint4 t[NQ];
+  memcpy(t, v, sizeof t);
+  uint4* q = reinterpret_cast<uint4*>(p) + g * NQ;
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) q[k] = t[k];
+}
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- programmatic dependent launch ------------------------------------------------
+// pdl_wait(): returns once the preceding kernel has completed and its writes are
+// visible (a no-op without a programmatic dependency). pdl_trigger(): this CTA no
+// longer holds the successor back (it may launch once every CTA has triggered or
+// exited); called after the main loops, before the reduction tails.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- sm_90+/sm_100a async bulk copy (TMA 1D) + mbarrier ------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

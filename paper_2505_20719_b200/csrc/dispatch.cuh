@@ -30,6 +30,25 @@ inline Dist to_dist(DistH d) { return Dist{d.mode, d.P, d.loc, d.all}; }
 
 constexpr int kThreads = 256;
 
+// every kernel is launched with programmatic stream serialization (PDL): it may
+// start while its predecessor drains, and waits in pdl_wait() (common.cuh) before
+// touching anything another kernel wrote. F3RG_PDL=0 turns it off (A/B runs).
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), int grid, int smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // occupancy-derived persistent grid for a tile kernel instantiation (cached per
 // instantiation by the caller through a function-local static)
 template <class K>

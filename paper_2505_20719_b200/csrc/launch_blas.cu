@@ -6,21 +6,21 @@ namespace f3rg {
 
 cudaError_t launch_fill(int p, Launch l, void* x, uint64_t n, double value) {
   const int g = l.grid ? l.grid : stream_grid();
-  with_p(p, [&](auto P) { k_fill<decltype(P)::value><<<g, kThreads, 0, l.stream>>>(x, n, value); });
+  with_p(p, [&](auto P) { launch_k(k_fill<decltype(P)::value>, g, 0, l.stream, x, n, value); });
   return cudaGetLastError();
 }
 
 cudaError_t launch_copy(int px, int py, Launch l, const void* x, void* y, uint64_t n) {
   const int g = l.grid ? l.grid : stream_grid();
   with_p(px, [&](auto X) {
-    with_p(py, [&](auto Y) { k_copy<decltype(X)::value, decltype(Y)::value><<<g, kThreads, 0, l.stream>>>(x, y, n); });
+    with_p(py, [&](auto Y) { launch_k(k_copy<decltype(X)::value, decltype(Y)::value>, g, 0, l.stream, x, y, n); });
   });
   return cudaGetLastError();
 }
 
 cudaError_t launch_scale(int p, Launch l, double alpha, void* x, uint64_t n) {
   const int g = l.grid ? l.grid : stream_grid();
-  with_p(p, [&](auto P) { k_scale<decltype(P)::value><<<g, kThreads, 0, l.stream>>>(alpha, x, n); });
+  with_p(p, [&](auto P) { launch_k(k_scale<decltype(P)::value>, g, 0, l.stream, alpha, x, n); });
   return cudaGetLastError();
 }
 
@@ -28,7 +28,7 @@ cudaError_t launch_axpy(int px, int py, Launch l, double alpha, const void* x, v
   const int g = l.grid ? l.grid : stream_grid();
   with_p(px, [&](auto X) {
     with_p(py, [&](auto Y) {
-      k_axpy<decltype(X)::value, decltype(Y)::value><<<g, kThreads, 0, l.stream>>>(alpha, x, y, n);
+      launch_k(k_axpy<decltype(X)::value, decltype(Y)::value>, g, 0, l.stream, alpha, x, y, n);
     });
   });
   return cudaGetLastError();
@@ -40,8 +40,7 @@ cudaError_t launch_add_scaled(int px, int py, int po, Launch l, const void* x, d
   with_p(px, [&](auto X) {
     with_p(py, [&](auto Y) {
       with_p(po, [&](auto O) {
-        k_add_scaled<decltype(X)::value, decltype(Y)::value, decltype(O)::value>
-            <<<g, kThreads, 0, l.stream>>>(x, alpha, y, out, n);
+        launch_k(k_add_scaled<decltype(X)::value, decltype(Y)::value, decltype(O)::value>, g, 0, l.stream, x, alpha, y, out, n);
       });
     });
   });
@@ -57,7 +56,7 @@ cudaError_t launch_dot(int px, int py, int floor_p, Launch l, const void* x, con
       with_p(c, [&](auto C) {
         constexpr int CX = decltype(C)::value, PX = decltype(X)::value, PY = decltype(Y)::value;
         if constexpr (CX >= PX && CX >= PY)
-          k_dot<PX, PY, CX, false, CX><<<g, kThreads, 0, l.stream>>>(x, y, n, out, to_sync(sync), to_dist(dist));
+          launch_k(k_dot<PX, PY, CX, false, CX>, g, 0, l.stream, x, y, n, out, to_sync(sync), to_dist(dist));
       });
     });
   });
@@ -68,7 +67,7 @@ cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* ou
   const int g = dist.mode == 2 ? 1 : l.grid ? l.grid : stream_grid();
   with_p(px, [&](auto X) {
     constexpr int PX = decltype(X)::value;
-    k_dot<PX, PX, PX, true, PX><<<g, kThreads, 0, l.stream>>>(x, x, n, out, to_sync(sync), to_dist(dist));
+    launch_k(k_dot<PX, PX, PX, true, PX>, g, 0, l.stream, x, x, n, out, to_sync(sync), to_dist(dist));
   });
   return cudaGetLastError();
 }
@@ -77,7 +76,7 @@ cudaError_t launch_gather(int p, Launch l, const void* src, const uint32_t* idx,
   if (cnt == 0) return cudaSuccess;
   const uint64_t want = (cnt + kThreads - 1) / kThreads;
   const int g = l.grid ? l.grid : (int)(want < (uint64_t)stream_grid() ? want : (uint64_t)stream_grid());
-  with_p(p, [&](auto P) { k_gather<decltype(P)::value><<<g, kThreads, 0, l.stream>>>(src, idx, cnt, dst); });
+  with_p(p, [&](auto P) { launch_k(k_gather<decltype(P)::value>, g, 0, l.stream, src, idx, cnt, dst); });
   return cudaGetLastError();
 }
 

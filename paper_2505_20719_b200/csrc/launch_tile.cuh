@@ -40,7 +40,7 @@ cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const 
           if (dist.mode == 2) g = 1;
           if (g < 1) g = 1;
           if (grid_out) *grid_out = g;
-          kern<<<g, kThreads, SM, l.stream>>>(A, T, z, V, ld, j, L, to_gate(gate), to_sync(sync), dots, defer,
+          launch_k(kern, g, SM, l.stream, A, T, z, V, ld, j, L, to_gate(gate), to_sync(sync), dots, defer,
                                               to_dist(dist));
           err = cudaGetLastError();
         }
@@ -69,7 +69,7 @@ cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const T
           int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
           if (dist.mode == 2) g = 1;
           if (g < 1) g = 1;
-          kern<<<g, kThreads, SM, l.stream>>>(A, T, x, b, r, L, out_norm, to_sync(sync), to_dist(dist));
+          launch_k(kern, g, SM, l.stream, A, T, x, b, r, L, out_norm, to_sync(sync), to_dist(dist));
           err = cudaGetLastError();
         }
       });
@@ -91,7 +91,7 @@ cudaError_t launch_spmv_t(int px, int py, Launch l, const CsrDev& A, const Tiles
         auto kern = k_spmv<PA, decltype(X)::value, decltype(Y)::value, IDX>;
         static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
         const int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
-        kern<<<g, kThreads, SM, l.stream>>>(A, T, x, y);
+        launch_k(kern, g, SM, l.stream, A, T, x, y);
         err = cudaGetLastError();
       });
     });
@@ -160,7 +160,7 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
           int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
           if (phase == PH_BOOK) g = 1;
           if (g < 1) g = 1;
-          kern<<<g, kThreads, SM, l.stream>>>(A, T, phase, k, v, v_scale, off, out, n, RS, R, Za, to_gate(gate), level,
+          launch_k(kern, g, SM, l.stream, A, T, phase, k, v, v_scale, off, out, n, RS, R, Za, to_gate(gate), level,
                                               cnt, to_sync(sync), to_dist(dist));
           err = cudaGetLastError();
         }

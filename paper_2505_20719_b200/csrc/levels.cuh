@@ -89,6 +89,7 @@ template <int PS, int PW>
 __global__ void __launch_bounds__(256) k_level_start(void* src, const double* src_scale, int writeback, void* dst,
                                                      uint64_t n, LevelState* L, int* dead, Gate gate, int level,
                                                      unsigned long long* cnt, Sync sync, const IoSlot* io, Dist dist) {
+  pdl_wait();
   __shared__ double scratch[64];
   __shared__ double tot[1];
   if (gate.closed()) return;
@@ -100,7 +101,26 @@ __global__ void __launch_bounds__(256) k_level_start(void* src, const double* sr
     const T_<PS> s = src_scale ? cvt<PS>(*src_scale) : Ar<PS>::one();
     T_<PW> acc[1] = {Ar<PW>::zero()};
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t i0 = 0;
+    if (!writeback && aligned16(src) && aligned16(dst)) {
+      // 8 elements per thread and round: 16-byte transactions, same per-element
+      // arithmetic (each thread's running sum just covers 8 neighbours per round)
+      const uint64_t ng = n / kGroup;
+      for (uint64_t g = tid; g < ng; g += stride) {
+        T_<PS> v[kGroup];
+        T_<PW> d[kGroup];
+        ld8<PS>(src, g, v);
+#pragma unroll
+        for (int k = 0; k < kGroup; ++k) {
+          d[k] = cvt<PW>(src_scale ? Ar<PS>::mul(s, v[k]) : v[k]);
+          acc[0] = Ar<PW>::add(acc[0], Ar<PW>::mul(d[k], d[k]));
+        }
+        st8<PW>(dst, g, d);
+      }
+      i0 = ng * kGroup;
+    }
+    for (uint64_t i = i0 + tid; i < n; i += stride) {
       T_<PS> v = ld<PS>(src, i);
       if (src_scale) {
         v = Ar<PS>::mul(s, v);
@@ -110,6 +130,7 @@ __global__ void __launch_bounds__(256) k_level_start(void* src, const double* sr
       st<PW>(dst, i, d);
       acc[0] = Ar<PW>::add(acc[0], Ar<PW>::mul(d, d));
     }
+    pdl_trigger();
     block_sum<PW, 1>(acc, scratch);
     if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
     if (!last_block(sync.counter)) return;
@@ -141,6 +162,7 @@ __global__ void __launch_bounds__(256) k_level_start(void* src, const double* sr
 template <int PW>
 __global__ void __launch_bounds__(256) k_copy_scaled(void* v, const double* scale, void* z, uint64_t n, Gate gate,
                                                      unsigned long long* cnt) {
+  pdl_wait();
   if (gate.closed()) return;
   const T_<PW> s = scale ? cvt<PW>(*scale) : Ar<PW>::one();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -238,6 +260,7 @@ template <int PA, int PZ, int PW, int IDX>
 __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t ld, int j,
                                                    LevelState* L, Gate gate, Sync sync, double* dots, int defer,
                                                    Dist dist) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double res[8];
@@ -262,6 +285,7 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv_dots(CsrDev A, Til
 template <int PW>
 __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, uint64_t ldv, int j, int k0,
                                                    LevelState* L, Gate gate, Sync sync, Dist dist) {
+  pdl_wait();
   __shared__ double scratch[8 * 8];
   __shared__ double res[8];
   if (gate.closed()) return;
@@ -302,10 +326,14 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, ui
 // the same fixed order -> identical h in all CTAs; CTA 0 records the H column).
 // `outer` levels never set their dead flag (the host decides) and report through
 // `info`.
-template <int PW>
-__global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, uint64_t ldv, int j, LevelState* L, int* dead,
+// NJ = min(j + 1, 8) is a kernel template parameter (one instantiation per
+// projection count): the small-NJ kernels then need few registers, run more CTAs
+// per SM and keep two rounds of 16-byte loads in flight per thread.
+template <int PW, int NJ>
+__global__ void __launch_bounds__(256, NJ <= 2 ? 4 : NJ <= 4 ? 3 : 2) k_cgs(void* V, uint64_t n, uint64_t ldv, int j, LevelState* L, int* dead,
                                              Gate gate, int level, int outer, int use_tol, StepInfo* info, Sync sync,
                                              const double* dots, int dots_G, Dist dist) {
+  pdl_wait();
   __shared__ double scratch[64];
   __shared__ double hs[128];
   __shared__ double tot[8];
@@ -330,81 +358,92 @@ __global__ void __launch_bounds__(256) k_cgs(void* V, uint64_t n, uint64_t ldv, 
   };
   T_<PW> acc[1] = {A::zero()};
   T_<PW>* w = static_cast<T_<PW>*>(V) + (size_t)(j + 1) * ldv;
-  // the first <= 8 coefficients and scales live in registers and the loop is
-  // specialised on their count (uniform per launch); 16-byte vector loads when the
-  // slots are 16-byte aligned (n a multiple of the vector width)
-  auto body = [&](auto NJ_) {
-    constexpr int NJ = decltype(NJ_)::value;
-    constexpr int VE = 16 / (int)sizeof(T_<PW>);
-    T_<PW> a[NJ], sc[NJ];
-    auto update = [&](uint64_t i, T_<PW> wi, const T_<PW>* vv) {
+  constexpr int VE = 16 / (int)sizeof(T_<PW>);
+  constexpr bool DEEP = NJ <= 4;  // two load rounds in flight
+  T_<PW> a[NJ], sc[NJ];
+  auto update = [&](uint64_t i, T_<PW> wi, const T_<PW>* vv) {
 #pragma unroll
-      for (int u = 0; u < NJ; ++u) wi = A::add(A::mul(a[u], A::mul(sc[u], vv[u])), wi);
-      for (int k = NJ; k <= j; ++k) {  // long outer cycles only
-        const T_<PW> v = A::mul(cvt<PW>(L->scale[k]), ld<PW>(V, (uint64_t)k * ldv + i));
-        wi = A::add(A::mul(k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]), v), wi);
-      }
-      acc[0] = A::add(acc[0], A::mul(wi, wi));
-      return wi;
-    };
-    auto coefficients = [&]() {
+    for (int u = 0; u < NJ; ++u) wi = A::add(A::mul(a[u], A::mul(sc[u], vv[u])), wi);
+    for (int k = NJ; k <= j; ++k) {  // long outer cycles only
+      const T_<PW> v = A::mul(cvt<PW>(L->scale[k]), ld<PW>(V, (uint64_t)k * ldv + i));
+      wi = A::add(A::mul(k < 128 ? cvt<PW>(hs[k]) : cvt<PW>(-h[k]), v), wi);
+    }
+    acc[0] = A::add(acc[0], A::mul(wi, wi));
+    return wi;
+  };
+  auto coefficients = [&]() {
 #pragma unroll
-      for (int u = 0; u < NJ; ++u) a[u] = cvt<PW>(hs[u]), sc[u] = cvt<PW>(L->scale[u]);
+    for (int u = 0; u < NJ; ++u) a[u] = cvt<PW>(hs[u]), sc[u] = cvt<PW>(L->scale[u]);
+  };
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  if (n % VE == 0 && ldv % VE == 0) {
+    const uint64_t nv = n / VE;
+    const uint4* w4 = reinterpret_cast<const uint4*>(w);
+    struct Round {
+      uint4 v[NJ];
+      uint4 w;
     };
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    if (n % VE == 0 && ldv % VE == 0) {
-      const uint64_t nv = n / VE;
-      const uint4* w4 = reinterpret_cast<const uint4*>(w);
-      uint4 raw[NJ], wr = {0u, 0u, 0u, 0u};
-      auto load = [&](uint64_t e) {
+    auto load = [&](Round& r, uint64_t e) {
+#pragma unroll
+      for (int u = 0; u < NJ; ++u)
+        r.v[u] = reinterpret_cast<const uint4*>(static_cast<const T_<PW>*>(V) + (uint64_t)u * ldv)[e];
+      r.w = w4[e];
+    };
+    auto process = [&](const Round& r, uint64_t e) {
+      T_<PW> wv[VE];
+      memcpy(wv, &r.w, 16);
+#pragma unroll
+      for (int l = 0; l < VE; ++l) {
+        T_<PW> vv[NJ];
 #pragma unroll
         for (int u = 0; u < NJ; ++u)
-          raw[u] = reinterpret_cast<const uint4*>(static_cast<const T_<PW>*>(V) + (uint64_t)u * ldv)[e];
-        wr = w4[e];
-      };
+          memcpy(&vv[u], reinterpret_cast<const char*>(&r.v[u]) + l * sizeof(T_<PW>), sizeof(T_<PW>));
+        wv[l] = update(e * VE + l, wv[l], vv);
+      }
+      uint4 out;
+      memcpy(&out, wv, 16);
+      reinterpret_cast<uint4*>(w)[e] = out;
+    };
+    if constexpr (DEEP) {
+      Round r0, r1;
       uint64_t e = tid;
-      if (e < nv) load(e);
+      if (e < nv) load(r0, e);
+      if (e + stride < nv) load(r1, e + stride);
+      get_h();
+      coefficients();
+      while (e < nv) {
+        process(r0, e);
+        if (e + 2 * stride < nv) load(r0, e + 2 * stride);
+        e += stride;
+        if (e >= nv) break;
+        process(r1, e);
+        if (e + 2 * stride < nv) load(r1, e + 2 * stride);
+        e += stride;
+      }
+    } else {
+      Round r0;
+      uint64_t e = tid;
+      if (e < nv) load(r0, e);
       get_h();
       coefficients();
       for (; e < nv;) {
-        T_<PW> wv[VE];
-        memcpy(wv, &wr, 16);
-#pragma unroll
-        for (int l = 0; l < VE; ++l) {
-          T_<PW> vv[NJ];
-#pragma unroll
-          for (int u = 0; u < NJ; ++u)
-            memcpy(&vv[u], reinterpret_cast<const char*>(&raw[u]) + l * sizeof(T_<PW>), sizeof(T_<PW>));
-          wv[l] = update(e * VE + l, wv[l], vv);
-        }
-        uint4 out;
-        memcpy(&out, wv, 16);
-        reinterpret_cast<uint4*>(w)[e] = out;
+        process(r0, e);
         e += stride;
-        if (e < nv) load(e);
-      }
-    } else {
-      get_h();
-      coefficients();
-      for (uint64_t i = tid; i < n; i += stride) {
-        T_<PW> vv[NJ];
-#pragma unroll
-        for (int u = 0; u < NJ; ++u) vv[u] = ld<PW>(V, (uint64_t)u * ldv + i);
-        w[i] = update(i, w[i], vv);
+        if (e < nv) load(r0, e);
       }
     }
-  };
-  switch (j + 1 < 8 ? j + 1 : 8) {
-    case 1: body(std::integral_constant<int, 1>{}); break;
-    case 2: body(std::integral_constant<int, 2>{}); break;
-    case 3: body(std::integral_constant<int, 3>{}); break;
-    case 4: body(std::integral_constant<int, 4>{}); break;
-    case 5: body(std::integral_constant<int, 5>{}); break;
-    case 6: body(std::integral_constant<int, 6>{}); break;
-    case 7: body(std::integral_constant<int, 7>{}); break;
-    default: body(std::integral_constant<int, 8>{}); break;
+  } else {
+    get_h();
+    coefficients();
+    for (uint64_t i = tid; i < n; i += stride) {
+      T_<PW> vv[NJ];
+#pragma unroll
+      for (int u = 0; u < NJ; ++u) vv[u] = ld<PW>(V, (uint64_t)u * ldv + i);
+      w[i] = update(i, w[i], vv);
+    }
   }
+  pdl_trigger();
   block_sum<PW, 1>(acc, scratch);
   if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = A::wide(acc[0]);
   if (!last_block(sync.counter)) return;
@@ -500,6 +539,7 @@ template <int PZ, int PW, int PX>
 __global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n, uint64_t ldz, LevelState* L, void* x,
                                                       int x_is_zero, Gate gate, int level, unsigned long long* cnt,
                                                       int count_iterations, const IoSlot* io) {
+  pdl_wait();
   __shared__ double ys[1024];
   if (gate.closed()) return;
   if (io) x = io->dst;
@@ -542,7 +582,32 @@ __global__ void __launch_bounds__(256) k_level_finish(const void* Z, uint64_t n,
     T_<C> yy[K > 0 ? K : 1];
 #pragma unroll
     for (int u = 0; u < K; ++u) yy[u] = cvt<C>(ys[u]);
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint64_t i0 = 0;
+    if (k <= K && ldz % kGroup == 0 && aligned16(Z) && aligned16(x)) {
+      // 8 elements per thread and round (16-byte transactions), same sequential
+      // per-element axpy order as below
+      const uint64_t ng = n / kGroup;
+      for (uint64_t g = tid; g < ng; g += stride) {
+        T_<PX> xv[kGroup];
+        if (x_is_zero) {
+#pragma unroll
+          for (int e = 0; e < kGroup; ++e) xv[e] = cvt<PX>(0.0);
+        } else {
+          ld8<PX>(x, g, xv);
+        }
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+          T_<PZ> zz[kGroup];
+          ld8<PZ>(static_cast<const T_<PZ>*>(Z) + (uint64_t)u * ldz, g, zz);
+#pragma unroll
+          for (int e = 0; e < kGroup; ++e) xv[e] = cvt<PX>(AC::add(AC::mul(yy[u], cvt<C>(zz[e])), cvt<C>(xv[e])));
+        }
+        st8<PX>(x, g, xv);
+      }
+      i0 = ng * kGroup;
+    }
+    for (uint64_t i = i0 + tid; i < n; i += stride) {
       T_<PZ> zz[K > 0 ? K : 1];
 #pragma unroll
       for (int u = 0; u < K; ++u) zz[u] = ld<PZ>(Z, (uint64_t)u * ldz + i);
@@ -593,6 +658,7 @@ struct EpiResidual {
 template <int PA, int PX, int PW, int IDX>
 __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
                                                   LevelState* L, double* out_norm, Sync sync, Dist dist) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double tot[1];

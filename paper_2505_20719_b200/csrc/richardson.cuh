@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, Ti
                                                     void* out, uint64_t n, RichState* RS, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, unsigned* bar_count,
                                                     unsigned* bar_gen, const IoSlot* io, uint64_t voff, int flags) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double red[2];
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_rich_phase(CsrDev A, Ti
                                                     const double* v_scale, uint64_t off, void* out, uint64_t n,
                                                     RichState* RS, void* R, void* Za, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, Dist dist) {
+  pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64];
   __shared__ double tot[2];

@@ -209,6 +209,7 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   __syncthreads();
   if (tid == 0)
     for (int s = 0; s < ST; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
+  pdl_trigger();
 }
 
 // ---- gathers ----------------------------------------------------------------------
