@@ -100,6 +100,14 @@ __global__ void __launch_bounds__(256) k_gather(const void* src, const uint32_t*
     st<P>(dst, i, ld<P>(src, idx[i]));
 }
 
+// P16 stream: fp16 value bits | D16 delta << 16, one word per entry
+static __global__ void __launch_bounds__(256) k_pack16(const __half* v, const uint16_t* d, uint32_t* out, uint64_t nnz) {
+  pdl_wait();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride)
+    out[i] = (uint32_t)__half_as_ushort(v[i]) | ((uint32_t)d[i] << 16);
+}
+
 // plain y = A x (any precision triple), for the kernel-level entry point
 template <int PA, int PX, int PY, int IDX>
 __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {

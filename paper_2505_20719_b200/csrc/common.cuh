@@ -92,6 +92,12 @@ template <> struct Ar<P16> {
   __device__ static bool finite(T a) { return (__half_as_ushort(a) & 0x7c00u) != 0x7c00u; }
 };
 
+// reinterpret 16 bits as an fp16 value (P16 stream decode)
+template <class T>
+__device__ __forceinline__ T bits_as(unsigned short b) {
+  return __ushort_as_half(b);
+}
+
 // generic typed load of element i of a precision-tagged array
 template <int P>
 __device__ __forceinline__ T_<P> ld(const void* p, uint64_t i) {

@@ -81,6 +81,7 @@ DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* 
   // the plain u32 stream, for A/B tests)
   const char* colfmt = std::getenv("F3RG_COLUMNS");
   bool d16 = !(colfmt && std::string(colfmt) == "u32") && nnz_ > 0;
+  const bool p16 = !(colfmt && (std::string(colfmt) == "u32" || std::string(colfmt) == "d16"));
   for (uint64_t i = 0; d16 && i < n_; ++i)
     for (uint32_t k = row_ptr[i] + 1; k < row_ptr[i + 1]; ++k)
       if (col_idx[k] - col_idx[k - 1] > 65535u) {
@@ -98,6 +99,11 @@ DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* 
     first_.alloc(fc.size() * 4);
     F3RG_CUDA(cudaMemcpy(dcol_.get(), dc.data(), dc.size() * 2, cudaMemcpyHostToDevice));
     F3RG_CUDA(cudaMemcpy(first_.get(), fc.data(), fc.size() * 4, cudaMemcpyHostToDevice));
+    if (p16) {  // F3RG_COLUMNS=d16 keeps the separate fp16 value + delta streams
+      pk_.alloc(nnz_ * 4 + 32);
+      F3RG_CUDA(cudaMemset(pk_.get(), 0, pk_.bytes()));
+      F3RG_CUDA(launch_pack16(Launch{}, val_[0].get(), dcol_.get<uint16_t>(), pk_.get<uint32_t>(), nnz_));
+    }
   }
   std::vector<uint32_t> r0, k0;
   for (int p = 0; p < 3; ++p) {
@@ -120,6 +126,7 @@ CsrDev DeviceMatrix::csr() const {
   for (int p = 0; p < 3; ++p) c.val[p] = val_[p].get();
   c.dcol = dcol_.get<const uint16_t>();
   c.first = first_.get<const uint32_t>();
+  c.pk = pk_.get<const uint32_t>();
   return c;
 }
 

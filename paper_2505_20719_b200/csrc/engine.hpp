@@ -129,7 +129,7 @@ class DeviceMatrix {
 
  private:
   uint64_t n_ = 0, nnz_ = 0;
-  DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_;
+  DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_, pk_;
   uint32_t ntiles_[3] = {0, 0, 0};
 };
 

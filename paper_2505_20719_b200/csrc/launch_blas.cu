@@ -80,4 +80,10 @@ cudaError_t launch_gather(int p, Launch l, const void* src, const uint32_t* idx,
   return cudaGetLastError();
 }
 
+cudaError_t launch_pack16(Launch l, const void* val16, const uint16_t* dcol, uint32_t* out, uint64_t nnz) {
+  if (nnz == 0) return cudaSuccess;
+  const int g = l.grid ? l.grid : stream_grid();
+  return launch_k(k_pack16, g, 0, l.stream, static_cast<const __half*>(val16), dcol, out, nnz);
+}
+
 }  // namespace f3rg

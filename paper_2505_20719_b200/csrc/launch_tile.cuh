@@ -13,6 +13,17 @@
 
 namespace f3rg {
 
+// column stream of a launch: P16 (packed fp16 value + delta) for the fp16 replica
+// when present, else D16, else u32
+template <int PA, class F>
+inline void dispatch_idx(const CsrDev& A, F&& go) {
+  if constexpr (PA == P16) {
+    if (A.pk) return go(std::integral_constant<int, 2>{});
+  }
+  if (A.dcol) go(std::integral_constant<int, 1>{});
+  else go(std::integral_constant<int, 0>{});
+}
+
 template <class K>
 inline int tile_kernel_grid(K kern, int smem, uint32_t ntiles, bool cap_by_tiles) {
   const int occ = occupancy_blocks(kern, smem);
@@ -47,8 +58,7 @@ cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const 
       });
     });
   };
-  if (A.dcol) go(std::integral_constant<int, 1>{});
-  else go(std::integral_constant<int, 0>{});
+  dispatch_idx<PA>(A, go);
   return err;
 }
 
@@ -75,8 +85,7 @@ cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const T
       });
     });
   };
-  if (A.dcol) go(std::integral_constant<int, 1>{});
-  else go(std::integral_constant<int, 0>{});
+  dispatch_idx<PA>(A, go);
   return err;
 }
 
@@ -96,8 +105,7 @@ cudaError_t launch_spmv_t(int px, int py, Launch l, const CsrDev& A, const Tiles
       });
     });
   };
-  if (A.dcol) go(std::integral_constant<int, 1>{});
-  else go(std::integral_constant<int, 0>{});
+  dispatch_idx<PA>(A, go);
   return err;
 }
 
@@ -136,8 +144,7 @@ cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const
       });
     });
   };
-  if (A.dcol) go(std::integral_constant<int, 1>{});
-  else go(std::integral_constant<int, 0>{});
+  dispatch_idx<PA>(A, go);
   return err;
 }
 
@@ -167,8 +174,7 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
       });
     });
   };
-  if (A.dcol) go(std::integral_constant<int, 1>{});
-  else go(std::integral_constant<int, 0>{});
+  dispatch_idx<PA>(A, go);
   return err;
 }
 

@@ -14,7 +14,9 @@
 // Column stream, IDX = 0: u32 indices (4 B/nnz). IDX = 1 ("D16"): u16 in-row
 // deltas + one u32 first column per row (2 B/nnz + 4 B/row), decoded by a running
 // sum during the (already sequential) row walk -- same columns, same order, a
-// third fewer bytes for an fp16 matrix.
+// third fewer bytes for an fp16 matrix. IDX = 2 ("P16", fp16 matrices only): the
+// D16 delta and the fp16 value of an entry packed in one 32-bit word, so the row
+// walk does one shared-memory load per entry instead of two (same bytes as D16).
 //
 // Tiles: contiguous row ranges with <= NT rows and <= TNNZ nonzeros (built on the
 // host, spec.cpp build_tiles). A row longer than TNNZ gets a tile of its own and is
@@ -36,6 +38,9 @@
 #ifndef F3RG_CHUNK
 #define F3RG_CHUNK 16
 #endif
+#ifndef F3RG_P16_CHUNK  // P16 rows keep the chunk's values in registers too
+#define F3RG_P16_CHUNK 16
+#endif
 
 namespace f3rg {
 
@@ -50,13 +55,13 @@ struct TileCfg {
   // which bounded the kernel below HBM bandwidth once the column bytes shrank.
   static constexpr int TNNZ = PA == P16 ? 7168 : PA == P32 ? 6912 : 4096;
   static constexpr int VAL = 16 / SA;  // value elements per 16 B
-  static constexpr int CS = IDX ? 2 : 4;
+  static constexpr int CS = IDX == 1 ? 2 : 4;
   static constexpr int CAL = 16 / CS;  // column elements per 16 B
-  static constexpr int STAGES = (PA == P16 && IDX == 1) ? F3RG_D16_STAGES : 2;
-  static constexpr int VAL_BYTES = ((TNNZ + 2 * VAL) * SA + 15) / 16 * 16;
+  static constexpr int STAGES = (PA == P16 && IDX >= 1) ? F3RG_D16_STAGES : 2;
+  static constexpr int VAL_BYTES = IDX == 2 ? 0 : ((TNNZ + 2 * VAL) * SA + 15) / 16 * 16;
   static constexpr int COL_BYTES = ((TNNZ + 2 * CAL) * CS + 15) / 16 * 16;
   static constexpr int RP_BYTES = (NT + 12) * 4;
-  static constexpr int FIRST_BYTES = IDX ? (NT + 12) * 4 : 0;
+  static constexpr int FIRST_BYTES = IDX >= 1 ? (NT + 12) * 4 : 0;
   static constexpr int STAGE_BYTES = VAL_BYTES + COL_BYTES + RP_BYTES + FIRST_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 64;
 };
@@ -64,7 +69,8 @@ struct TileCfg {
 // Streams all tiles owned by this CTA (tile t = blockIdx.x + i*gridDim.x) through
 // shared memory and calls epi.row(row, acc) for every row with acc at
 // C = promote(PA, gather precision).
-template <int PA, int C, int IDX, class Gather, class Epi>
+// CH: gather chunk (0 = default: F3RG_CHUNK, or F3RG_P16_CHUNK for the P16 stream)
+template <int PA, int C, int IDX, int CH = 0, class Gather, class Epi>
 __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
   using Cfg = TileCfg<PA, IDX>;
   using TA = T_<PA>;
@@ -72,8 +78,10 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   constexpr int ST = Cfg::STAGES, VAL = Cfg::VAL, CAL = Cfg::CAL;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ST * Cfg::STAGE_BYTES);
   const TA* vals = static_cast<const TA*>(A.val[PA]);
+  static_assert(IDX != 2 || PA == P16, "the packed P16 stream holds fp16 values");
   const TC* cols;
   if constexpr (IDX == 1) cols = A.dcol;
+  else if constexpr (IDX == 2) cols = A.pk;
   else cols = A.ci;
   const uint32_t G = gridDim.x, tid = threadIdx.x;
 
@@ -97,8 +105,9 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
     const uint32_t k0v = k0 & ~(uint32_t)(VAL - 1), k1v = (k1 + VAL - 1) & ~(uint32_t)(VAL - 1);
     const uint32_t k0c = k0 & ~(uint32_t)(CAL - 1), k1c = (k1 + CAL - 1) & ~(uint32_t)(CAL - 1);
     const uint32_t r0a = r0 & ~3u, r1a = (r1 + 1 + 3) & ~3u;
-    const uint32_t vb = (k1v - k0v) * Cfg::SA, cb = (k1c - k0c) * Cfg::CS, rb = (r1a - r0a) * 4u;
-    const uint32_t fb = IDX ? (((r1 + 3) & ~3u) - r0a) * 4u : 0u;
+    const uint32_t vb = IDX == 2 ? 0u : (k1v - k0v) * Cfg::SA, cb = (k1c - k0c) * Cfg::CS,
+                   rb = (r1a - r0a) * 4u;
+    const uint32_t fb = IDX >= 1 ? (((r1 + 3) & ~3u) - r0a) * 4u : 0u;
     mbar_arrive_expect_tx(bar, vb + cb + rb + fb);
     uint8_t* sp = stage_ptr(s);
     if (vb) bulk_g2s(sp, vals + k0v, vb, bar);
@@ -116,7 +125,7 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   // up to CHUNK gathers of a row are issued before the first is consumed (one
   // latency round per CHUNK entries); groups of 8 are unpredicated, only the last
   // partial group is predicated
-  constexpr int CHUNK = F3RG_CHUNK;
+  constexpr int CHUNK = CH ? CH : IDX == 2 ? F3RG_P16_CHUNK : F3RG_CHUNK;
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < T.ntiles; t += G, ++it) {
     const int s = (int)(it % ST);
@@ -141,11 +150,17 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
         const TA* pv = sv + (kb - k0v);
         const TC* pc = sc + (kb - k0c);
         const uint32_t len = ke - kb;
-        uint32_t col = 0;  // D16: running column
-        if constexpr (IDX == 1)
+        uint32_t col = 0;  // D16 / P16: running column
+        if constexpr (IDX >= 1)
           col = reinterpret_cast<const uint32_t*>(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES + Cfg::RP_BYTES)[row - r0a];
-        auto column = [&](uint32_t q) -> uint32_t {
-          if constexpr (IDX == 1) {
+        // column of entry q (and, P16, its value out of the same word)
+        auto fetch = [&](uint32_t q, TA& a) -> uint32_t {
+          if constexpr (IDX == 2) {
+            const uint32_t w = pc[q];
+            if (q > 0) col += w >> 16;
+            a = bits_as<TA>((unsigned short)(w & 0xffffu));
+            return col;
+          } else if constexpr (IDX == 1) {
             if (q > 0) col += pc[q];
             return col;
           } else {
@@ -155,28 +170,33 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
         for (uint32_t q = 0; q < len; q += CHUNK) {
           const uint32_t cnt = len - q < (uint32_t)CHUNK ? len - q : (uint32_t)CHUNK;
           typename Gather::Raw xs[CHUNK];
+          TA av[CHUNK];  // P16 values (unused otherwise)
 #pragma unroll
           for (int b = 0; b < CHUNK / 8; ++b) {
             if ((uint32_t)(8 * b + 8) <= cnt) {
 #pragma unroll
-              for (int u = 0; u < 8; ++u) xs[8 * b + u] = g.load(column(q + 8 * b + u));
+              for (int u = 0; u < 8; ++u) xs[8 * b + u] = g.load(fetch(q + 8 * b + u, av[8 * b + u]));
             } else {
 #pragma unroll
               for (int u = 0; u < 8; ++u)
-                if ((uint32_t)(8 * b + u) < cnt) xs[8 * b + u] = g.load(column(q + 8 * b + u));
+                if ((uint32_t)(8 * b + u) < cnt) xs[8 * b + u] = g.load(fetch(q + 8 * b + u, av[8 * b + u]));
             }
           }
+          auto aval = [&](int i) -> TA {
+            if constexpr (IDX == 2) return av[i];
+            else return pv[q + i];
+          };
 #pragma unroll
           for (int b = 0; b < CHUNK / 8; ++b) {
             if ((uint32_t)(8 * b + 8) <= cnt) {
 #pragma unroll
               for (int u = 0; u < 8; ++u)
-                acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[q + 8 * b + u]), g.value(xs[8 * b + u])));
+                acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(aval(8 * b + u)), g.value(xs[8 * b + u])));
             } else {
 #pragma unroll
               for (int u = 0; u < 8; ++u)
                 if ((uint32_t)(8 * b + u) < cnt)
-                  acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(pv[q + 8 * b + u]), g.value(xs[8 * b + u])));
+                  acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(aval(8 * b + u)), g.value(xs[8 * b + u])));
             }
           }
         }
@@ -185,16 +205,24 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
     } else if (tid == 0) {
       T_<C> acc = Ar<C>::zero();
       uint32_t col = 0;
-      if constexpr (IDX == 1) col = A.first[r0];
+      if constexpr (IDX >= 1) col = A.first[r0];
       for (uint32_t k = k0; k < k1; ++k) {
         uint32_t c;
-        if constexpr (IDX == 1) {
+        TA a;
+        if constexpr (IDX == 2) {
+          const uint32_t w = A.pk[k];
+          if (k > k0) col += w >> 16;
+          c = col;
+          a = bits_as<TA>((unsigned short)(w & 0xffffu));
+        } else if constexpr (IDX == 1) {
           if (k > k0) col += A.dcol[k];
           c = col;
+          a = vals[k];
         } else {
           c = A.ci[k];
+          a = vals[k];
         }
-        acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vals[k]), g.value(g.load(c))));
+        acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(a), g.value(g.load(c))));
       }
       e.row(r0, acc);
     }

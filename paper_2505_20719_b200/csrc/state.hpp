@@ -18,6 +18,10 @@ struct CsrDev {
   // deltas instead of 4-byte indices.
   const uint16_t* dcol = nullptr;   // nnz (+pad)
   const uint32_t* first = nullptr;  // n (+pad)
+  // "P16" stream of the fp16 replica: pk[k] = fp16 bits of val16[k] | dcol[k] << 16,
+  // one 4-byte word per entry (one shared-memory load per entry instead of two);
+  // present with the D16 stream
+  const uint32_t* pk = nullptr;     // nnz (+pad)
 };
 
 struct TilesDev {
