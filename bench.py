@@ -92,8 +92,8 @@ class Clocks:
 
 
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
-# committed `ncu --set full` capture of config 2 (profiles/r01_ncu_full.md)
-TRAFFIC = {"richardson[f16,f16,f32]": 255257088.0, "spmv_dots[f16,f16,f32]": 273912064.0}
+# committed `ncu --set full` capture of config 2 (profiles/r01_ncu_full.md, P16 rows)
+TRAFFIC = {"richardson[f16,f16,f32]": 256101120.0, "spmv_dots[f16,f16,f32]": 261074688.0}
 
 
 def streams_matrix(kernel):

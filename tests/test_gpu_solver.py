@@ -74,16 +74,58 @@ def test_config1_full_vs_reference(cuda, reference):
     assert run.report.precond_invocations == ref.precond_invocations
 
 
-def test_u32_and_d16_column_streams_solve_identically(probs, monkeypatch):
+def test_column_streams_solve_identically(probs, monkeypatch):
+    """P16 (default: packed fp16 value + delta), D16 and u32 column streams carry the
+    same columns in the same order: bitwise identical solves"""
     import paper_2505_20719_b200 as f
     name, p = probs[3]
     s1, _ = _solver(p, F3R16)
     r1 = s1.run(p.b, f.RunOptions(tol=TOL))
-    monkeypatch.setenv("F3RG_COLUMNS", "u32")
-    s2, _ = _solver(p, F3R16)
-    r2 = s2.run(p.b, f.RunOptions(tol=TOL))
-    assert r1.report.residual_history == r2.report.residual_history
-    assert np.array_equal(r1.x, r2.x)
+    for fmt in ("d16", "u32"):
+        monkeypatch.setenv("F3RG_COLUMNS", fmt)
+        s2, _ = _solver(p, F3R16)
+        r2 = s2.run(p.b, f.RunOptions(tol=TOL))
+        assert r1.report.residual_history == r2.report.residual_history, fmt
+        assert np.array_equal(r1.x, r2.x), fmt
+
+
+def _reference_run(config):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "reference_runs.json")
+    return json.load(open(path)).get(f"config{config}/fp16-f3r")
+
+
+@pytest.mark.parametrize("config", [2, 3, 4, 5])
+def test_full_config_vs_reference(cuda, config):
+    """BASELINE configs at full size against the recorded runs of the UNMODIFIED
+    reference (tests/golden/reference_runs.json): converged to 1e-10 on the fp64
+    true residual, outer count within 10 %. Config 5 (n = 2e7) is the documented
+    exception: the reference's sequential fp32 dots over 2e7 entries lose digits
+    that our tree reductions keep, and it converges in 2 outer steps instead of 3
+    -- exactly what the oracle gives with pairwise dots
+    (tests/golden/dot_order_config5.jsonl, tools/dot_order_experiment.py)."""
+    import json
+    import os
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+    ref = _reference_run(config)
+    if ref is None:
+        pytest.skip(f"no recorded reference run for config {config} yet")
+    p = problems.problem(config)
+    assert (p.n, p.nnz) == (ref["n"], ref["nnz"])
+    s, _ = _solver(p, F3R16)
+    bd = cuda.from_numpy(p.b).cuda()
+    rep = s.run(bd, f.RunOptions(tol=TOL), want_x=False).report
+    assert rep.converged and rep.final_true_residual <= TOL, rep
+    want = ref["outer_iterations"]
+    if config == 5:
+        path = os.path.join(os.path.dirname(__file__), "golden", "dot_order_config5.jsonl")
+        runs = {r["dots"]: r for r in map(json.loads, open(path))}
+        assert runs["sequential"]["outer"] == want              # the oracle reproduces the reference
+        assert runs["sequential"]["hist"] == pytest.approx(ref["residual_history"], rel=1e-12)
+        want = runs["pairwise"]["outer"]                        # the order class of our reductions
+    assert abs(rep.outer_iterations - want) <= max(1, round(0.1 * want)), (rep.outer_iterations, want)
 
 
 def test_determinism_bitwise(probs):
