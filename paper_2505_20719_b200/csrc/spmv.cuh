@@ -48,11 +48,10 @@ template <int PA, int IDX = 0>
 struct TileCfg {
   static constexpr int NT = 256;  // threads = max rows per tile
   static constexpr int SA = (int)sizeof(T_<PA>);
-  // Two CTAs per SM (<= ~113 KB of shared memory each). The tile table is shared by
-  // both column formats, so TNNZ depends on PA only: fp16 / fp32 tiles hold 256
-  // rows of a 27-point stencil, fp64 ones 151. The smaller D16 fp16 tiles afford a
-  // third stage -- with 2 the next tile's load gets only one compute period to land,
-  // which bounded the kernel below HBM bandwidth once the column bytes shrank.
+  // Three CTAs per SM (F3RG_TILE_MINB; 2 stages of <= ~31 KB for fp16 D16/P16
+  // tiles). The tile table is shared by all column formats, so TNNZ depends on PA
+  // only: fp16 / fp32 tiles hold 256 rows of a 27-point stencil, fp64 ones 151.
+  // Stage count and chunk size are from tools/variant_sweep.py on config 2.
   static constexpr int TNNZ = PA == P16 ? 7168 : PA == P32 ? 6912 : 4096;
   static constexpr int VAL = 16 / SA;  // value elements per 16 B
   static constexpr int CS = IDX == 1 ? 2 : 4;
