@@ -140,3 +140,17 @@ def test_partition_rejects_unsupported(cuda, probs):
         partition.LocalPartition(_csr(p), "F8:f64/f64 > R3:f16,c=64 > identity", 2)
     with pytest.raises(f.UnsupportedError):
         partition.LocalPartition(_csr(p), "R2:f64,c=64 > identity", 2)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_partitioned_ragged(cuda, oracle, P):
+    """odd n (2431 rows, blocks of 811/810/810): halo pads, unaligned block sizes"""
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import partition, problems
+    p = problems.problem(1, grid=(17, 13, 11))
+    x = oracle.round_vec(1, np.random.default_rng(5).uniform(-1, 1, p.n))
+    want = oracle.spmv((p.n, p.row_ptr, p.col_idx), oracle.round_vec(0, p.values), 0, x, 1, 1)
+    assert np.array_equal(partition.local_spmv(_csr(p), P, 0, 1, 1, x), want)
+    lp = partition.LocalPartition(_csr(p), F3R16, P)
+    _, rr = lp.run(p.b, f.RunOptions(tol=TOL))
+    assert rr[0].converged and rr[0].final_true_residual <= TOL

@@ -217,6 +217,25 @@ def test_other_specs_match_oracle(cuda, oracle, spec):
         abs(run.report.outer_iterations - ref.outer_iterations) > 0
 
 
+@pytest.mark.parametrize("grid", [(17, 13, 11), (3, 5, 7)])
+def test_ragged_sizes_match_oracle(cuda, oracle, grid):
+    """n not a multiple of the 8-element vector groups / 16-byte transactions nor of
+    the tile height: the scalar remainders of every vectorised kernel and partial
+    tiles are exercised (n = 2431, and n = 105 < one tile)"""
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import problems
+    p = problems.problem(1, grid=grid)
+    assert p.n % 8 != 0
+    for spec in (F3R16, F3R32):
+        s, _ = _solver(p, spec)
+        run = s.run(p.b, f.RunOptions(tol=TOL))
+        ref = oracle.solve((p.n, p.row_ptr, p.col_idx), p.values, spec, p.b, tol=TOL)
+        assert run.report.converged and ref.converged
+        assert run.report.final_true_residual <= TOL
+        assert abs(run.report.outer_iterations - ref.outer_iterations) <= max(1, round(0.1 * ref.outer_iterations))
+        assert normwise(run.x, ref.x) < 1e-6
+
+
 def test_build_validation(cuda):
     import paper_2505_20719_b200 as f
     from paper_2505_20719_b200 import problems
