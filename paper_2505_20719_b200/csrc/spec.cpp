@@ -205,12 +205,7 @@ std::string Spec::to_string() const {
 }
 
 // ---- tiles --------------------------------------------------------------------------
-uint32_t tile_max_rows() { return 256; }
-#ifndef F3RG_TILE_SCALE
-#define F3RG_TILE_SCALE 8
-#endif
-// = TileCfg<PA>::TNNZ (spmv.cuh)
-uint32_t tile_max_nnz(int pa) { return pa == 0 ? 7168u : pa == 1 ? 6912u : 4096u; }
+// (tile_max_rows / tile_max_nnz are defined next to TileCfg, launch_level.cu)
 
 void build_tiles(uint64_t n, const uint32_t* rp, uint32_t max_rows, uint32_t max_nnz, std::vector<uint32_t>& r0,
                  std::vector<uint32_t>& k0) {
