@@ -199,7 +199,9 @@ Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_ki
         throw Error(ERR_UNSUPPORTED, "row-block partition: Richardson levels with m > 2 are not implemented");
   }
   build_levels();
-  if (!ex_) capture_inner_graph();  // partitioned solves launch eagerly
+  // the in-process transport synchronises ranks on the host between kernels, so it
+  // launches eagerly; NCCL exchanges are stream work and go into the graph
+  if (!ex_ || ex_->capturable()) capture_inner_graph();
 }
 
 Solver::~Solver() {

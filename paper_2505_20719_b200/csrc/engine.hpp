@@ -155,6 +155,8 @@ class Exchange {
   virtual double* all_buf() = 0;
   // stream the rank's solver must use (nullptr: its own)
   virtual cudaStream_t stream() const { return nullptr; }
+  // exchanges are pure stream work (capturable into the inner CUDA graph)
+  virtual bool capturable() const { return false; }
 };
 
 // P ranks of one process sharing the current device and ONE stream (each rank's
@@ -218,6 +220,7 @@ class NcclExchange : public Exchange {
   void allgather(double* loc, double* all, cudaStream_t s) override;
   double* loc_buf() override { return loc_.get<double>(); }
   double* all_buf() override { return all_.get<double>(); }
+  bool capturable() const override { return true; }
   static void unique_id(void* out128);
 
  private:
