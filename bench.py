@@ -171,7 +171,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": min(args.warmup, 1), "ms_per_step": per_outer * 1e3, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "mixed f64/f32/f16 (software binary16)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "mixed f64/f32/f16 (software binary16)",
         "data": "synthetic", "config": _config(args, p),
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -342,7 +342,7 @@ def run_ours(args):
 
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "mixed f64/f32/f16", "data": "synthetic", "config": _config(args, p),
         "outer_iterations": outer, "final_true_residual": run.report.final_true_residual,
         "roofline": {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak,
