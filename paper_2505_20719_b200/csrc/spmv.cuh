@@ -38,6 +38,9 @@
 #ifndef F3RG_CHUNK
 #define F3RG_CHUNK 16
 #endif
+#ifndef F3RG_TNNZ16  // entries per fp16 tile (256 rows of a 27-point stencil)
+#define F3RG_TNNZ16 7168
+#endif
 #ifndef F3RG_P16_CHUNK  // P16 rows keep the chunk's values in registers too
 #define F3RG_P16_CHUNK 16
 #endif
@@ -52,7 +55,7 @@ struct TileCfg {
   // tiles). The tile table is shared by all column formats, so TNNZ depends on PA
   // only: fp16 / fp32 tiles hold 256 rows of a 27-point stencil, fp64 ones 151.
   // Stage count and chunk size are from tools/variant_sweep.py on config 2.
-  static constexpr int TNNZ = PA == P16 ? 7168 : PA == P32 ? 6912 : 4096;
+  static constexpr int TNNZ = PA == P16 ? F3RG_TNNZ16 : PA == P32 ? 6912 : 4096;
   static constexpr int VAL = 16 / SA;  // value elements per 16 B
   static constexpr int CS = IDX == 1 ? 2 : 4;
   static constexpr int CAL = 16 / CS;  // column elements per 16 B

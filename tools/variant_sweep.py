@@ -12,12 +12,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+# compile-time knobs of spmv.cuh: CTAs per SM (register budget), fp16 pipeline
+# depth, gather chunk (u32/D16 streams, and P16), fp16 tile size
 VARIANTS = {
-    "m2_s3_c32": ["F3RG_TILE_MINB=2", "F3RG_D16_STAGES=3", "F3RG_CHUNK=32"],
     "m2_s3_c16": ["F3RG_TILE_MINB=2", "F3RG_D16_STAGES=3", "F3RG_CHUNK=16"],
     "m3_s2_c16": ["F3RG_TILE_MINB=3", "F3RG_D16_STAGES=2", "F3RG_CHUNK=16"],
-    "m3_s2_c8": ["F3RG_TILE_MINB=3", "F3RG_D16_STAGES=2", "F3RG_CHUNK=8"],
-    "m4_s1_c8": ["F3RG_TILE_MINB=4", "F3RG_D16_STAGES=1", "F3RG_CHUNK=8"],
+    "m3_s2_c8": ["F3RG_TILE_MINB=3", "F3RG_D16_STAGES=2", "F3RG_CHUNK=8", "F3RG_P16_CHUNK=8"],
+    "m4_t5k": ["F3RG_TILE_MINB=4", "F3RG_TNNZ16=5120"],
 }
 if os.environ.get("SWEEP"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP"].split(",")}
