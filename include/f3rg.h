@@ -151,6 +151,15 @@ int f3rg_richardson_state(f3rg_richardson* r, double* omegas_host, uint64_t* cou
 /* v, z: device vectors at the Richardson precision */
 int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t stream);
 
+/* ---- the reference's fp64 competitor solvers (src/cg.cpp:22-171: cg_solve,
+ *      bicgstab_solve) with M = identity, on the device. which: 0 = CG, 1 = BiCGStab.
+ *      b, x: HOST fp64 arrays (x may be NULL). history (optional, hist_cap entries)
+ *      receives the relative residuals, entry 0 = 1 (ConvergenceReport semantics).
+ *      CG on an indefinite operator returns F3RG_ESOLVER, as the reference throws
+ *      SolverError; breakdown / cap are report flags ("breakdown", "capped"). */
+int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* b_host, double* x_host, double tol,
+                      uint64_t max_precond_invocations, f3rg_report* rep, double* history, uint64_t hist_cap);
+
 /* ---- row-block partition over P ranks ---------
  * Rows split by the reference's rule (src/ilu.cpp:47-54: base = n/P, remainder to the
  * leading blocks). Each rank keeps its rows of A and of every Krylov vector; SpMV

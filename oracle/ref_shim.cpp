@@ -25,6 +25,7 @@
 #include <omp.h>
 #endif
 
+#include "f3r/cg.hpp"
 #include "f3r/csr.hpp"
 #include "f3r/dense_vector.hpp"
 #include "f3r/fgmres.hpp"
@@ -352,6 +353,36 @@ int ref_solve(void* h, const char* spec, const double* b, double tol, int max_ou
     std::strncpy(rep->flag, r.flag.c_str(), sizeof(rep->flag) - 1);
     std::strncpy(rep->id, solver.id().c_str(), sizeof(rep->id) - 1);
     if (x_out) read_vec(run.x, x_out);
+  });
+}
+
+// The reference's competitor solvers (src/cg.cpp:22-171) with M = IdentityPrecond:
+// which = 0 cg_solve, 1 bicgstab_solve. Same report layout as ref_solve.
+int ref_krylov_solve(void* h, int which, const double* b, double tol, uint64_t max_precond, double* x_out,
+                     double* history, uint64_t hist_cap, RefReport* rep) {
+  return guarded([&] {
+    auto* m = static_cast<RefMatrix*>(h);
+    const std::size_t n = m->reps.a64.rows();
+    f3r::IdentityPrecond ident(n);
+    f3r::ReferenceSolveOptions opts;
+    opts.tol = tol;
+    opts.max_precond_invocations = max_precond;
+    const DenseVector bv = make_vec(b, n, 2);
+    const auto t0 = std::chrono::steady_clock::now();
+    const f3r::ConvergenceReport r = which == 0 ? f3r::cg_solve(m->reps.a64, ident, bv, opts)
+                                                : f3r::bicgstab_solve(m->reps.a64, ident, bv, opts);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::memset(rep, 0, sizeof(*rep));
+    rep->converged = r.converged;
+    rep->outer_iterations = r.outer_iterations;
+    rep->precond_invocations = r.precond_invocations;
+    rep->final_true_residual = r.final_true_residual;
+    rep->wall_seconds = secs;
+    rep->n_history = r.residual_history.size();
+    for (std::size_t i = 0; i < r.residual_history.size() && i < hist_cap; ++i) history[i] = r.residual_history[i];
+    std::strncpy(rep->flag, r.flag.c_str(), sizeof(rep->flag) - 1);
+    std::strncpy(rep->id, r.solver_id.c_str(), sizeof(rep->id) - 1);
+    (void)x_out;
   });
 }
 

@@ -32,7 +32,8 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 CXX = "g++"
 
-CU_SRCS = ["launch_t16.cu", "launch_t32.cu", "launch_t64.cu", "launch_level.cu", "launch_rich.cu", "launch_blas.cu"]
+CU_SRCS = ["launch_t16.cu", "launch_t32.cu", "launch_t64.cu", "launch_level.cu", "launch_rich.cu", "launch_blas.cu",
+           "launch_krylov.cu"]
 CPP_SRCS = ["engine.cpp", "spec.cpp", "capi.cpp", "problems.cpp", "partition.cpp", "exchange.cpp"]
 
 

@@ -372,6 +372,23 @@ int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t 
 
 }  // extern "C"
 
+// ---- fp64 CG / BiCGStab -------------------------------------------------------------
+extern "C" int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* b_host, double* x_host, double tol,
+                                 uint64_t max_precond, f3rg_report* rep, double* history, uint64_t hist_cap) {
+  return guarded([&] {
+    if (!a || !b_host) throw Error(ERR_DIMENSION, "null argument");
+    const uint64_t n = a->m->rows();
+    KrylovSolver ks(a->m);
+    DevBuf b(n * 8 + 16), x(n * 8 + 16);
+    F3RG_CUDA(cudaMemcpy(b.get(), b_host, n * 8, cudaMemcpyHostToDevice));
+    const Report r = ks.solve(which, b.get<double>(), x.get<double>(), tol, max_precond, nullptr);
+    if (x_host) F3RG_CUDA(cudaMemcpy(x_host, x.get(), n * 8, cudaMemcpyDeviceToHost));
+    fill_report(r, rep);
+    for (uint64_t i = 0; history && i < r.residual_history.size() && i < hist_cap; ++i)
+      history[i] = r.residual_history[i];
+  });
+}
+
 // ---- row-block partition ----------------------------------------
 struct f3rg_comm {
   int P = 1;

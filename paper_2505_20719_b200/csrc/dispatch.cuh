@@ -48,6 +48,20 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), int grid, int smem, cudaStre
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
+// one-thread scalar kernel (state updates between batched kernels)
+template <class... KArgs, class... Args>
+inline cudaError_t launch_k1(void (*kern)(KArgs...), cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // occupancy-derived persistent grid for a tile kernel instantiation (cached per
 // instantiation by the caller through a function-local static)

@@ -785,3 +785,141 @@ std::vector<unsigned long long> Solver::level_invocations() {
 }
 
 }  // namespace f3rg
+
+// ---- fp64 CG / BiCGStab (reference src/cg.cpp:22-171) ---------------------------------
+namespace f3rg {
+
+KrylovSolver::KrylovSolver(std::shared_ptr<DeviceMatrix> a) : a_(std::move(a)), n_(a_->rows()) {
+  F3RG_CUDA(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking));
+  for (DevBuf* b : {&x_, &r_, &p_, &q_, &s_, &t_, &rhat_, &tmp_}) b->alloc(n_ * 8 + 16);
+  state_.alloc(sizeof(KState));
+  partials_.alloc((size_t)max_partial_blocks() * 16 * sizeof(double));
+  counter_.alloc(64);
+  norm_.alloc(64);
+  F3RG_CUDA(cudaMemset(counter_.get(), 0, counter_.bytes()));
+  F3RG_CUDA(cudaHostAlloc((void**)&stage_host_, 4096, cudaHostAllocDefault));
+}
+
+KrylovSolver::~KrylovSolver() {
+  if (stage_host_) cudaFreeHost(stage_host_);
+  if (own_) cudaStreamDestroy(own_);
+}
+
+double KrylovSolver::true_rel(const double* b, double bnorm, cudaStream_t s) {
+  // src/cg.cpp:10-17: spmv(a, x, ax); add_scaled(b, -1, ax, r); norm2(r) / bnorm
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  F3RG_CUDA(launch_residual(2, 2, 2, Launch{0, s}, a_->csr(), a_->tiles(2), x_.get(), b, tmp_.get(), nullptr,
+                            norm_.get<double>(), sync));
+  F3RG_CUDA(cudaMemcpyAsync(stage_host_, norm_.get(), 8, cudaMemcpyDeviceToHost, s));
+  F3RG_CUDA(cudaStreamSynchronize(s));
+  return stage_host_[0] / bnorm;
+}
+
+Report KrylovSolver::solve(int which, const double* b, double* x_out, double tol, unsigned long long max_precond,
+                           cudaStream_t stream) {
+  if (which != 0 && which != 1) throw Error(ERR_SOLVER, "krylov solve: which must be 0 (cg) or 1 (bicgstab)");
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t s = stream ? stream : own_;
+  const uint64_t n = n_;
+  Report rep;
+  rep.solver_id = which == 0 ? "cg" : "bicgstab";
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  auto read = [&](const void* dev, size_t bytes) {
+    F3RG_CUDA(cudaMemcpyAsync(stage_host_, dev, bytes, cudaMemcpyDeviceToHost, s));
+    F3RG_CUDA(cudaStreamSynchronize(s));
+  };
+  F3RG_CUDA(launch_norm2(2, Launch{0, s}, b, n, norm_.get<double>(), sync));
+  read(norm_.get(), 8);
+  const double bnorm = stage_host_[0];
+  rep.residual_history.push_back(bnorm == 0.0 ? 0.0 : 1.0);
+  if (bnorm == 0.0) {
+    rep.converged = true;
+    if (x_out) F3RG_CUDA(cudaMemsetAsync(x_out, 0, n * 8, s));
+    F3RG_CUDA(cudaStreamSynchronize(s));
+    return rep;
+  }
+  const unsigned long long cap = max_precond + 2;
+  if (hist_.bytes() < cap * 8) hist_.alloc(cap * 8);
+  F3RG_CUDA(cudaMemsetAsync(x_.get(), 0, n * 8, s));
+  F3RG_CUDA(cudaMemcpyAsync(r_.get(), b, n * 8, cudaMemcpyDeviceToDevice, s));  // x0 = 0: r = b
+  KState h{};
+  h.bnorm = bnorm;
+  h.tol = tol;
+  h.rho = h.alpha = h.omega = 1.0;
+  h.max_precond = max_precond;
+  h.hist_cap = cap;
+  h.hist = hist_.get<double>();
+  if (which == 0) {  // z = M r = r, p = z, rz = (r, z)
+    F3RG_CUDA(cudaMemcpyAsync(p_.get(), r_.get(), n * 8, cudaMemcpyDeviceToDevice, s));
+    F3RG_CUDA(launch_dot(2, 2, 2, Launch{0, s}, r_.get(), r_.get(), n, norm_.get<double>(), sync));
+    read(norm_.get(), 8);
+    h.rz = stage_host_[0];
+    h.precond = 1;
+  } else {  // rhat = r; p = v = 0
+    F3RG_CUDA(cudaMemcpyAsync(rhat_.get(), r_.get(), n * 8, cudaMemcpyDeviceToDevice, s));
+    F3RG_CUDA(cudaMemsetAsync(p_.get(), 0, n * 8, s));
+    F3RG_CUDA(cudaMemsetAsync(q_.get(), 0, n * 8, s));
+  }
+  F3RG_CUDA(cudaMemcpyAsync(state_.get(), &h, sizeof h, cudaMemcpyHostToDevice, s));
+  KState* S = state_.get<KState>();
+  const CsrDev A = a_->csr();
+  const TilesDev T = a_->tiles(2);
+  double* x = x_.get<double>();
+  double* r = r_.get<double>();
+  double* p = p_.get<double>();
+  double* v = q_.get<double>();  // CG: q; BiCGStab: v
+  const int batch = 8;           // iterations enqueued per host synchronisation
+  for (;;) {
+    for (int k = 0; k < batch; ++k) {
+      if (which == 0) {
+        F3RG_CUDA(launch_cg_spmv(Launch{0, s}, A, T, p, v, S, sync));
+        F3RG_CUDA(launch_cg_update(Launch{0, s}, x, r, p, v, n, S, sync));
+        F3RG_CUDA(launch_cg_next(Launch{0, s}, S));
+        F3RG_CUDA(launch_cg_p(Launch{0, s}, p, r, n, S));
+      } else {
+        F3RG_CUDA(launch_bi_rho(Launch{0, s}, rhat_.get<double>(), r, n, S, sync));
+        F3RG_CUDA(launch_bi_p(Launch{0, s}, p, v, r, n, S));
+        F3RG_CUDA(launch_bi_v(Launch{0, s}, A, T, p, v, rhat_.get<double>(), S, sync));
+        F3RG_CUDA(launch_bi_s(Launch{0, s}, s_.get<double>(), r, v, n, S));
+        F3RG_CUDA(launch_bi_t(Launch{0, s}, A, T, s_.get<double>(), t_.get<double>(), S, sync));
+        F3RG_CUDA(launch_bi_update(Launch{0, s}, x, r, p, s_.get<double>(), t_.get<double>(), n, S, sync));
+      }
+    }
+    read(S, sizeof h);
+    std::memcpy(&h, stage_host_, sizeof h);
+    if (h.stop == KS_RUN) continue;
+    if (h.stop == KS_TOL) {
+      const double tr = true_rel(b, bnorm, s);
+      if (tr < tol) {
+        rep.converged = true;
+        rep.final_true_residual = tr;
+        break;
+      }
+      // the reference carries on with the iteration (cap test, then CG's z/rz/beta/p)
+      F3RG_CUDA(launch_krylov_resume(Launch{0, s}, S));
+      if (which == 0) {
+        F3RG_CUDA(launch_cg_next(Launch{0, s}, S));
+        F3RG_CUDA(launch_cg_p(Launch{0, s}, p, r, n, S));
+      }
+      continue;
+    }
+    if (h.stop == KS_INDEFINITE) throw Error(ERR_SOLVER, "cg: indefinite operator detected");
+    rep.flag = h.stop == KS_CAPPED ? "capped" : "breakdown";
+    rep.final_true_residual = true_rel(b, bnorm, s);
+    break;
+  }
+  rep.outer_iterations = h.it;
+  rep.precond_invocations = h.precond;
+  if (h.it > 0) {
+    std::vector<double> hist(h.it);
+    F3RG_CUDA(cudaMemcpyAsync(hist.data(), hist_.get<double>() + 1, h.it * 8, cudaMemcpyDeviceToHost, s));
+    F3RG_CUDA(cudaStreamSynchronize(s));
+    rep.residual_history.insert(rep.residual_history.end(), hist.begin(), hist.end());
+  }
+  if (x_out) F3RG_CUDA(cudaMemcpyAsync(x_out, x, n * 8, cudaMemcpyDeviceToDevice, s));
+  F3RG_CUDA(cudaStreamSynchronize(s));
+  rep.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return rep;
+}
+
+}  // namespace f3rg

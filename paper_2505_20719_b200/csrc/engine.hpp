@@ -328,4 +328,26 @@ class Solver {
   std::vector<std::unique_ptr<ProfRec>> prof_;
 };
 
+// ---- fp64 competitor solvers (reference src/cg.cpp:22-171), M = identity ------------
+class KrylovSolver {
+ public:
+  explicit KrylovSolver(std::shared_ptr<DeviceMatrix> a);
+  ~KrylovSolver();
+  KrylovSolver(const KrylovSolver&) = delete;
+  KrylovSolver& operator=(const KrylovSolver&) = delete;
+  // which: 0 = cg_solve, 1 = bicgstab_solve. b, x: device fp64 vectors (x may be
+  // null); stream 0 = own stream. Throws Error(ERR_SOLVER) where the reference
+  // throws SolverError (CG on an indefinite operator).
+  Report solve(int which, const double* b, double* x, double tol, unsigned long long max_precond,
+               cudaStream_t stream);
+
+ private:
+  double true_rel(const double* b, double bnorm, cudaStream_t s);
+  std::shared_ptr<DeviceMatrix> a_;
+  uint64_t n_ = 0;
+  DevBuf x_, r_, p_, q_, s_, t_, rhat_, tmp_, hist_, state_, partials_, counter_, norm_;
+  double* stage_host_ = nullptr;
+  cudaStream_t own_ = nullptr;
+};
+
 }  // namespace f3rg

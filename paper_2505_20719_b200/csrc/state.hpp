@@ -80,4 +80,14 @@ struct RichState {
   void* Zb;
 };
 
+// Scalar state of the fp64 CG / BiCGStab solvers (krylov.cuh), device-resident
+enum { KS_RUN = 0, KS_TOL = 1, KS_CAPPED = 2, KS_INDEFINITE = 3, KS_BREAKDOWN = 4 };
+struct KState {
+  double bnorm, tol;
+  double rz, alpha, beta, rho, omega, rr;
+  unsigned long long it, precond, max_precond, hist_cap;
+  double* hist;  // residual history, hist[0] = 1
+  int stop;
+};
+
 }  // namespace f3rg

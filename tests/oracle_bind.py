@@ -239,6 +239,8 @@ class Reference:
         L.ref_solve.argtypes = [C.c_void_p, C.c_char_p, _dp, C.c_double, C.c_int, C.c_uint64, C.c_int, C.c_void_p,
                                 _dp, C.c_uint64, C.POINTER(_RefReport)]
         L.ref_spec_canonical.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64]
+        L.ref_krylov_solve.argtypes = [C.c_void_p, C.c_int, _dp, C.c_double, C.c_uint64, C.c_void_p, _dp,
+                                       C.c_uint64, C.POINTER(_RefReport)]
         L.ref_set_threads.argtypes = [C.c_int]
         L.ref_max_threads.restype = C.c_int
 
@@ -357,6 +359,16 @@ class Reference:
         return Report(bool(rep.converged), rep.outer_iterations, rep.precond_invocations, rep.final_true_residual,
                       list(rep.level_iterations[:rep.n_levels]), list(hist[:min(rep.n_history, hist_cap)]),
                       list(rep.omegas[:rep.n_omegas]), rep.flag.decode(), rep.wall_seconds, rep.id.decode(), x=x)
+
+    def krylov_solve(self, mat, which, b, tol=1e-10, max_precond=19200, hist_cap=1 << 16) -> Report:
+        """reference cg_solve (which="cg") / bicgstab_solve ("bicgstab"), src/cg.cpp:22-171, M = identity"""
+        hist = np.zeros(hist_cap)
+        rep = _RefReport()
+        self._check(self.lib.ref_krylov_solve(mat.h, 0 if which == "cg" else 1, _f64(b), tol, max_precond, None, hist,
+                                              hist_cap, C.byref(rep)))
+        return Report(bool(rep.converged), rep.outer_iterations, rep.precond_invocations, rep.final_true_residual,
+                      [], list(hist[:min(rep.n_history, hist_cap)]), [], rep.flag.decode(), rep.wall_seconds,
+                      rep.id.decode())
 
     def spec_canonical(self, spec):
         buf = C.create_string_buffer(512)

@@ -1,0 +1,43 @@
+"""fp16-F3R against the reference's fp64 competitor solvers (CG, BiCGStab; M =
+identity) on the device, BASELINE configs: outer/iteration counts and
+time-to-solution (the paper's comparison, on B200).
+
+    python tools/competitors.py [configs...]      (default: 1 2 3 4)
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2505_20719_b200 as f  # noqa: E402
+from paper_2505_20719_b200 import problems  # noqa: E402
+
+SPEC = "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > identity"
+TOL = 1e-10
+for cfg in [int(c) for c in sys.argv[1:]] or [1, 2, 3, 4]:
+    p = problems.problem(cfg)
+    reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
+    out = {"config": cfg, "n": p.n, "nnz": p.nnz}
+    s = f.build(f.parse_solver_spec(SPEC), reps, f.IdentityPrecond(p.n))
+    b = torch.from_numpy(p.b).cuda()
+    for _ in range(2):
+        s.reset(); s.run(b, f.RunOptions(tol=TOL))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s.reset(); r = s.run(b, f.RunOptions(tol=TOL), want_x=False).report
+    torch.cuda.synchronize()
+    out["f3r16"] = {"outer": r.outer_iterations, "res": r.final_true_residual, "s": time.perf_counter() - t0}
+    for name, solve in (("cg", f.cg_solve), ("bicgstab", f.bicgstab_solve)):
+        if name == "cg" and cfg in (3, 5):
+            continue  # non-symmetric
+        solve(reps, f.IdentityPrecond(p.n), p.b, f.ReferenceSolveOptions(tol=TOL))  # warm-up
+        t0 = time.perf_counter()
+        k = solve(reps, f.IdentityPrecond(p.n), p.b, f.ReferenceSolveOptions(tol=TOL))
+        out[name] = {"iterations": k.outer_iterations, "converged": k.converged, "flag": k.flag,
+                     "res": k.final_true_residual, "s": time.perf_counter() - t0}
+    print(json.dumps(out), flush=True)
