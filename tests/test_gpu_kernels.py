@@ -67,14 +67,16 @@ def test_spmv_both_column_streams(cuda, oracle, columns, monkeypatch):
 
 
 def test_spmv_long_rows_and_empty_rows(cuda, oracle):
-    """rows longer than a shared-memory tile and empty rows (CSR edge cases)."""
+    """rows longer than a shared-memory tile and empty rows (CSR edge cases), on
+    every column stream (u32, D16 and, for fp16, P16)"""
     import paper_2505_20719_b200 as f
     rng = np.random.default_rng(3)
-    n = 3000
+    n = 9000
     lens = rng.integers(0, 40, n)
     lens[5] = 0
-    lens[17] = 2999  # longer than every tile capacity
-    lens[18] = 9000 % n
+    lens[17] = 8999  # longer than every tile capacity (TNNZ 7168 / 6912 / 4096)
+    lens[18] = 5000  # longer than an fp64 tile only
+    lens[19] = 0
     rows, cols = [], []
     for i, L in enumerate(lens):
         c = np.sort(rng.choice(n, size=min(L, n), replace=False))
@@ -83,15 +85,21 @@ def test_spmv_long_rows_and_empty_rows(cuda, oracle):
     rp[1:] = np.cumsum([len(c) for c in cols])
     ci = np.concatenate(cols).astype(np.uint32)
     va = rng.uniform(-1, 1, ci.size)
-    reps = f.make_replicas(f.SparseCsr(n, rp, ci, va))
     a = (n, rp, ci)
-    for pa in PRECS:
-        vals = oracle.round_vec(pa, va)
-        for px, py in ((pa, pa), (0, 1), (2, 2)):
-            x = rand_vec(oracle, px, n, 11)
-            y = f.DenseVector(n, py)
-            f.spmv(reps.at(pa), f.DenseVector(x, px), y)
-            assert np.array_equal(y.numpy(), oracle.spmv(a, vals, pa, x, px, py)), (pa, px, py)
+    import os
+    for fmt in ("", "d16", "u32"):
+        os.environ["F3RG_COLUMNS"] = fmt
+        try:
+            reps = f.make_replicas(f.SparseCsr(n, rp, ci, va))
+        finally:
+            os.environ.pop("F3RG_COLUMNS")
+        for pa in PRECS:
+            vals = oracle.round_vec(pa, va)
+            for px, py in ((pa, pa), (0, 1), (2, 2)):
+                x = rand_vec(oracle, px, n, 11)
+                y = f.DenseVector(n, py)
+                f.spmv(reps.at(pa), f.DenseVector(x, px), y)
+                assert np.array_equal(y.numpy(), oracle.spmv(a, vals, pa, x, px, py)), (fmt, pa, px, py)
 
 
 def test_elementwise_bit_exact(cuda, oracle):
