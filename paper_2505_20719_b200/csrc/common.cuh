@@ -238,9 +238,12 @@ __device__ __forceinline__ void block_sum(T_<C> (&v)[NV], double* scratch) {
 // last returns true (and re-arms the counter for the next launch).
 __device__ __forceinline__ bool last_block(unsigned* counter) {
   __shared__ bool is_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
+    // only thread 0 published data for the last CTA (the block's partials), so
+    // only its stores need ordering before the count (a fence by every thread
+    // waits out all their outputs: measured as membar stalls in k_cgs)
+    __threadfence();
     const unsigned t = atomicAdd(counter, 1u);
     is_last = (t == gridDim.x - 1);
     if (is_last) *counter = 0u;
