@@ -329,15 +329,22 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, ui
 // NJ = min(j + 1, 8) is a kernel template parameter (one instantiation per
 // projection count): the small-NJ kernels then need few registers, run more CTAs
 // per SM and keep two rounds of 16-byte loads in flight per thread.
+// shared memory of the CGS body (declared by the calling kernel: one copy however
+// many cgs_body instantiations a kernel holds)
+struct CgsSmem {
+  double scratch[64];
+  double hs[128];
+  double tot[8];
+  double hc[kStageMax + 1], cs[kStageMax], sn[kStageMax], gj_tol[3];
+};
+
 template <int PW, int NJ>
-__global__ void __launch_bounds__(256, NJ <= 2 ? 4 : NJ <= 4 ? 3 : 2) k_cgs(void* V, uint64_t n, uint64_t ldv, int j, LevelState* L, int* dead,
-                                             Gate gate, int level, int outer, int use_tol, StepInfo* info, Sync sync,
-                                             const double* dots, int dots_G, Dist dist) {
-  pdl_wait();
-  __shared__ double scratch[64];
-  __shared__ double hs[128];
-  __shared__ double tot[8];
-  if (gate.closed()) return;
+__device__ __forceinline__ void cgs_body(void* V, uint64_t n, uint64_t ldv, int j, LevelState* L, int* dead,
+                                         int level, int outer, int use_tol, StepInfo* info, Sync sync,
+                                         const double* dots, int dots_G, Dist dist, CgsSmem& sm) {
+  double* scratch = sm.scratch;
+  double* hs = sm.hs;
+  double* tot = sm.tot;
   using A = Ar<PW>;
   const int m1 = L->m + 1;
   double* h = L->H + (size_t)j * m1;
@@ -452,7 +459,10 @@ __global__ void __launch_bounds__(256, NJ <= 2 ? 4 : NJ <= 4 ? 3 : 2) k_cgs(void
   // the previous rotations, g_j) in shared memory, overlapped with the partials
   // reduction; thread 0 then runs the serial recurrence out of shared memory
   // instead of a chain of dependent global loads
-  __shared__ double hc[kStageMax + 1], cs[kStageMax], sn[kStageMax], gj_tol[3];
+  double* hc = sm.hc;
+  double* cs = sm.cs;
+  double* sn = sm.sn;
+  double* gj_tol = sm.gj_tol;
   const bool staged = j < kStageMax;
   if (staged) {
     for (int i = threadIdx.x; i <= j; i += blockDim.x) hc[i] = __ldcg(h + i);
@@ -531,6 +541,17 @@ __global__ void __launch_bounds__(256, NJ <= 2 ? 4 : NJ <= 4 ? 3 : 2) k_cgs(void
     info->tol_hit = L->tol_hit;
   }
 }
+
+template <int PW, int NJ>
+__global__ void __launch_bounds__(256, NJ <= 2 ? 4 : NJ <= 4 ? 3 : 2) k_cgs(void* V, uint64_t n, uint64_t ldv, int j, LevelState* L, int* dead,
+                                             Gate gate, int level, int outer, int use_tol, StepInfo* info, Sync sync,
+                                             const double* dots, int dots_G, Dist dist) {
+  pdl_wait();
+  __shared__ CgsSmem sm;
+  if (gate.closed()) return;
+  cgs_body<PW, NJ>(V, n, ldv, j, L, dead, level, outer, use_tol, info, sync, dots, dots_G, dist, sm);
+}
+
 
 // ------------------------------------------------------------------------------
 // Back-substitution (in W) + x (+)= sum_l y_l z_l, sequential axpys per element
