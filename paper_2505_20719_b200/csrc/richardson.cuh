@@ -26,7 +26,10 @@ namespace f3rg {
 // gather chunk of the Richardson passes: with the P16 stream a chunk's values ride
 // in registers next to its gathers, and chunks of 16 spill in this kernel
 // (measured ~2 % slower than 8)
-constexpr int rich_chunk(int idx) { return idx == 2 ? 8 : 0; }
+#ifndef F3RG_RICH_CHUNK
+#define F3RG_RICH_CHUNK 9
+#endif
+constexpr int rich_chunk(int idx) { return idx == 2 ? F3RG_RICH_CHUNK : 0; }
 
 // Right-hand side of the call: v_i = demote(s * parent_v_i) (s optional). v is in
 // the ext layout (row-block partition): gathers index it by ext column, row-local

@@ -42,7 +42,7 @@
 #define F3RG_TNNZ16 7168
 #endif
 #ifndef F3RG_P16_CHUNK  // P16 rows keep the chunk's values in registers too
-#define F3RG_P16_CHUNK 16
+#define F3RG_P16_CHUNK 9
 #endif
 
 namespace f3rg {
@@ -128,6 +128,9 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   // latency round per CHUNK entries); groups of 8 are unpredicated, only the last
   // partial group is predicated
   constexpr int CHUNK = CH ? CH : IDX == 2 ? F3RG_P16_CHUNK : F3RG_CHUNK;
+  // groups of GS unpredicated loads (8, or the whole chunk when it is not a multiple
+  // of 8: a 27-point row is exactly 3 chunks of 9)
+  constexpr int GS = CHUNK % 8 == 0 ? 8 : CHUNK, NG = CHUNK / GS;
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < T.ntiles; t += G, ++it) {
     const int s = (int)(it % ST);
@@ -174,14 +177,14 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
           typename Gather::Raw xs[CHUNK];
           TA av[CHUNK];  // P16 values (unused otherwise)
 #pragma unroll
-          for (int b = 0; b < CHUNK / 8; ++b) {
-            if ((uint32_t)(8 * b + 8) <= cnt) {
+          for (int b = 0; b < NG; ++b) {
+            if ((uint32_t)(GS * b + GS) <= cnt) {
 #pragma unroll
-              for (int u = 0; u < 8; ++u) xs[8 * b + u] = g.load(fetch(q + 8 * b + u, av[8 * b + u]));
+              for (int u = 0; u < GS; ++u) xs[GS * b + u] = g.load(fetch(q + GS * b + u, av[GS * b + u]));
             } else {
 #pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if ((uint32_t)(8 * b + u) < cnt) xs[8 * b + u] = g.load(fetch(q + 8 * b + u, av[8 * b + u]));
+              for (int u = 0; u < GS; ++u)
+                if ((uint32_t)(GS * b + u) < cnt) xs[GS * b + u] = g.load(fetch(q + GS * b + u, av[GS * b + u]));
             }
           }
           auto aval = [&](int i) -> TA {
@@ -189,16 +192,16 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
             else return pv[q + i];
           };
 #pragma unroll
-          for (int b = 0; b < CHUNK / 8; ++b) {
-            if ((uint32_t)(8 * b + 8) <= cnt) {
+          for (int b = 0; b < NG; ++b) {
+            if ((uint32_t)(GS * b + GS) <= cnt) {
 #pragma unroll
-              for (int u = 0; u < 8; ++u)
-                acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(aval(8 * b + u)), g.value(xs[8 * b + u])));
+              for (int u = 0; u < GS; ++u)
+                acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(aval(GS * b + u)), g.value(xs[GS * b + u])));
             } else {
 #pragma unroll
-              for (int u = 0; u < 8; ++u)
-                if ((uint32_t)(8 * b + u) < cnt)
-                  acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(aval(8 * b + u)), g.value(xs[8 * b + u])));
+              for (int u = 0; u < GS; ++u)
+                if ((uint32_t)(GS * b + u) < cnt)
+                  acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(aval(GS * b + u)), g.value(xs[GS * b + u])));
             }
           }
         }
