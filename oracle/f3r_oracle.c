@@ -172,6 +172,240 @@ void or_scale(double alpha, double* x, int px, uint64_t n) {
   for (uint64_t i = 0; i < n; ++i) x[i] = mul_c(px, a, x[i]);
 }
 
+/* ------------------------------------------- block-Jacobi ILU(0) / IC(0) */
+/* Restates BlockJacobiIlu0 (reference src/ilu.cpp:38-263, include/f3r/ilu.hpp:44-84):
+ * contiguous row blocks (remainder to the leading blocks, :47-54), each diagonal
+ * block factorised at fp64 with zero fill on a working copy whose diagonal is
+ * scaled by alpha (:62-86); ILU in IKJ order (:88-106), IC on the lower pattern
+ * (:108-137); factors split and rounded to the apply precision (:140-183). */
+
+static double* vnew(uint64_t n) { return (double*)calloc(n ? n : 1, sizeof(double)); }
+
+struct or_ilu {
+  uint64_t n, nblocks;
+  int symmetric, prec;
+  uint32_t* br;                 /* nblocks + 1 row offsets */
+  uint32_t *lp, *li, *upp, *ui; /* lower / upper CSR (upper empty for IC) */
+  double *lv, *uv;              /* values, exactly representable at prec */
+};
+
+static int ilu_fail(char* err, size_t cap, const char* msg) {
+  if (err && cap) snprintf(err, cap, "%s", msg);
+  return 5;
+}
+
+static uint64_t ilu_block_of(const or_ilu* m, uint64_t row) {
+  uint64_t b = 0;
+  while (m->br[b + 1] <= row) ++b;
+  return b;
+}
+
+void or_ilu_free(or_ilu* m) {
+  if (!m) return;
+  free(m->br);
+  free(m->lp);
+  free(m->li);
+  free(m->upp);
+  free(m->ui);
+  free(m->lv);
+  free(m->uv);
+  free(m);
+}
+
+int or_ilu_factorize(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals, uint64_t nblocks,
+                     double alpha, int symmetric, int prec, or_ilu** out, char* err, size_t errcap) {
+  char msg[256];
+  *out = NULL;
+  if (nblocks == 0 || nblocks > n) return ilu_fail(err, errcap, "nblocks must be in [1, n]");
+  if (!(alpha > 0.0)) return ilu_fail(err, errcap, "alpha must be positive");
+  or_ilu* m = (or_ilu*)calloc(1, sizeof *m);
+  m->n = n;
+  m->nblocks = nblocks;
+  m->symmetric = symmetric;
+  m->prec = prec;
+  m->br = (uint32_t*)malloc((nblocks + 1) * sizeof(uint32_t));
+  m->br[0] = 0;
+  for (uint64_t b = 0; b < nblocks; ++b) m->br[b + 1] = m->br[b] + (uint32_t)(n / nblocks + (b < n % nblocks));
+
+  /* working rows: in-block entries (IC: j <= i only), diagonal scaled by alpha */
+  const uint64_t nnz = rp[n];
+  uint32_t* wp = (uint32_t*)calloc(n + 1, sizeof(uint32_t));
+  uint32_t* wi = (uint32_t*)malloc((nnz ? nnz : 1) * sizeof(uint32_t));
+  double* wv = (double*)malloc((nnz ? nnz : 1) * sizeof(double));
+  uint32_t* wd = (uint32_t*)calloc(n ? n : 1, sizeof(uint32_t));
+  uint64_t w = 0;
+  int rc = 0;
+  for (uint64_t b = 0; b < nblocks && !rc; ++b) {
+    const uint32_t lo = m->br[b], hi = m->br[b + 1];
+    for (uint32_t i = lo; i < hi; ++i) {
+      int diag = 0;
+      for (uint32_t k = rp[i]; k < rp[i + 1]; ++k) {
+        const uint32_t j = ci[k];
+        if (j < lo || j >= hi || (symmetric && j > i)) continue;
+        if (j == i) {
+          diag = 1;
+          wd[i] = (uint32_t)w;
+          wv[w] = vals[k] * alpha;
+        } else {
+          wv[w] = vals[k];
+        }
+        wi[w++] = j;
+      }
+      if (!diag) {
+        snprintf(msg, sizeof msg, "missing diagonal entry in block %llu, row %u", (unsigned long long)b, i);
+        rc = ilu_fail(err, errcap, msg);
+        break;
+      }
+      wp[i + 1] = (uint32_t)w;
+    }
+  }
+  if (!rc && !symmetric) {
+    /* ILU(0): row i eliminates with every earlier row of its pattern, in order */
+    int64_t* pos = (int64_t*)malloc((n ? n : 1) * sizeof(int64_t));
+    for (uint64_t i = 0; i < n; ++i) pos[i] = -1;
+    for (uint64_t b = 0; b < nblocks && !rc; ++b) {
+      for (uint32_t i = m->br[b]; i < m->br[b + 1]; ++i) {
+        for (uint32_t k = wp[i]; k < wp[i + 1]; ++k) pos[wi[k]] = k;
+        for (uint32_t k = wp[i]; k < wp[i + 1] && wi[k] < i; ++k) {
+          const uint32_t r = wi[k];
+          wv[k] = wv[k] / wv[wd[r]];
+          const double f = wv[k];
+          for (uint32_t q = wd[r] + 1; q < wp[r + 1]; ++q)
+            if (pos[wi[q]] >= 0) wv[pos[wi[q]]] = wv[pos[wi[q]]] - f * wv[q];
+        }
+        for (uint32_t k = wp[i]; k < wp[i + 1]; ++k) pos[wi[k]] = -1;
+        if (wv[wd[i]] == 0.0) {
+          snprintf(msg, sizeof msg, "zero pivot in block %llu, row %u", (unsigned long long)b, i);
+          rc = ilu_fail(err, errcap, msg);
+          break;
+        }
+      }
+    }
+    free(pos);
+  } else if (!rc) {
+    /* IC(0): l_ij = (a_ij - sum_{k<j} l_ik l_jk) / l_jj, l_ii = sqrt(a_ii - sum l_ik^2);
+     * the sums walk the two rows' common columns below j in ascending order */
+    for (uint64_t b = 0; b < nblocks && !rc; ++b) {
+      for (uint32_t i = m->br[b]; i < m->br[b + 1] && !rc; ++i) {
+        for (uint32_t k = wp[i]; k < wp[i + 1]; ++k) {
+          const uint32_t j = wi[k];
+          double s = wv[k];
+          uint32_t a = wp[i], c = wp[j];
+          while (a < wp[i + 1] && c < wp[j + 1] && wi[a] < j && wi[c] < j) {
+            if (wi[a] == wi[c]) s = s - wv[a++] * wv[c++];
+            else if (wi[a] < wi[c]) ++a;
+            else ++c;
+          }
+          if (j < i) {
+            wv[k] = s / wv[wd[j]];
+          } else if (s <= 0.0) {
+            snprintf(msg, sizeof msg, "non-positive pivot in block %llu, row %u", (unsigned long long)b, i);
+            rc = ilu_fail(err, errcap, msg);
+            break;
+          } else {
+            wv[k] = sqrt(s);
+          }
+        }
+      }
+    }
+  }
+  if (!rc) {
+    /* split: IC keeps the whole lower row (diagonal last), ILU the strict lower
+     * part and the upper part with its diagonal first */
+    m->lp = (uint32_t*)calloc(n + 1, sizeof(uint32_t));
+    m->upp = (uint32_t*)calloc(n + 1, sizeof(uint32_t));
+    m->li = (uint32_t*)malloc((w ? w : 1) * sizeof(uint32_t));
+    m->ui = (uint32_t*)malloc((w ? w : 1) * sizeof(uint32_t));
+    m->lv = (double*)malloc((w ? w : 1) * sizeof(double));
+    m->uv = (double*)malloc((w ? w : 1) * sizeof(double));
+    uint64_t nl = 0, nu = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      for (uint32_t k = wp[i]; k < wp[i + 1]; ++k) {
+        if (symmetric || wi[k] < i) {
+          m->li[nl] = wi[k];
+          m->lv[nl++] = wv[k];
+        } else {
+          m->ui[nu] = wi[k];
+          m->uv[nu++] = wv[k];
+        }
+      }
+      m->lp[i + 1] = (uint32_t)nl;
+      m->upp[i + 1] = (uint32_t)nu;
+    }
+    static const char* pname[3] = {"f16", "f32", "f64"};
+    for (uint64_t i = 0; i < n && !rc; ++i) {
+      const double d = symmetric ? m->lv[m->lp[i + 1] - 1] : m->uv[m->upp[i]];
+      const double cast = or_round(prec, d);
+      if (cast == 0.0 || !isfinite(cast)) {
+        snprintf(msg, sizeof msg, "casting factors to %s lost the diagonal of row %llu; block %llu", pname[prec],
+                 (unsigned long long)i, (unsigned long long)ilu_block_of(m, i));
+        rc = ilu_fail(err, errcap, msg);
+      }
+    }
+    for (uint64_t k = 0; k < nl; ++k) m->lv[k] = or_round(prec, m->lv[k]);
+    for (uint64_t k = 0; k < nu; ++k) m->uv[k] = or_round(prec, m->uv[k]);
+  }
+  free(wp);
+  free(wi);
+  free(wv);
+  free(wd);
+  if (rc) {
+    or_ilu_free(m);
+    return rc;
+  }
+  *out = m;
+  return 0;
+}
+
+uint64_t or_ilu_count(const or_ilu* m, int upper) { return upper ? m->upp[m->n] : m->lp[m->n]; }
+
+void or_ilu_export(const or_ilu* m, int upper, uint32_t* ptr, uint32_t* idx, double* vals) {
+  const uint32_t* p = upper ? m->upp : m->lp;
+  const uint64_t nz = p[m->n];
+  memcpy(ptr, p, (m->n + 1) * sizeof(uint32_t));
+  memcpy(idx, upper ? m->ui : m->li, nz * sizeof(uint32_t));
+  memcpy(vals, upper ? m->uv : m->lv, nz * sizeof(double));
+}
+
+/* BlockJacobiIlu0::apply (src/ilu.cpp:187-263): per block, at C = promote(prec,
+ * pr); every multiply and subtract rounds to C. IC's backward sweep scatters row
+ * i's x_i into the earlier rows (column-oriented, :237-244). */
+void or_ilu_apply(const or_ilu* m, const double* r, int pr, double* z, int pz) {
+  const int c = maxp(m->prec, pr);
+  double* t = vnew(m->n);
+  for (uint64_t b = 0; b < m->nblocks; ++b) {
+    const uint32_t lo = m->br[b], hi = m->br[b + 1];
+    if (!m->symmetric) {
+      for (uint32_t i = lo; i < hi; ++i) {
+        double acc = r[i];
+        for (uint32_t k = m->lp[i]; k < m->lp[i + 1]; ++k) acc = sub_c(c, acc, mul_c(c, m->lv[k], t[m->li[k]]));
+        t[i] = acc;
+      }
+      for (uint32_t i = hi; i-- > lo;) {
+        double acc = t[i];
+        for (uint32_t k = m->upp[i] + 1; k < m->upp[i + 1]; ++k)
+          acc = sub_c(c, acc, mul_c(c, m->uv[k], t[m->ui[k]]));
+        t[i] = div_c(c, acc, m->uv[m->upp[i]]);
+      }
+    } else {
+      for (uint32_t i = lo; i < hi; ++i) {
+        double acc = r[i];
+        const uint32_t dk = m->lp[i + 1] - 1;
+        for (uint32_t k = m->lp[i]; k < dk; ++k) acc = sub_c(c, acc, mul_c(c, m->lv[k], t[m->li[k]]));
+        t[i] = div_c(c, acc, m->lv[dk]);
+      }
+      for (uint32_t i = hi; i-- > lo;) {
+        const uint32_t dk = m->lp[i + 1] - 1;
+        const double xi = div_c(c, t[i], m->lv[dk]);
+        t[i] = xi;
+        for (uint32_t k = m->lp[i]; k < dk; ++k) t[m->li[k]] = sub_c(c, t[m->li[k]], mul_c(c, m->lv[k], xi));
+      }
+    }
+  }
+  for (uint64_t i = 0; i < m->n; ++i) z[i] = or_round(pz, t[i]);
+  free(t);
+}
+
 /* --------------------------------------------------------------- the solver */
 
 typedef struct {
@@ -187,9 +421,9 @@ typedef struct {
   /* Richardson state per level */
   double* omegas[16];
   uint64_t call_count[16], update_count[16], degenerate[16];
+  const or_ilu* M; /* primary preconditioner; NULL = IdentityPrecond */
 } ctx_t;
 
-static double* vnew(uint64_t n) { return (double*)calloc(n ? n : 1, sizeof(double)); }
 
 static void multiply(ctx_t* c, int d, const double* x, int px, double* y, int py) {
   or_spmv(c->n, c->rp, c->ci, c->vals[c->lv[d].pa], c->lv[d].pa, x, px, y, py);
@@ -200,9 +434,10 @@ static void inner_solve(ctx_t* c, int d, const double* rhs, int prhs, double* ou
 /* LevelOperator::precondition (src/nesting.cpp:53-64) of level d */
 static void precondition(ctx_t* c, int d, const double* v, int pv, double* z, int pz) {
   const int child = d + 1;
-  if (child >= c->D) { /* PrimarySolver: identity M (src/ilu.cpp:33-36) */
+  if (child >= c->D) { /* PrimarySolver (src/nesting.cpp:70-83): M applies itself */
     c->precond_invocations++;
-    or_copy(v, pv, z, pz, c->n);
+    if (c->M) or_ilu_apply(c->M, v, pv, z, pz);
+    else or_copy(v, pv, z, pz, c->n); /* IdentityPrecond (src/ilu.cpp:33-36) */
     return;
   }
   const int cp = c->lv[child].pv;
@@ -436,6 +671,15 @@ static void push_hist(or_report* rep, double* hist, uint64_t cap, double v) {
 int or_solve(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals64, const or_level* levels,
              int nlevels, const double* b, double tol, int max_outer_restarts, uint64_t max_outer_total,
              int reset_richardson, double* x_out, double* history, uint64_t hist_cap, or_report* rep) {
+  return or_solve_m(n, rp, ci, vals64, levels, nlevels, NULL, b, tol, max_outer_restarts, max_outer_total,
+                    reset_richardson, x_out, history, hist_cap, rep);
+}
+
+int or_solve_m(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals64, const or_level* levels,
+               int nlevels, const or_ilu* M, const double* b, double tol, int max_outer_restarts,
+               uint64_t max_outer_total, int reset_richardson, double* x_out, double* history, uint64_t hist_cap,
+               or_report* rep) {
+  if (M && M->n != n) return 2;
   if (nlevels < 1 || nlevels > 16) return 3;
   for (int d = 0; d < nlevels; ++d)
     if (levels[d].m < 1) return 3;
@@ -459,6 +703,7 @@ int or_solve(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* v
   c.vals[OR_P64] = vals64;
   c.lv = levels;
   c.D = nlevels;
+  c.M = M;
   for (int d = 0; d < nlevels; ++d) {
     c.omegas[d] = (double*)calloc((size_t)levels[d].m, sizeof(double));
     reset_rich(&c, d);
@@ -568,6 +813,12 @@ int or_solve(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* v
 
 void or_richardson_apply(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals_p, int p, int m,
                          uint64_t cycle_len, double* omegas, uint64_t* counters, const double* v, double* z) {
+  or_richardson_apply_m(n, rp, ci, vals_p, p, m, cycle_len, NULL, omegas, counters, v, z);
+}
+
+void or_richardson_apply_m(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals_p, int p, int m,
+                           uint64_t cycle_len, const or_ilu* M, double* omegas, uint64_t* counters, const double* v,
+                           double* z) {
   or_level lv = {1, m, p, p, cycle_len, 0, 0.0};
   ctx_t c;
   memset(&c, 0, sizeof c);
@@ -577,6 +828,7 @@ void or_richardson_apply(uint64_t n, const uint32_t* rp, const uint32_t* ci, con
   c.vals[p] = vals_p;
   c.lv = &lv;
   c.D = 1;
+  c.M = M;
   richardson(&c, 0, m, cycle_len, omegas, &counters[0], &counters[1], &counters[2], v, p, z, p);
 }
 
@@ -684,9 +936,10 @@ int or_parse_spec(const char* spec, or_level* levels, int cap) {
       }
       levels[nl++] = L;
     } else {
-      /* terminal: only identity is meaningful to this oracle */
+      /* terminal: identity, ilu0(...) or ic0(...); like the reference's, it only
+       * names M -- the caller passes the preconditioner itself */
       if (e) return -1;
-      if (!(end - s == 8 && !strncmp(s, "identity", 8))) return -1;
+      if (!(end - s == 8 && !strncmp(s, "identity", 8)) && strncmp(s, "ilu0", 4) && strncmp(s, "ic0", 3)) return -1;
     }
     if (!e) break;
     p = e + 1;

@@ -16,6 +16,7 @@
 #ifndef F3R_ORACLE_H
 #define F3R_ORACLE_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -42,8 +43,22 @@ void or_add_scaled(const double* x, int px, double alpha, const double* y, int p
 void or_copy(const double* x, int px, double* y, int py, uint64_t n);
 void or_scale(double alpha, double* x, int px, uint64_t n);
 
+/* Block-Jacobi ILU(0)/IC(0) primary preconditioner (reference src/ilu.cpp:38-263).
+ * or_ilu_factorize returns 0, or 5 (FactorizationError) with the reference's
+ * message in err. Factor values are exactly representable at `prec`. */
+typedef struct or_ilu or_ilu;
+int or_ilu_factorize(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals, uint64_t nblocks,
+                     double alpha, int symmetric, int prec, or_ilu** out, char* err, size_t errcap);
+void or_ilu_free(or_ilu* m);
+void or_ilu_apply(const or_ilu* m, const double* r, int pr, double* z, int pz);
+/* stored factors: upper = 0 the lower factor (IC: with its diagonal last), 1 the
+ * upper factor (ILU, diagonal first) */
+uint64_t or_ilu_count(const or_ilu* m, int upper);
+void or_ilu_export(const or_ilu* m, int upper, uint32_t* ptr, uint32_t* idx, double* vals);
+
 /* Nested solver (reference src/nesting.cpp, src/fgmres.cpp, src/richardson.cpp)
- * with the primary preconditioner M = identity. */
+ * with the primary preconditioner M = identity (or_solve) or a block-Jacobi
+ * ILU(0)/IC(0) (or_solve_m, M != NULL). */
 typedef struct {
   int kind; /* 0 = FGMRES, 1 = Richardson */
   int m;
@@ -78,6 +93,15 @@ int or_parse_spec(const char* spec, or_level* levels, int cap);
 int or_solve(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals64, const or_level* levels,
              int nlevels, const double* b, double tol, int max_outer_restarts, uint64_t max_outer_total,
              int reset_richardson, double* x_out, double* history, uint64_t hist_cap, or_report* rep);
+
+int or_solve_m(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals64, const or_level* levels,
+               int nlevels, const or_ilu* M, const double* b, double tol, int max_outer_restarts,
+               uint64_t max_outer_total, int reset_richardson, double* x_out, double* history, uint64_t hist_cap,
+               or_report* rep);
+
+void or_richardson_apply_m(uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* vals_p, int p, int m,
+                           uint64_t cycle_len, const or_ilu* M, double* omegas, uint64_t* counters, const double* v,
+                           double* z);
 
 /* One richardson_apply with (A_p, M = I) and a persistent state
  * (src/richardson.cpp:10-54). state layout: omegas[m], then counters

@@ -282,6 +282,55 @@ int ref_richardson_apply(void* h, void* s, int p, const double* v, double* z) {
   });
 }
 
+// ---- block-Jacobi ILU(0)/IC(0) (include/f3r/ilu.hpp:44-84) ------------------
+// Factorises the fp64 replica of h. On success *out is a BlockJacobiIlu0*.
+int ref_ilu_factorize(void* h, uint64_t nblocks, double alpha, int symmetric, int p, void** out) {
+  *out = nullptr;
+  return guarded([&] {
+    f3r::IluConfig cfg;
+    cfg.nblocks = nblocks;
+    cfg.alpha = alpha;
+    cfg.symmetric = symmetric != 0;
+    cfg.apply_precision = prec(p);
+    *out = new f3r::BlockJacobiIlu0(f3r::BlockJacobiIlu0::factorize(static_cast<RefMatrix*>(h)->reps.a64, cfg));
+  });
+}
+void ref_ilu_destroy(void* m) { delete static_cast<f3r::BlockJacobiIlu0*>(m); }
+// z = M r (Preconditioner::apply), r at pr, z at pz
+int ref_ilu_apply(void* m, const double* r, int pr, double* z, int pz) {
+  return guarded([&] {
+    const auto* M = static_cast<f3r::BlockJacobiIlu0*>(m);
+    const std::size_t n = M->rows();
+    DenseVector zv(n, prec(pz));
+    M->apply(make_vec(r, n, pr), zv);
+    read_vec(zv, z);
+  });
+}
+
+// richardson_apply on (A_p, M) -- the operator a RichardsonInner sees when its child
+// is the PrimarySolver (src/nesting.cpp:46-83: multiply = spmv, precondition = M)
+class MatrixPrecondOp final : public f3r::LinearOperator {
+ public:
+  MatrixPrecondOp(const f3r::SparseCsr& a, const f3r::Preconditioner& m) : a_(&a), m_(&m) {}
+  std::size_t size() const override { return a_->rows(); }
+  void multiply(const DenseVector& x, DenseVector& y) const override { f3r::spmv(*a_, x, y); }
+  void precondition(const DenseVector& v, DenseVector& z) override { m_->apply(v, z); }
+
+ private:
+  const f3r::SparseCsr* a_;
+  const f3r::Preconditioner* m_;
+};
+int ref_richardson_apply_m(void* h, void* s, int p, void* precond, const double* v, double* z) {
+  return guarded([&] {
+    const auto& a = static_cast<RefMatrix*>(h)->reps.at(prec(p));
+    MatrixPrecondOp op(a, *static_cast<f3r::BlockJacobiIlu0*>(precond));
+    const std::size_t n = a.rows();
+    DenseVector zv(n, prec(p));
+    f3r::richardson_apply(op, make_vec(v, n, p), *static_cast<f3r::RichardsonState*>(s), zv);
+    read_vec(zv, z);
+  });
+}
+
 // ---- one FGMRES cycle against (A_pa, M = identity), vectors at pw ------------
 int ref_fgmres_cycle(void* h, int pa, int pw, const double* b, double* x, int m, double rel_tol, int use_tol,
                      int x_is_zero, int* iterations, double* estimates /* m+1 */, int* flags /* happy, diverged, step */) {
@@ -320,14 +369,27 @@ struct RefReport {
 
 // Solves with `spec` (the reference grammar) and M = IdentityPrecond.
 // history: capacity hist_cap; x_out may be NULL.
+int ref_solve_m(void* h, const char* spec, void* precond, const double* b, double tol, int max_outer_restarts,
+                uint64_t max_outer_total, int reset_richardson, double* x_out, double* history, uint64_t hist_cap,
+                RefReport* rep);
 int ref_solve(void* h, const char* spec, const double* b, double tol, int max_outer_restarts,
               uint64_t max_outer_total, int reset_richardson, double* x_out, double* history, uint64_t hist_cap,
               RefReport* rep) {
+  return ref_solve_m(h, spec, nullptr, b, tol, max_outer_restarts, max_outer_total, reset_richardson, x_out, history,
+                     hist_cap, rep);
+}
+
+// Same with M = a BlockJacobiIlu0 from ref_ilu_factorize (nullptr: IdentityPrecond).
+int ref_solve_m(void* h, const char* spec, void* precond, const double* b, double tol, int max_outer_restarts,
+                uint64_t max_outer_total, int reset_richardson, double* x_out, double* history, uint64_t hist_cap,
+                RefReport* rep) {
   return guarded([&] {
     auto* m = static_cast<RefMatrix*>(h);
     const std::size_t n = m->reps.a64.rows();
     f3r::IdentityPrecond ident(n);
-    auto solver = f3r::build(f3r::parse_solver_spec(spec), m->reps, ident);
+    const f3r::Preconditioner& M =
+        precond ? static_cast<const f3r::Preconditioner&>(*static_cast<f3r::BlockJacobiIlu0*>(precond)) : ident;
+    auto solver = f3r::build(f3r::parse_solver_spec(spec), m->reps, M);
     f3r::RunOptions opts;
     opts.tol = tol;
     opts.max_outer_restarts = max_outer_restarts;

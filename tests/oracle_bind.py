@@ -98,6 +98,20 @@ class Oracle:
                                C.c_int, C.c_uint64, C.c_int, _dp, _dp, C.c_uint64, C.POINTER(_OrReport)]
         L.or_richardson_apply.argtypes = [C.c_uint64, _u32p, _u32p, _dp, C.c_int, C.c_int, C.c_uint64, _dp,
                                           C.POINTER(C.c_uint64), _dp, _dp]
+        L.or_ilu_factorize.restype = C.c_int
+        L.or_ilu_factorize.argtypes = [C.c_uint64, _u32p, _u32p, _dp, C.c_uint64, C.c_double, C.c_int, C.c_int,
+                                       C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+        L.or_ilu_free.argtypes = [C.c_void_p]
+        L.or_ilu_apply.argtypes = [C.c_void_p, _dp, C.c_int, _dp, C.c_int]
+        L.or_ilu_count.restype = C.c_uint64
+        L.or_ilu_count.argtypes = [C.c_void_p, C.c_int]
+        L.or_ilu_export.argtypes = [C.c_void_p, C.c_int, _u32p, _u32p, _dp]
+        L.or_solve_m.restype = C.c_int
+        L.or_solve_m.argtypes = [C.c_uint64, _u32p, _u32p, _dp, C.POINTER(_OrLevel), C.c_int, C.c_void_p, _dp,
+                                 C.c_double, C.c_int, C.c_uint64, C.c_int, _dp, _dp, C.c_uint64,
+                                 C.POINTER(_OrReport)]
+        L.or_richardson_apply_m.argtypes = [C.c_uint64, _u32p, _u32p, _dp, C.c_int, C.c_int, C.c_uint64,
+                                            C.c_void_p, _dp, C.POINTER(C.c_uint64), _dp, _dp]
         L.or_fgmres_cycle.restype = C.c_int
         L.or_fgmres_cycle.argtypes = [C.c_uint64, _u32p, _u32p, _dp, C.c_int, C.c_int, _dp, _dp, C.c_int,
                                       C.c_double, C.c_int, C.c_int, C.POINTER(C.c_int), _dp, C.POINTER(C.c_int)]
@@ -161,27 +175,41 @@ class Oracle:
             raise ValueError(f"oracle cannot parse spec {spec!r}")
         return levels, nl
 
+    def ilu(self, a, vals64, nblocks, alpha=1.0, symmetric=False, prec=P64):
+        """BlockJacobiIlu0::factorize (src/ilu.cpp:38-185) -> OracleIlu; raises
+        FactorizationFailed carrying the reference's message."""
+        n, rp, ci = a
+        h = C.c_void_p()
+        err = C.create_string_buffer(256)
+        rc = self.lib.or_ilu_factorize(n, _u32(rp), _u32(ci), _f64(vals64), nblocks, alpha, int(symmetric), prec,
+                                       C.byref(h), err, 256)
+        if rc:
+            raise FactorizationFailed(err.value.decode())
+        return OracleIlu(self, h, n)
+
     def solve(self, a, vals64, spec, b, tol=1e-10, max_outer_restarts=3, max_outer_total=300,
-              reset_richardson=False, hist_cap=4096) -> Report:
+              reset_richardson=False, hist_cap=4096, precond=None) -> Report:
         n, rp, ci = a
         levels, nl = self.parse_spec(spec)
         x = np.zeros(n)
         hist = np.zeros(hist_cap)
         rep = _OrReport()
-        rc = self.lib.or_solve(n, _u32(rp), _u32(ci), _f64(vals64), levels, nl, _f64(b), tol, max_outer_restarts,
-                               max_outer_total, int(reset_richardson), x, hist, hist_cap, C.byref(rep))
+        rc = self.lib.or_solve_m(n, _u32(rp), _u32(ci), _f64(vals64), levels, nl,
+                                 precond.h if precond is not None else None, _f64(b), tol, max_outer_restarts,
+                                 max_outer_total, int(reset_richardson), x, hist, hist_cap, C.byref(rep))
         if rc != 0:
             raise RuntimeError(f"oracle solve failed rc={rc}")
         return Report(bool(rep.converged), rep.outer_iterations, rep.precond_invocations, rep.final_true_residual,
                       list(rep.level_iterations[:rep.n_levels]), list(hist[:min(rep.n_history, hist_cap)]),
                       list(rep.omegas[:rep.n_omegas]), rep.flag.decode(), x=x)
 
-    def richardson_apply(self, a, vals_p, p, m, cycle, omegas, counters, v):
+    def richardson_apply(self, a, vals_p, p, m, cycle, omegas, counters, v, precond=None):
         n, rp, ci = a
         z = np.zeros(n)
         cnt = (C.c_uint64 * 3)(*counters)
         om = _f64(omegas).copy()
-        self.lib.or_richardson_apply(n, _u32(rp), _u32(ci), _f64(vals_p), p, m, cycle, om, cnt, _f64(v), z)
+        self.lib.or_richardson_apply_m(n, _u32(rp), _u32(ci), _f64(vals_p), p, m, cycle,
+                                       precond.h if precond is not None else None, om, cnt, _f64(v), z)
         return z, om, [cnt[0], cnt[1], cnt[2]]
 
     def fgmres_cycle(self, a, vals_pa, pa, pw, b, x, m, rel_tol=None, x_is_zero=True):
@@ -241,6 +269,13 @@ class Reference:
         L.ref_spec_canonical.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64]
         L.ref_krylov_solve.argtypes = [C.c_void_p, C.c_int, _dp, C.c_double, C.c_uint64, C.c_void_p, _dp,
                                        C.c_uint64, C.POINTER(_RefReport)]
+        L.ref_solve_m.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p, _dp, C.c_double, C.c_int, C.c_uint64,
+                                  C.c_int, C.c_void_p, _dp, C.c_uint64, C.POINTER(_RefReport)]
+        L.ref_ilu_factorize.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_int, C.c_int,
+                                        C.POINTER(C.c_void_p)]
+        L.ref_ilu_destroy.argtypes = [C.c_void_p]
+        L.ref_ilu_apply.argtypes = [C.c_void_p, _dp, C.c_int, _dp, C.c_int]
+        L.ref_richardson_apply_m.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, _dp, _dp]
         L.ref_set_threads.argtypes = [C.c_int]
         L.ref_max_threads.restype = C.c_int
 
@@ -348,14 +383,23 @@ class Reference:
                                               rel_tol is not None, int(x_is_zero), C.byref(it), est, flags))
         return x, it.value, est[:it.value + 1], (flags[0], flags[1], flags[2])
 
+    def ilu(self, mat, nblocks, alpha=1.0, symmetric=False, prec=P64):
+        """the reference's BlockJacobiIlu0::factorize on mat's fp64 values"""
+        h = C.c_void_p()
+        rc = self.lib.ref_ilu_factorize(mat.h, nblocks, alpha, int(symmetric), prec, C.byref(h))
+        if rc == 5:
+            raise FactorizationFailed(self.lib.ref_last_error().decode())
+        self._check(rc)
+        return _RefIlu(self, h, mat.n)
+
     def solve(self, mat, spec, b, tol=1e-10, max_outer_restarts=3, max_outer_total=300, reset_richardson=False,
-              want_x=True, hist_cap=4096) -> Report:
+              want_x=True, hist_cap=4096, precond=None) -> Report:
         hist = np.zeros(hist_cap)
         rep = _RefReport()
         x = np.zeros(mat.n) if want_x else None
-        self._check(self.lib.ref_solve(mat.h, spec.encode(), _f64(b), tol, max_outer_restarts, max_outer_total,
-                                       int(reset_richardson), x.ctypes.data if x is not None else None, hist,
-                                       hist_cap, C.byref(rep)))
+        self._check(self.lib.ref_solve_m(mat.h, spec.encode(), precond.h if precond is not None else None, _f64(b),
+                                         tol, max_outer_restarts, max_outer_total, int(reset_richardson),
+                                         x.ctypes.data if x is not None else None, hist, hist_cap, C.byref(rep)))
         return Report(bool(rep.converged), rep.outer_iterations, rep.precond_invocations, rep.final_true_residual,
                       list(rep.level_iterations[:rep.n_levels]), list(hist[:min(rep.n_history, hist_cap)]),
                       list(rep.omegas[:rep.n_omegas]), rep.flag.decode(), rep.wall_seconds, rep.id.decode(), x=x)
@@ -386,9 +430,12 @@ class _RefRichardson:
         if getattr(self, "h", None):
             self.ref.lib.ref_richardson_destroy(self.h)
 
-    def apply(self, mat, p, v):
+    def apply(self, mat, p, v, precond=None):
         z = np.zeros(mat.n)
-        self.ref._check(self.ref.lib.ref_richardson_apply(mat.h, self.h, p, _f64(v), z))
+        if precond is None:
+            self.ref._check(self.ref.lib.ref_richardson_apply(mat.h, self.h, p, _f64(v), z))
+        else:
+            self.ref._check(self.ref.lib.ref_richardson_apply_m(mat.h, self.h, p, precond.h, _f64(v), z))
         return z
 
     def state(self):
@@ -402,6 +449,51 @@ class _RefRichardson:
         ln = C.c_uint64()
         self.ref.lib.ref_richardson_log(self.h, out, 4096, C.byref(ln))
         return out[:ln.value]
+
+
+class FactorizationFailed(RuntimeError):
+    """f3r::FactorizationError raised by a checker's factorize"""
+
+
+class OracleIlu:
+    """A block-Jacobi ILU(0)/IC(0) factorised by the C oracle."""
+
+    def __init__(self, oracle, h, n):
+        self.o, self.h, self.n = oracle, h, n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o.lib.or_ilu_free(self.h)
+            self.h = None
+
+    def apply(self, r, pr, pz):
+        z = np.zeros(self.n)
+        self.o.lib.or_ilu_apply(self.h, _f64(r), pr, z, pz)
+        return z
+
+    def factors(self, upper):
+        """(ptr, idx, vals) of the stored lower (upper=0) or upper (1) factor"""
+        nz = self.o.lib.or_ilu_count(self.h, int(upper))
+        ptr = np.zeros(self.n + 1, np.uint32)
+        idx = np.zeros(max(nz, 1), np.uint32)
+        vals = np.zeros(max(nz, 1))
+        self.o.lib.or_ilu_export(self.h, int(upper), ptr, idx, vals)
+        return ptr, idx[:nz], vals[:nz]
+
+
+class _RefIlu:
+    def __init__(self, ref, h, n):
+        self.ref, self.h, self.n = ref, h, n
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_ilu_destroy(self.h)
+            self.h = None
+
+    def apply(self, r, pr, pz):
+        z = np.zeros(self.n)
+        self.ref._check(self.ref.lib.ref_ilu_apply(self.h, _f64(r), pr, z, pz))
+        return z
 
 
 def reference_available() -> bool:
