@@ -97,10 +97,48 @@ int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host);
  *      src/solver_spec.cpp:147-212) */
 int f3rg_spec_canonical(const char* spec, char* out, size_t cap);
 
+/* ---- primary preconditioner M (replaces IdentityPrecond and
+ *      BlockJacobiIlu0::factorize / apply, include/f3r/ilu.hpp:25-84,
+ *      src/ilu.cpp:33-263). The factorisation runs on the host at fp64 exactly as
+ *      the reference's; the triangular sweeps of apply run on the device, bit-exact
+ *      (level-scheduled, sync-free). Errors: F3RG_EFACTORIZATION with the
+ *      reference's message (missing diagonal, zero / non-positive pivot, a pivot
+ *      lost in the cast to the apply precision, nblocks / alpha out of range). */
+typedef struct f3rg_precond f3rg_precond;
+/* reference IluConfig, include/f3r/ilu.hpp:44-49 */
+typedef struct {
+  uint64_t nblocks;
+  double alpha;
+  int32_t symmetric;       /* 1: IC(0), 0: ILU(0) */
+  int32_t apply_precision; /* F3RG_P16 / _P32 / _P64 */
+} f3rg_ilu_config;
+int f3rg_ilu_factorize(f3rg_precond** out, const f3rg_csr* a64, const f3rg_ilu_config* cfg);
+int f3rg_precond_identity(f3rg_precond** out, uint64_t n);
+void f3rg_precond_destroy(f3rg_precond* m);
+uint64_t f3rg_precond_rows(const f3rg_precond* m);
+/* config (nblocks 0 = identity), sweep depths levels[2] (forward, backward) and
+ * block_ranges (nblocks + 1 row offsets, up to cap); any output may be NULL */
+int f3rg_precond_info(const f3rg_precond* m, f3rg_ilu_config* cfg, uint32_t* levels, uint32_t* block_ranges,
+                      uint64_t cap);
+/* Preconditioner::apply: z = M r; device vectors r (prec_r) and z (prec_z); computes
+ * at promote(apply_precision, prec_r) like the reference */
+int f3rg_precond_apply(const f3rg_precond* m, const void* r, int prec_r, void* z, int prec_z, uintptr_t stream);
+/* the host factorisation alone (no device work): stored factors as the reference
+ * keeps them -- lower (IC: diagonal last in each row) and upper (ILU: diagonal
+ * first). Call with NULL arrays for the sizes; lp / up have n + 1 entries. */
+int f3rg_ilu_factorize_host(const f3rg_csr* a64, const f3rg_ilu_config* cfg, uint64_t* nnz_lower,
+                            uint64_t* nnz_upper, uint32_t* lp, uint32_t* li, double* lv, uint32_t* up, uint32_t* ui,
+                            double* uv);
+
 /* ---- composed solver (replaces build(spec, replicas, M) + ComposedSolver::run,
- *      src/nesting.cpp:176-352,354-357). precond_kind must be IDENTITY on this
- *      build (the spec's terminal, like the reference's, only names it). */
+ *      src/nesting.cpp:176-352,354-357).
+ *      f3rg_solver_create_m: with a preconditioner from f3rg_ilu_factorize /
+ *      f3rg_precond_identity (shared: it may be destroyed before the solver).
+ *      f3rg_solver_create: IDENTITY, or ILU0/IC0 factorised here from the spec
+ *      terminal's parameters with the reference bench's defaults (blocks 4,
+ *      alpha 1, f64; src/bench.cpp:150-177). */
 int f3rg_solver_create(f3rg_solver** out, const f3rg_matrix* a, const char* spec, int precond_kind);
+int f3rg_solver_create_m(f3rg_solver** out, const f3rg_matrix* a, const char* spec, const f3rg_precond* m);
 void f3rg_solver_destroy(f3rg_solver* s);
 const char* f3rg_solver_id(const f3rg_solver* s);
 /* b, x: HOST fp64 arrays of length n (x may be NULL); copies happen inside */
@@ -141,7 +179,8 @@ int f3rg_scale(double alpha, void* x, int prec_x, uint64_t n, uintptr_t stream);
 int f3rg_fill(void* x, int prec_x, uint64_t n, double value, uintptr_t stream);             /* fill :77 */
 
 /* ---- Richardson with persistent state (richardson_apply + RichardsonState,
- *      src/richardson.cpp:10-54, include/f3r/richardson.hpp:26-46), M = identity */
+ *      src/richardson.cpp:10-54, include/f3r/richardson.hpp:26-46); M = identity
+ *      unless f3rg_richardson_set_precond names one */
 typedef struct f3rg_richardson f3rg_richardson;
 int f3rg_richardson_create(f3rg_richardson** out, const f3rg_matrix* a, int prec, int m, uint64_t cycle);
 void f3rg_richardson_destroy(f3rg_richardson* r);
@@ -150,6 +189,9 @@ int f3rg_richardson_set_omegas(f3rg_richardson* r, const double* omegas_host);
 int f3rg_richardson_state(f3rg_richardson* r, double* omegas_host, uint64_t* counters_host);
 /* v, z: device vectors at the Richardson precision */
 int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t stream);
+/* op.precondition = M for the following applies (NULL: identity again); the
+ * RichardsonInner-over-PrimarySolver operator of src/nesting.cpp:46-83 */
+int f3rg_richardson_set_precond(f3rg_richardson* r, const f3rg_precond* m);
 
 /* ---- the reference's fp64 competitor solvers (src/cg.cpp:22-171: cg_solve,
  *      bicgstab_solve) with M = identity, on the device. which: 0 = CG, 1 = BiCGStab.

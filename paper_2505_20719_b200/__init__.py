@@ -74,6 +74,11 @@ class _Csr(C.Structure):
     _fields_ = [("n", C.c_uint64), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
 
 
+class _IluCfg(C.Structure):
+    _fields_ = [("nblocks", C.c_uint64), ("alpha", C.c_double), ("symmetric", C.c_int32),
+                ("apply_precision", C.c_int32)]
+
+
 class _RunOpts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_outer_restarts", C.c_int32), ("max_outer_total", C.c_uint64),
                 ("reset_richardson_on_restart", C.c_int32)]
@@ -141,6 +146,18 @@ def lib():
     L.f3rg_richardson_set_omegas.argtypes = [vp, vp]
     L.f3rg_richardson_state.argtypes = [vp, vp, vp]
     L.f3rg_richardson_apply.argtypes = [vp, vp, vp, C.c_size_t]
+    L.f3rg_richardson_set_precond.argtypes = [vp, vp]
+    # primary preconditioner (ilu.hpp)
+    L.f3rg_ilu_factorize.argtypes = [C.POINTER(vp), C.POINTER(_Csr), C.POINTER(_IluCfg)]
+    L.f3rg_precond_identity.argtypes = [C.POINTER(vp), u64]
+    L.f3rg_precond_destroy.argtypes = [vp]
+    L.f3rg_precond_rows.restype = u64
+    L.f3rg_precond_rows.argtypes = [vp]
+    L.f3rg_precond_info.argtypes = [vp, C.POINTER(_IluCfg), vp, vp, u64]
+    L.f3rg_precond_apply.argtypes = [vp, vp, i32, vp, i32, C.c_size_t]
+    L.f3rg_ilu_factorize_host.argtypes = [C.POINTER(_Csr), C.POINTER(_IluCfg), C.POINTER(u64), C.POINTER(u64), vp, vp,
+                                          vp, vp, vp, vp]
+    L.f3rg_solver_create_m.argtypes = [C.POINTER(vp), vp, C.c_char_p, vp]
     _lib = L
     return L
 
@@ -369,16 +386,103 @@ def spmv(a: ReplicaView, x: DenseVector, y: DenseVector) -> None:
 
 
 # ------------------------------------------------------------ preconditioner (ilu.hpp)
-class IdentityPrecond:
-    """reference IdentityPrecond (include/f3r/ilu.hpp:34-42); the only primary
-    preconditioner of this build (ILU(0)/IC(0) is SURVEY.md §8(f)-1)."""
+class Preconditioner:
+    """reference Preconditioner (include/f3r/ilu.hpp:25-32): z = M r on the device."""
+    kind = 2
+    h = None
+
+    def rows(self) -> int:
+        return self.n
+
+    def apply(self, r: DenseVector, z: DenseVector) -> None:
+        """z ~= A^{-1} r at compute_precision(factors, r), stored at z's precision."""
+        if r.size() != self.n or z.size() != self.n:
+            raise DimensionError("preconditioner apply: size mismatch")
+        _check(lib().f3rg_precond_apply(self._handle(), r.ptr(), r.precision(), z.ptr(), z.precision(), _stream()))
+
+    def _handle(self):
+        if self.h is None:
+            self.h = C.c_void_p()
+            _check(lib().f3rg_precond_identity(C.byref(self.h), self.n))
+        return self.h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.f3rg_precond_destroy(self.h)
+            self.h = None
+
+
+class IdentityPrecond(Preconditioner):
+    """reference IdentityPrecond (include/f3r/ilu.hpp:34-42): apply = copy_into."""
     kind = 2
 
     def __init__(self, n: int):
         self.n = int(n)
 
-    def rows(self) -> int:
-        return self.n
+
+@dataclass
+class IluConfig:
+    """reference IluConfig (include/f3r/ilu.hpp:44-49)"""
+    nblocks: int = 1
+    alpha: float = 1.0
+    symmetric: bool = False
+    apply_precision: Precision = Precision.P64
+
+    def _c(self):
+        return _IluCfg(int(self.nblocks), float(self.alpha), int(bool(self.symmetric)), int(self.apply_precision))
+
+
+class BlockJacobiIlu0(Preconditioner):
+    """reference BlockJacobiIlu0 (include/f3r/ilu.hpp:51-84): block-Jacobi ILU(0) /
+    IC(0), factorised on the host at fp64 (src/ilu.cpp:38-185); apply runs the two
+    triangular sweeps on the device, bit-exact with the reference's sequential
+    ones (src/ilu.cpp:187-263)."""
+
+    def __init__(self, h, n: int, cfg: IluConfig):
+        self.h, self.n, self._cfg = h, int(n), cfg
+        self.kind = 1 if cfg.symmetric else 0
+
+    @staticmethod
+    def factorize(a: SparseCsr, cfg: IluConfig) -> "BlockJacobiIlu0":
+        """Raises FactorizationError naming the block and row, as the reference."""
+        h = C.c_void_p()
+        csr = _Csr(a.n, a.row_ptr.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data)
+        _check(lib().f3rg_ilu_factorize(C.byref(h), C.byref(csr), C.byref(cfg._c())))
+        return BlockJacobiIlu0(h, a.n, cfg)
+
+    def config(self) -> IluConfig:
+        return self._cfg
+
+    def _info(self):
+        cfg = _IluCfg()
+        lev = np.zeros(2, dtype=np.uint32)
+        br = np.zeros(int(self._cfg.nblocks) + 1, dtype=np.uint32)
+        _check(lib().f3rg_precond_info(self.h, C.byref(cfg), lev.ctypes.data, br.ctypes.data, br.size))
+        return lev, br
+
+    def block_ranges(self) -> list:
+        return [int(v) for v in self._info()[1]]
+
+    def sweep_levels(self) -> tuple:
+        """dependency depth of the forward and backward sweeps (the device critical path)"""
+        lev = self._info()[0]
+        return int(lev[0]), int(lev[1])
+
+
+def ilu_factorize_host(a: SparseCsr, cfg: IluConfig):
+    """The product's host factorisation alone (no GPU): ((lp, li, lv), (up, ui, uv)),
+    the stored factors as the reference keeps them."""
+    csr = _Csr(a.n, a.row_ptr.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data)
+    nl, nu = C.c_uint64(), C.c_uint64()
+    L = lib()
+    _check(L.f3rg_ilu_factorize_host(C.byref(csr), C.byref(cfg._c()), C.byref(nl), C.byref(nu), None, None, None,
+                                     None, None, None))
+    lp, up = np.zeros(a.n + 1, np.uint32), np.zeros(a.n + 1, np.uint32)
+    li, ui = np.zeros(max(1, nl.value), np.uint32), np.zeros(max(1, nu.value), np.uint32)
+    lv, uv = np.zeros(max(1, nl.value)), np.zeros(max(1, nu.value))
+    _check(L.f3rg_ilu_factorize_host(C.byref(csr), C.byref(cfg._c()), None, None, lp.ctypes.data, li.ctypes.data,
+                                     lv.ctypes.data, up.ctypes.data, ui.ctypes.data, uv.ctypes.data))
+    return (lp, li[:nl.value], lv[:nl.value]), (up, ui[:nu.value], uv[:nu.value])
 
 
 # ---------------------------------------------------------------- spec (solver_spec.hpp)
@@ -473,13 +577,13 @@ class ComposedSolver:
     """reference ComposedSolver (include/f3r/nesting.hpp:55-77): the whole nest runs
     on the GPU; one C-ABI call per solve."""
 
-    def __init__(self, spec, a: PrecisionReplicas, m: IdentityPrecond):
+    def __init__(self, spec, a: PrecisionReplicas, m: Preconditioner):
         if m.rows() != a.rows():
             raise DimensionError("preconditioner size does not match the matrix")
         text = spec.text if isinstance(spec, SolverSpec) else str(spec)
         self.h = C.c_void_p()
-        self._a = a
-        _check(lib().f3rg_solver_create(C.byref(self.h), a.dev.h, text.encode(), int(m.kind)))
+        self._a, self._m = a, m
+        _check(lib().f3rg_solver_create_m(C.byref(self.h), a.dev.h, text.encode(), m._handle()))
         self.n = a.rows()
 
     def __del__(self):
@@ -555,11 +659,11 @@ class ComposedSolver:
         return out
 
 
-def build(spec, a: PrecisionReplicas, m: IdentityPrecond) -> ComposedSolver:
+def build(spec, a: PrecisionReplicas, m: Preconditioner) -> ComposedSolver:
     return ComposedSolver(spec, a, m)
 
 
-def build_f3r(cfg: F3rConfig, a: PrecisionReplicas, m: IdentityPrecond) -> ComposedSolver:
+def build_f3r(cfg: F3rConfig, a: PrecisionReplicas, m: Preconditioner) -> ComposedSolver:
     return ComposedSolver(f3r_spec(cfg), a, m)
 
 
@@ -646,8 +750,13 @@ class RichardsonState:
         return self._state()[1][2]
 
 
-def richardson_apply(state: RichardsonState, v: DenseVector, z: DenseVector) -> None:
-    """reference richardson_apply (src/richardson.cpp:10-54) with M = identity."""
+def richardson_apply(state: RichardsonState, v: DenseVector, z: DenseVector, m: Preconditioner = None) -> None:
+    """reference richardson_apply (src/richardson.cpp:10-54) on the operator
+    (A, M): M = identity by default, else the given preconditioner."""
+    want = m.h if (m is not None and not isinstance(m, IdentityPrecond)) else None
+    if getattr(state, "_m", None) is not want:
+        _check(lib().f3rg_richardson_set_precond(state.h, want))
+        state._m = want
     if v.precision() != state.a.p or z.precision() != state.a.p:
         raise DimensionError("richardson: vectors must be at the state's precision")
     if v.size() != state.a.rows() or z.size() != state.a.rows():
@@ -659,7 +768,8 @@ __all__ = [
     "F3rError", "ParseError", "DimensionError", "FactorizationError", "SolverError", "UnsupportedError",
     "CudaError", "Precision", "compute_precision", "precision_name", "DenseVector", "fill", "copy_into",
     "converted", "scale_in_place", "axpy", "add_scaled", "dot", "dot_at_least", "norm2", "SparseCsr",
-    "PrecisionReplicas", "make_replicas", "spmv", "IdentityPrecond", "SolverSpec", "parse_solver_spec",
+    "PrecisionReplicas", "make_replicas", "spmv", "Preconditioner", "IdentityPrecond", "IluConfig",
+    "BlockJacobiIlu0", "ilu_factorize_host", "SolverSpec", "parse_solver_spec",
     "canonical_spec", "F3rMode", "F3rConfig", "f3r_spec", "RunOptions", "ConvergenceReport", "RunResult",
     "ComposedSolver", "build", "build_f3r", "RichardsonState", "richardson_apply", "lib",
 ]

@@ -27,7 +27,13 @@ struct f3rg_solver {
 struct f3rg_richardson {
   std::shared_ptr<DeviceMatrix> a;
   int prec = 0, m = 1;
-  DevBuf state, omegas, wused, wupd, calls, R, Za, Zb, dead, cnt, partials, counter, bar;
+  DevBuf state, omegas, wused, wupd, calls, R, Za, Zb, P, dead, cnt, partials, counter, bar;
+  std::shared_ptr<const DevicePrecond> M;  // null: identity
+  std::unique_ptr<SweepWork> work;
+};
+
+struct f3rg_precond {
+  std::shared_ptr<DevicePrecond> p;
 };
 
 namespace {
@@ -144,11 +150,129 @@ int f3rg_spec_canonical(const char* spec, char* out, size_t cap) {
   });
 }
 
+// ---- primary preconditioner (include/f3r/ilu.hpp) ------------------------------------
+namespace {
+IluConfig to_cfg(const f3rg_ilu_config* c) {
+  if (!c) throw Error(ERR_DIMENSION, "null ilu config");
+  check_prec(c->apply_precision);
+  IluConfig k;
+  k.nblocks = c->nblocks;
+  k.alpha = c->alpha;
+  k.symmetric = c->symmetric != 0;
+  k.prec = c->apply_precision;
+  return k;
+}
+
+// the fp64 CSR of a device matrix, back in host memory (setup only)
+void download(const DeviceMatrix& m, std::vector<uint32_t>& rp, std::vector<uint32_t>& ci, std::vector<double>& v) {
+  const CsrDev c = m.csr();
+  rp.resize(m.rows() + 1);
+  ci.resize(m.nnz());
+  v.resize(m.nnz());
+  F3RG_CUDA(cudaDeviceSynchronize());
+  F3RG_CUDA(cudaMemcpy(rp.data(), c.rp, rp.size() * 4, cudaMemcpyDeviceToHost));
+  if (m.nnz()) {
+    F3RG_CUDA(cudaMemcpy(ci.data(), c.ci, ci.size() * 4, cudaMemcpyDeviceToHost));
+    F3RG_CUDA(cudaMemcpy(v.data(), c.val[2], v.size() * 8, cudaMemcpyDeviceToHost));
+  }
+}
+}  // namespace
+
+int f3rg_ilu_factorize(f3rg_precond** out, const f3rg_csr* a, const f3rg_ilu_config* cfg) {
+  return guarded([&] {
+    if (!out || !a) throw Error(ERR_DIMENSION, "null argument");
+    auto h = std::make_unique<f3rg_precond>();
+    h->p = std::make_shared<DevicePrecond>(a->n, a->row_ptr, a->col_idx, a->values, to_cfg(cfg));
+    *out = h.release();
+  });
+}
+
+int f3rg_precond_identity(f3rg_precond** out, uint64_t n) {
+  return guarded([&] {
+    if (!out) throw Error(ERR_DIMENSION, "null argument");
+    auto h = std::make_unique<f3rg_precond>();
+    h->p = std::make_shared<DevicePrecond>(n);
+    *out = h.release();
+  });
+}
+
+void f3rg_precond_destroy(f3rg_precond* m) { delete m; }
+uint64_t f3rg_precond_rows(const f3rg_precond* m) { return m ? m->p->rows() : 0; }
+
+int f3rg_precond_info(const f3rg_precond* m, f3rg_ilu_config* cfg, uint32_t* levels, uint32_t* ranges,
+                      uint64_t cap) {
+  return guarded([&] {
+    if (!m) throw Error(ERR_DIMENSION, "null argument");
+    const DevicePrecond& p = *m->p;
+    if (cfg) {
+      cfg->nblocks = p.identity() ? 0 : p.config().nblocks;
+      cfg->alpha = p.config().alpha;
+      cfg->symmetric = p.config().symmetric;
+      cfg->apply_precision = p.config().prec;
+    }
+    if (levels) levels[0] = p.nlevels(0), levels[1] = p.nlevels(1);
+    const auto& br = p.block_ranges();
+    for (uint64_t i = 0; ranges && i < br.size() && i < cap; ++i) ranges[i] = br[i];
+  });
+}
+
+int f3rg_precond_apply(const f3rg_precond* m, const void* r, int pr, void* z, int pz, uintptr_t stream) {
+  return guarded([&] {
+    if (!m) throw Error(ERR_DIMENSION, "null argument");
+    check_prec(pr), check_prec(pz);
+    m->p->apply(r, pr, z, pz, as_stream(stream));
+  });
+}
+
+int f3rg_ilu_factorize_host(const f3rg_csr* a, const f3rg_ilu_config* cfg, uint64_t* nnz_lower, uint64_t* nnz_upper,
+                            uint32_t* lp, uint32_t* li, double* lv, uint32_t* up, uint32_t* ui, double* uv) {
+  return guarded([&] {
+    if (!a) throw Error(ERR_DIMENSION, "null argument");
+    validate_csr(a->n, a->row_ptr, a->col_idx);
+    const HostFactors f = factorize_host(a->n, a->row_ptr, a->col_idx, a->values, to_cfg(cfg));
+    if (nnz_lower) *nnz_lower = f.li.size();
+    if (nnz_upper) *nnz_upper = f.ui.size();
+    if (lp) std::memcpy(lp, f.lp.data(), f.lp.size() * 4);
+    if (li) std::memcpy(li, f.li.data(), f.li.size() * 4);
+    if (lv) std::memcpy(lv, f.lv.data(), f.lv.size() * 8);
+    if (up) std::memcpy(up, f.up.data(), f.up.size() * 4);
+    if (ui) std::memcpy(ui, f.ui.data(), f.ui.size() * 4);
+    if (uv) std::memcpy(uv, f.uv.data(), f.uv.size() * 8);
+  });
+}
+
+int f3rg_solver_create_m(f3rg_solver** out, const f3rg_matrix* a, const char* spec, const f3rg_precond* m) {
+  return guarded([&] {
+    if (!out || !a || !spec || !m) throw Error(ERR_DIMENSION, "null argument");
+    auto h = std::make_unique<f3rg_solver>();
+    const int kind = m->p->identity() ? PK_IDENTITY : m->p->config().symmetric ? PK_IC0 : PK_ILU0;
+    h->s = std::make_unique<Solver>(parse_spec(spec), a->m, kind, nullptr, m->p);
+    *out = h.release();
+  });
+}
+
 int f3rg_solver_create(f3rg_solver** out, const f3rg_matrix* a, const char* spec, int precond_kind) {
   return guarded([&] {
     if (!out || !a || !spec) throw Error(ERR_DIMENSION, "null argument");
     auto h = std::make_unique<f3rg_solver>();
-    h->s = std::make_unique<Solver>(parse_spec(spec), a->m, precond_kind);
+    const Spec sp = parse_spec(spec);
+    std::shared_ptr<const DevicePrecond> M;
+    if (precond_kind == PK_ILU0 || precond_kind == PK_IC0) {
+      // factorise from the spec terminal with the reference bench's defaults
+      // (blocks 4, alpha 1, fp64 apply; src/bench.cpp:160-177, include/f3r/bench.hpp:31-34)
+      IluConfig cfg;
+      cfg.symmetric = precond_kind == PK_IC0;
+      cfg.nblocks = sp.has_precond && sp.precond.has_blocks ? sp.precond.blocks : 4;
+      cfg.alpha = sp.has_precond && sp.precond.has_alpha ? sp.precond.alpha : 1.0;
+      cfg.prec = sp.has_precond && sp.precond.has_prec ? sp.precond.prec : 2;
+      std::vector<uint32_t> rp, ci;
+      std::vector<double> v;
+      download(*a->m, rp, ci, v);
+      M = std::make_shared<DevicePrecond>(a->m->rows(), rp.data(), ci.data(), v.data(), cfg);
+    } else if (precond_kind != PK_IDENTITY) {
+      throw Error(ERR_DIMENSION, "precond_kind must be F3RG_PRECOND_ILU0, _IC0 or _IDENTITY");
+    }
+    h->s = std::make_unique<Solver>(sp, a->m, precond_kind, nullptr, M);
     *out = h.release();
   });
 }
@@ -359,9 +483,46 @@ int f3rg_richardson_state(f3rg_richardson* r, double* omegas, uint64_t* counters
   });
 }
 
+int f3rg_richardson_set_precond(f3rg_richardson* r, const f3rg_precond* m) {
+  return guarded([&] {
+    if (!r) throw Error(ERR_DIMENSION, "null argument");
+    if (m && m->p->rows() != r->a->rows()) throw Error(ERR_DIMENSION, "preconditioner size does not match the matrix");
+    F3RG_CUDA(cudaDeviceSynchronize());
+    r->M = m ? m->p : nullptr;
+    if (r->M && !r->M->identity()) {
+      const uint64_t n = r->a->rows();
+      r->P.alloc(n * (r->prec == 0 ? 2 : r->prec == 1 ? 4 : 8) + 16);
+      r->work = r->M->make_work();
+    }
+  });
+}
+
 int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t stream) {
   return guarded([&] {
     const int p = r->prec;
+    if (r->M && !r->M->identity()) {
+      // richardson_apply with op.precondition = M (src/richardson.cpp:10-54): the
+      // launch sequence of Solver::enqueue_richardson_m
+      cudaStream_t s = as_stream(stream);
+      const uint64_t n = r->a->rows();
+      const GateH gate{r->dead.get<int>(), 0};
+      const SyncH sync{r->partials.get<double>(), r->counter.get<unsigned>()};
+      auto phase = [&](int ph, int k) {
+        F3RG_CUDA(launch_richm_phase(p, p, p, Launch{0, s}, r->a->csr(), r->a->tiles(p), ph, k, v, nullptr, z, n,
+                                     r->state.get<RichState>(), r->R.get(), r->P.get(), r->Za.get(), gate, 0,
+                                     r->cnt.get<unsigned long long>(), sync));
+      };
+      phase(RM_START_H, 0);
+      for (int k = 0; k < r->m; ++k) {
+        if (k > 0) phase(RM_RESID_H, k);
+        RichEpiH re{r->state.get<RichState>(), k, k > 0 ? r->Za.get() : nullptr, k + 1 == r->m ? z : r->Za.get()};
+        r->M->enqueue(*r->work, r->R.get(), p, r->P.get(), p, s, nullptr, 0, &re);
+        phase(RM_DOTS_H, k);
+        phase(RM_UPDATE_H, k);
+      }
+      phase(RM_BOOK_H, 0);
+      return;
+    }
     F3RG_CUDA(launch_richardson(p, p, p, Launch{0, as_stream(stream)}, r->a->csr(), r->a->tiles(p), v, nullptr, z,
                                 r->a->rows(), r->state.get<RichState>(), GateH{r->dead.get<int>(), 0}, 0,
                                 r->cnt.get<unsigned long long>(),

@@ -150,7 +150,7 @@ struct Solver::Level {
   LevelState* dstate = nullptr;
   LevelState host;
   // Richardson
-  DevBuf rs, omegas, wused, wupd, calls, R, Za, Zb;
+  DevBuf rs, omegas, wused, wupd, calls, R, Za, Zb, P;
   RichState* drs = nullptr;
   size_t vbytes(uint64_t n) const { return n * psize(W); }
   size_t zbytes(uint64_t n) const { return n * psize(PZ); }
@@ -162,8 +162,9 @@ struct Solver::ProfRec {
   cudaEvent_t e0, e1;
 };
 
-Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind, Exchange* ex)
-    : spec_(spec), a_(std::move(a)), ex_(ex) {
+Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind, Exchange* ex,
+               std::shared_ptr<const DevicePrecond> m)
+    : spec_(spec), a_(std::move(a)), ex_(ex), M_(std::move(m)) {
   if (spec_.levels.empty()) throw Error(ERR_SOLVER, "composed solver needs at least one level");
   for (const auto& L : spec_.levels)
     if (L.m < 1) throw Error(ERR_SOLVER, "every level needs m >= 1");
@@ -175,9 +176,12 @@ Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_ki
                                   std::to_string(d + 1) + " (pass allow_precision_increase to permit)");
   }
   if (spec_.levels.size() > 15) throw Error(ERR_SOLVER, "at most 15 nesting levels are supported");
-  if (precond_kind != PK_IDENTITY)
-    throw Error(ERR_UNSUPPORTED, "device primary preconditioner: only 'identity' is implemented (ILU(0)/IC(0) is "
-                                 "SURVEY.md 8(f)-1)");
+  if (precond_kind != PK_IDENTITY && !has_m())
+    throw Error(ERR_UNSUPPORTED, "an ILU(0)/IC(0) primary preconditioner needs its factorisation (f3rg_ilu_factorize)");
+  if (M_ && M_->rows() != a_->rows()) throw Error(ERR_DIMENSION, "preconditioner size does not match the matrix");
+  if (has_m() && ex_)
+    throw Error(ERR_UNSUPPORTED, "row-block partition: a block-Jacobi ILU(0)/IC(0) primary preconditioner is not "
+                                 "implemented (its blocks need not align with the ranks)");
   for (size_t d = 0; d + 1 < spec_.levels.size(); ++d)
     if (spec_.levels[d].kind == LK_RICHARDSON)
       throw Error(ERR_UNSUPPORTED, "a Richardson level with an inner solver below it is not implemented on the device");
@@ -295,6 +299,7 @@ void Solver::build_levels() {
         F3RG_CUDA(cudaMemset(L.Za.get(), 0, L.Za.bytes()));
       }
       L.Zb.alloc(m > 2 ? L.vbytes(n_) + 16 : 16);
+      if (has_m()) L.P.alloc(L.vbytes(n_) + 16);
       RichState h;
       h.m = m;
       h.cycle = L.spec.cycle;
@@ -320,6 +325,13 @@ void Solver::build_levels() {
     for (int k = 0; k < S.m && k < 1000; ++k) img[k] = S.has_omega ? S.omega : 1.0;
     unsigned long long calls[4] = {1ull, 0ull, 0ull, 0ull};
     std::memcpy(img + 1000, calls, sizeof calls);
+  }
+  if (has_m()) {
+    // the sweeps' workspace (row values, level counters) and the staging vector
+    work_ = M_->make_work();
+    work_->prepare(M_->compute_prec(lv_[D - 1]->W), own_stream_);  // before the graph capture
+    mbuf_.alloc(n_ * 8 + 16);
+    F3RG_CUDA(cudaStreamSynchronize(own_stream_));
   }
   Level& top = *lv_[0];
   xbuf_.alloc(ld_ * psize(top.spec.pv) + 16);
@@ -415,6 +427,10 @@ void Solver::enqueue_richardson(int l, int j, void* v_ext, const double* sj, voi
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
   const TilesDev T = a_->tiles(R.PA);
   const double bytes = mbytes(R.PA) + (double)n * (psize(L.W) + psize(R.W));
+  if (has_m()) {
+    enqueue_richardson_m(l, L.W, v_ext, sj, z_own, s);
+    return;
+  }
   if (!ex_) {
     PROF(kname("richardson", R.PA, R.W, L.W).c_str(), bytes,
          launch_richardson(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, v_ext, sj, z_own, n, R.drs, GateH{dead, l}, l,
@@ -449,6 +465,35 @@ void Solver::enqueue_richardson(int l, int j, void* v_ext, const double* sj, voi
                               R.drs, R.R.get(), R.Za.get(), GateH{dead, l}, l, cnt, sync, DistH{}));
 }
 
+void Solver::enqueue_richardson_m(int l, int pv, const void* v, const double* sj, void* out, cudaStream_t s) {
+  Level& R = *lv_[l];
+  const uint64_t n = n_;
+  int* dead = dead_.get<int>();
+  auto* cnt = cnt_.get<unsigned long long>();
+  SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
+  const TilesDev T = a_->tiles(R.PA);
+  const GateH gate{dead, l};
+  const int m = R.spec.m;
+  const double vb = (double)n * psize(R.W);
+  auto phase = [&](int ph, int k) {
+    return launch_richm_phase(R.PA, R.W, pv, Launch{0, s}, a_->csr(), T, ph, k, v, sj, out, n, R.drs, R.R.get(),
+                              R.P.get(), R.Za.get(), gate, l, cnt, sync);
+  };
+  PROF("richm_start", (double)n * (psize(pv) + psize(R.W)), phase(RM_START_H, 0));
+  for (int k = 0; k < m; ++k) {
+    if (k > 0)
+      PROF(kname("richm_resid", R.PA, R.W, pv).c_str(), mbytes(R.PA) + (double)n * psize(pv) + 2 * vb,
+           phase(RM_RESID_H, k));
+    RichEpiH re{R.drs, k, k > 0 ? R.Za.get() : nullptr, k + 1 == m ? out : R.Za.get()};
+    prof_begin(s);
+    M_->enqueue(*work_, R.R.get(), R.W, R.P.get(), R.W, s, dead, l, &re);
+    prof_end(s, M_->config().symmetric ? "precond_ic0" : "precond_ilu0", 0.0);
+    PROF(kname("richm_dots", R.PA, R.W, pv).c_str(), 0.0, phase(RM_DOTS_H, k));
+    PROF("richm_update", 0.0, phase(RM_UPDATE_H, k));
+  }
+  PROF("richm_book", 0.0, phase(RM_BOOK_H, 0));
+}
+
 void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
   Level& L = *lv_[l];
   const uint64_t n = n_;
@@ -476,6 +521,14 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
     }
   } else if (L.child == 1) {
     enqueue_richardson(l + 1, j, vj, sj, zj_own, s);
+  } else if (has_m()) {
+    // z_j = M (s_j v_j): the normalised basis vector staged at W (counts the
+    // PrimarySolver invocation), then the two sweeps (src/nesting.cpp:70-83)
+    PROF(kname("copy_scaled", L.W, L.W, L.W).c_str(), 2.0 * n * psize(L.W),
+         launch_copy_scaled(L.W, Launch{0, s}, vj_own, sj, mbuf_.get(), n, GateH{dead, l + 1}, cnt));
+    prof_begin(s);
+    M_->enqueue(*work_, mbuf_.get(), L.W, zj_own, L.PZ, s, dead, l + 1, nullptr);
+    prof_end(s, M_->config().symmetric ? "precond_ic0" : "precond_ilu0", 0.0);
   } else {
     PROF(kname("copy_scaled", L.W, L.W, L.W).c_str(), 2.0 * n * psize(L.W),
          launch_copy_scaled(L.W, Launch{0, s}, vj_own, sj, zj_own, n, GateH{dead, l + 1}, cnt));
@@ -730,10 +783,14 @@ Report Solver::run_richardson_top(const double* b, const RunOptions& opts, cudaS
       rep.flag = "capped";
       break;
     }
-    PROF(kname("richardson", top.PA, pv, pv).c_str(), mbytes(top.PA) + 2.0 * n * psize(pv),
-         launch_richardson(top.PA, pv, pv, Launch{0, s}, a_->csr(), a_->tiles(top.PA), rbuf_.get(), nullptr,
-                           zbuf_.get(), n, top.drs, GateH{dead, 0}, 0, cnt, sync, bar_.get<unsigned>(),
-                           bar_.get<unsigned>() + 1, nullptr));
+    if (has_m()) {
+      enqueue_richardson_m(0, pv, rbuf_.get(), nullptr, zbuf_.get(), s);
+    } else {
+      PROF(kname("richardson", top.PA, pv, pv).c_str(), mbytes(top.PA) + 2.0 * n * psize(pv),
+           launch_richardson(top.PA, pv, pv, Launch{0, s}, a_->csr(), a_->tiles(top.PA), rbuf_.get(), nullptr,
+                             zbuf_.get(), n, top.drs, GateH{dead, 0}, 0, cnt, sync, bar_.get<unsigned>(),
+                             bar_.get<unsigned>() + 1, nullptr));
+    }
     F3RG_CUDA(launch_axpy(pv, pv, Launch{0, s}, 1.0, zbuf_.get(), xbuf_.get(), n));
     rep.outer_iterations += 1;
     PROF(kname("residual", top.PA, pv, pv).c_str(), mbytes(top.PA) + (double)n * (2 * psize(pv) + 8),

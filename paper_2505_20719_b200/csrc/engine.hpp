@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "partition.hpp"
+#include "precond.hpp"
 #include "state.hpp"
 
 namespace f3rg {
@@ -256,7 +257,11 @@ class Solver {
  public:
   // ex != nullptr: this solver is one rank of a row-block partition; `a` holds the
   // rank's rows (columns in its ext layout) and every vector is the rank's slice
-  Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind, Exchange* ex = nullptr);
+  // m: the primary preconditioner (reference ComposedSolver(spec, replicas, M),
+  // src/nesting.cpp:176-215); null = IdentityPrecond. precond_kind is checked
+  // against it (an ILU/IC kind with no factorised M is ERR_UNSUPPORTED).
+  Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_kind, Exchange* ex = nullptr,
+         std::shared_ptr<const DevicePrecond> m = nullptr);
   ~Solver();
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
@@ -303,6 +308,10 @@ class Solver {
   template <class F>
   void reduce(cudaStream_t s, F&& launch);
   void enqueue_richardson(int l, int j, void* v_ext, const double* sj, void* z_own, cudaStream_t s);
+  // one Richardson call of level l with the block-Jacobi M (launch sequence,
+  // richardson.cuh k_richm_phase + the trsv.cuh sweeps); v at precision pv
+  void enqueue_richardson_m(int l, int pv, const void* v, const double* sj, void* out, cudaStream_t s);
+  bool has_m() const { return M_ && !M_->identity(); }
   size_t own(int p) const { return off_ * (p == 0 ? 2 : p == 1 ? 4 : 8); }  // byte offset of the owned rows
 
   Spec spec_;
@@ -313,7 +322,9 @@ class Solver {
   uint64_t ld_ = 0;   // vector stride of a basis (ext layout; = n_ on one rank)
   uint64_t off_ = 0;  // owned rows start here in an ext-layout vector
   Exchange* ex_ = nullptr;
-  DevBuf dead_, cnt_, partials_, dpartials_, counter_, bar_, info_, io_, norm_, xbuf_, rbuf_, zbuf_;
+  DevBuf dead_, cnt_, partials_, dpartials_, counter_, bar_, info_, io_, norm_, xbuf_, rbuf_, zbuf_, mbuf_;
+  std::shared_ptr<const DevicePrecond> M_;
+  std::unique_ptr<SweepWork> work_;
   StepInfo* info_host_ = nullptr;
   IoSlot* io_host_ = nullptr;
   double* stage_host_ = nullptr;

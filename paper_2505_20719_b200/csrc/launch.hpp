@@ -78,6 +78,28 @@ cudaError_t launch_rich_phase(int pa, int pw, int pv, Launch l, const CsrDev& A,
                               RichState* RS, void* R, void* Za, GateH gate, int level, unsigned long long* cnt,
                               SyncH sync, DistH dist);
 
+// ---- Richardson with a block-Jacobi ILU(0)/IC(0) M (richardson.cuh k_richm_phase) ----
+enum { RM_START_H = 0, RM_RESID_H = 1, RM_DOTS_H = 2, RM_UPDATE_H = 3, RM_BOOK_H = 4 };
+cudaError_t launch_richm_phase(int pa, int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, int phase, int k,
+                               const void* v, const double* v_scale, void* out, uint64_t n, RichState* RS, void* R,
+                               void* P, void* Za, GateH gate, int level, unsigned long long* cnt, SyncH sync);
+
+// ---- block-Jacobi ILU(0)/IC(0) sweeps (trsv.cuh) ------------------------------------
+struct SweepDev;
+struct SweepCtl;
+struct RichEpiH {
+  const RichState* RS = nullptr;
+  int k = 0;
+  const void* zin = nullptr;
+  void* zout = nullptr;
+};
+// forward sweep: t = L \ r (r at pin; factor precision pf; C = max(pf, pin))
+cudaError_t launch_sweep_fwd(int pf, int pin, Launch l, const SweepDev& S, const void* r, void* cells,
+                             unsigned* level_done, SweepCtl* ctl, GateH gate);
+// backward sweep at compute precision pc: z = U \ t rounded to pout (+ fused Richardson update)
+cudaError_t launch_sweep_bwd(int pf, int pc, int pout, Launch l, const SweepDev& S, const void* fcells, void* cells,
+                             void* out, unsigned* level_done, SweepCtl* ctl, GateH gate, RichEpiH re);
+
 // ---- fp64 CG / BiCGStab (krylov.cuh) ----------------------------------------------
 struct KState;
 int red_grid();

@@ -53,4 +53,12 @@ cudaError_t launch_rich_phase(int pa, int pw, int pv, Launch l, const CsrDev& A,
 #undef C_
 }
 
+cudaError_t launch_richm_phase(int pa, int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, int phase, int k,
+                               const void* v, const double* v_scale, void* out, uint64_t n, RichState* RS, void* R,
+                               void* P, void* Za, GateH gate, int level, unsigned long long* cnt, SyncH sync) {
+#define C_(PP) launch_richm_phase_t<PP>(pw, pv, l, A, T, phase, k, v, v_scale, out, n, RS, R, P, Za, gate, level, cnt, sync)
+  F3RG_BY_PA(pa, C_)
+#undef C_
+}
+
 }  // namespace f3rg

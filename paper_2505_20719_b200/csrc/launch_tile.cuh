@@ -178,6 +178,35 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
   return err;
 }
 
+template <int PA>
+cudaError_t launch_richm_phase_t(int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, int phase, int k,
+                                 const void* v, const double* v_scale, void* out, uint64_t n, RichState* RS, void* R,
+                                 void* P, void* Za, GateH gate, int level, unsigned long long* cnt, SyncH sync) {
+  cudaError_t err = cudaErrorInvalidValue;
+  auto go = [&](auto IDX_) {
+    constexpr int IDX = decltype(IDX_)::value;
+    constexpr int SM = TileCfg<PA, IDX>::SMEM_BYTES;
+    with_p(pv, [&](auto V) {
+      constexpr int PV = decltype(V)::value;
+      with_p(pw, [&](auto W) {
+        constexpr int PW = decltype(W)::value;
+        if constexpr (PW <= PV) {
+          auto kern = k_richm_phase<PA, PW, PV, IDX>;
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
+          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          if (phase == RM_BOOK) g = 1;
+          if (g < 1) g = 1;
+          launch_k(kern, g, SM, l.stream, A, T, phase, k, v, v_scale, out, n, RS, R, P, Za, to_gate(gate), level, cnt,
+                   to_sync(sync));
+          err = cudaGetLastError();
+        }
+      });
+    });
+  };
+  dispatch_idx<PA>(A, go);
+  return err;
+}
+
 #define F3RG_TILE_INSTANTIATE(PA)                                                                                  \
   template cudaError_t launch_spmv_dots_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*, void*, \
                                               uint64_t, int, LevelState*, GateH, SyncH, double*, int, int*, DistH); \
@@ -190,6 +219,9 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
                                                uint64_t, int);                                                     \
   template cudaError_t launch_rich_phase_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, int, int,          \
                                                const void*, const double*, uint64_t, void*, uint64_t, RichState*,  \
-                                               void*, void*, GateH, int, unsigned long long*, SyncH, DistH);
+                                               void*, void*, GateH, int, unsigned long long*, SyncH, DistH);        \
+  template cudaError_t launch_richm_phase_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, int, int,         \
+                                                const void*, const double*, void*, uint64_t, RichState*, void*,     \
+                                                void*, void*, GateH, int, unsigned long long*, SyncH);
 
 }  // namespace f3rg

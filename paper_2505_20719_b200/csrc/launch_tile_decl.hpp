@@ -26,5 +26,9 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
                                 const void* v, const double* v_scale, uint64_t off, void* out, uint64_t n,
                                 RichState* RS, void* R, void* Za, GateH gate, int level, unsigned long long* cnt,
                                 SyncH sync, DistH dist);
+template <int PA>
+cudaError_t launch_richm_phase_t(int pw, int pv, Launch l, const CsrDev& A, const TilesDev& T, int phase, int k,
+                                 const void* v, const double* v_scale, void* out, uint64_t n, RichState* RS, void* R,
+                                 void* P, void* Za, GateH gate, int level, unsigned long long* cnt, SyncH sync);
 
 }  // namespace f3rg

@@ -351,4 +351,93 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_rich_phase(CsrDev A, Ti
   }
 }
 
+
+// ---- Richardson with a block-Jacobi ILU(0)/IC(0) primary preconditioner -----------
+// One call of richardson_apply (src/richardson.cpp:10-54) with op.precondition = M
+// (the PrimarySolver's apply, src/nesting.cpp:70-83) as a launch sequence:
+//   RM_START  r = converted(v)                            (:19)
+//   per step k:  [k > 0] RM_RESID  r = v - A z_k          (:24-27)
+//                forward + backward sweep  p = M r         (:28, trsv.cuh); on plain
+//                calls the backward sweep also does z_{k+1} = z_k + fl(w_k) p (:49)
+//                RM_DOTS / RM_UPDATE  (update calls only, decided here on the device
+//                from call_count % c): s = A p, w' = (r,s)/(s,s) at >= fp32, z += w' p
+//   RM_BOOK   weight averaging and counters              (:42-52)
+enum { RM_START = 0, RM_RESID = 1, RM_DOTS = 2, RM_UPDATE = 3, RM_BOOK = 4 };
+
+template <int PA, int PW, int PV, int IDX>
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richm_phase(CsrDev A, TilesDev T, int phase, int k,
+                                                                     const void* v, const double* v_scale,
+                                                                     void* out, uint64_t n, RichState* RS, void* R,
+                                                                     void* P, void* Za, Gate gate, int level,
+                                                                     unsigned long long* cnt, Sync sync) {
+  pdl_wait();
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ double scratch[64];
+  __shared__ double tot[2];
+  if (gate.closed()) return;
+  constexpr int C = pmax(PA, PW);
+  constexpr int CD = pmax(P32, PW);
+  using AW = Ar<PW>;
+  const int m = RS->m;
+  const unsigned long long call = RS->calls[0];
+  const bool update = RS->cycle != 0ull && (call % RS->cycle) == 0ull;
+  RhsView<PV, PW> rhs{v, v_scale ? cvt<PV>(*v_scale) : Ar<PV>::one(), v_scale != nullptr, 0};
+  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (phase == RM_START) {
+    for (uint64_t i = gtid; i < n; i += gstride) st<PW>(R, i, rhs.row(i));
+  } else if (phase == RM_RESID) {
+    GatherCG<PW, C> g{Za};
+    EpiResid<PV, PW, C> e{rhs, R, {}};
+    spmv_tiles<PA, C, IDX, rich_chunk(IDX)>(A, T, g, e, smem);
+  } else if (phase == RM_DOTS) {
+    if (!update) return;
+    GatherCG<PW, C> g{P};
+    EpiDotsRs<PV, PW, C, CD> e{rhs, R, Ar<CD>::zero(), Ar<CD>::zero(), {}, {}};
+    spmv_tiles<PA, C, IDX, rich_chunk(IDX)>(A, T, g, e, smem);
+    T_<CD> acc[2] = {e.num, e.den};
+    block_sum<CD, 2>(acc, scratch);
+    if (threadIdx.x == 0) {
+      sync.partials[(size_t)blockIdx.x * kMaxPart + 0] = Ar<CD>::wide(acc[0]);
+      sync.partials[(size_t)blockIdx.x * kMaxPart + 1] = Ar<CD>::wide(acc[1]);
+    }
+    if (!last_block(sync.counter)) return;
+    reduce_partials<CD, 2>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (threadIdx.x == 0) {
+      const double num = tot[0], den = tot[1];
+      if (den == 0.0 || !isfinite(num) || !isfinite(den)) {
+        RS->wused[k] = RS->omegas[k];
+        RS->wupd[k] = 0;
+      } else {
+        RS->wused[k] = Ar<CD>::wide(Ar<CD>::div(cvt<CD>(num), cvt<CD>(den)));
+        RS->wupd[k] = 1;
+      }
+    }
+  } else if (phase == RM_UPDATE) {
+    if (!update) return;
+    const T_<PW> wh = cvt<PW>(RS->wused[k]);
+    void* zn = (k + 1 == m) ? out : Za;
+    for (uint64_t i = gtid; i < n; i += gstride) {
+      const T_<PW> zi = k > 0 ? ld<PW>(Za, i) : AW::zero();
+      st<PW>(zn, i, AW::add(AW::mul(wh, ld<PW>(P, i)), zi));
+    }
+  } else if (blockIdx.x == 0 && threadIdx.x == 0) {  // RM_BOOK
+    if (update) {
+      const double l = (double)(call / RS->cycle - 1ull);
+      for (int q = 0; q < m; ++q) {
+        if (RS->wupd[q]) {
+          RS->omegas[q] = __ddiv_rn(__dadd_rn(__dmul_rn(l, RS->omegas[q]), RS->wused[q]), __dadd_rn(l, 1.0));
+        } else {
+          RS->calls[2] += 1ull;
+        }
+      }
+      RS->calls[1] += 1ull;
+    }
+    RS->calls[0] = call + 1ull;
+    cnt[CNT_INV + level] += 1ull;
+    cnt[CNT_IT + level] += (unsigned long long)m;
+    cnt[CNT_PRECOND] += (unsigned long long)m;
+  }
+}
+
 }  // namespace f3rg

@@ -6,7 +6,7 @@ outer-iteration counts, residual histories and timings in reference_runs.json.
 These are the outer-count oracle for the full-size configs and the denominator
 of bench.py's reference-arm extrapolation. Test infrastructure only.
 
-    python tests/golden/make_reference_runs.py 1 2 [3 4 5]
+    python tests/golden/make_reference_runs.py 1 2 [3 4 5] [--mode=fp16-f3r-ic0,...]
 """
 import json
 import os
@@ -26,7 +26,13 @@ SPECS = {
     "fp16-f3r": "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > identity",
     "fp32-f3r": "F100:f64/f64 > F8:f32/f32 > F4:f32/f32 > R2:f32,c=64 > identity",
     "fp64-f3r": "F100:f64/f64 > F8:f64/f64 > F4:f64/f64 > R2:f64,c=64 > identity",
+    # the reference bench's default primary preconditioner (include/f3r/bench.hpp:31-34,
+    # src/bench.cpp:160-177): block-Jacobi IC(0) on symmetric problems, ILU(0)
+    # otherwise, 4 blocks, alpha 1, factors at the Richardson precision
+    "fp16-f3r-ic0": "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > ic0(blocks=4,alpha=1,prec=f16)",
+    "fp16-f3r-ilu0": "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > ilu0(blocks=4,alpha=1,prec=f16)",
 }
+PRECOND = {"fp16-f3r-ic0": (4, 1.0, True, 0), "fp16-f3r-ilu0": (4, 1.0, False, 0)}
 OUT = os.path.join(HERE, "reference_runs.json")
 
 
@@ -39,7 +45,8 @@ def main(configs, modes=("fp16-f3r",)):
         m = r.matrix(p.row_ptr, p.col_idx, p.values)
         for mode in modes:
             t0 = time.time()
-            rep = r.solve(m, SPECS[mode], p.b, tol=1e-10, want_x=False)
+            M = r.ilu(m, *PRECOND[mode]) if mode in PRECOND else None
+            rep = r.solve(m, SPECS[mode], p.b, tol=1e-10, want_x=False, precond=M)
             data[f"config{c}/{mode}"] = {
                 "n": p.n, "nnz": p.nnz, "outer_iterations": rep.outer_iterations,
                 "precond_invocations": rep.precond_invocations, "converged": rep.converged,
@@ -56,4 +63,7 @@ def main(configs, modes=("fp16-f3r",)):
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     modes = ("fp16-f3r", "fp32-f3r", "fp64-f3r") if "--all-modes" in sys.argv else ("fp16-f3r",)
+    for a in sys.argv[1:]:
+        if a.startswith("--mode="):
+            modes = tuple(a[7:].split(","))
     main(args or ["1", "2"], modes)
