@@ -40,6 +40,15 @@ METRIC = "time-to-solution to rel. residual 1e-10 (s)"
 TOL = 1e-10
 
 
+def spec_for(args):
+    """the timed nest: M = identity (the north-star path) or, with --precond, the
+    reference bench's default block-Jacobi M (4 blocks, alpha 1, fp16 factors;
+    include/f3r/bench.hpp:31-34, src/bench.cpp:160-177)"""
+    if args.precond == "identity":
+        return SPEC
+    return SPEC.rsplit(">", 1)[0] + f"> {args.precond}(blocks=4,alpha=1,prec=f16)"
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -126,7 +135,7 @@ def reference_runs():
         return {}
 
 
-def cpu_reference_sample(p, outer_full: int, threads: int, sample_outer: int = 1):
+def cpu_reference_sample(p, outer_full: int, threads: int, sample_outer: int = 1, args=None):
     """Times the UNMODIFIED reference solve for `sample_outer` outer iterations
     (RunOptions.max_outer_total, include/f3r/nesting.hpp:35); returns seconds per
     outer iteration and the extrapolated time-to-solution."""
@@ -134,9 +143,23 @@ def cpu_reference_sample(p, outer_full: int, threads: int, sample_outer: int = 1
     r = Reference()
     r.set_threads(threads)
     m = r.matrix(p.row_ptr, p.col_idx, p.values)
-    rep = r.solve(m, SPEC, p.b, tol=TOL, max_outer_total=sample_outer, want_x=False)
+    M = _ref_m(r, m, args)
+    rep = r.solve(m, spec_for(args) if args else SPEC, p.b, tol=TOL, max_outer_total=sample_outer, want_x=False,
+                  precond=M)
     per_outer = rep.wall_seconds / max(1, rep.outer_iterations)
     return per_outer, per_outer * outer_full, rep
+
+
+def _ref_m(r, m, args):
+    """the reference's own BlockJacobiIlu0::factorize for --precond (untimed setup, as
+    the reference bench times factorisation apart, src/bench.cpp:202-207)"""
+    if args is None or args.precond == "identity":
+        return None
+    return r.ilu(m, 4, 1.0, args.precond == "ic0", 0)
+
+
+def _mode_key(args):
+    return "fp16-f3r" if args.precond == "identity" else f"fp16-f3r-{args.precond}"
 
 
 def run_reference_arm(args):
@@ -146,7 +169,7 @@ def run_reference_arm(args):
     from paper_2505_20719_b200 import problems
     p = problems.problem(args.config)
     threads = os.cpu_count()
-    runs = reference_runs().get(f"config{args.config}/fp16-f3r", {})
+    runs = reference_runs().get(f"config{args.config}/{_mode_key(args)}", {})
     outer_full = int(runs.get("outer_iterations", 0)) or None
     from oracle_bind import Reference, reference_available
     if not reference_available():
@@ -155,14 +178,16 @@ def run_reference_arm(args):
     r = Reference()
     r.set_threads(threads)
     m = r.matrix(p.row_ptr, p.col_idx, p.values)
+    M = _ref_m(r, m, args)
+    spec = spec_for(args)
     if outer_full is None:  # no committed full run for this config: measure it once
-        full = r.solve(m, SPEC, p.b, tol=TOL, want_x=False)
+        full = r.solve(m, spec, p.b, tol=TOL, want_x=False, precond=M)
         outer_full = full.outer_iterations
     for _ in range(min(args.warmup, 1)):
-        r.solve(m, SPEC, p.b, tol=TOL, max_outer_total=1, want_x=False)
+        r.solve(m, spec, p.b, tol=TOL, max_outer_total=1, want_x=False, precond=M)
     times = []
     for _ in range(args.steps):
-        rep = r.solve(m, SPEC, p.b, tol=TOL, max_outer_total=1, want_x=False)
+        rep = r.solve(m, spec, p.b, tol=TOL, max_outer_total=1, want_x=False, precond=M)
         times.append(rep.wall_seconds)
     per_outer = float(np.mean(times))
     value = per_outer * outer_full
@@ -180,8 +205,9 @@ def run_reference_arm(args):
 
 
 def _config(args, p):
-    return {"workload": f"BASELINE config {args.config}: fp16-F3R solve to 1e-10 (M = identity)", "n": p.n,
-            "nnz": p.nnz, "solver": SPEC, "problem": p.name, "tol": TOL,
+    mname = "identity" if args.precond == "identity" else f"block-Jacobi {args.precond}, 4 blocks, fp16 factors"
+    return {"workload": f"BASELINE config {args.config}: fp16-F3R solve to 1e-10 (M = {mname})", "n": p.n,
+            "nnz": p.nnz, "solver": spec_for(args), "problem": p.name, "tol": TOL,
             "l2_flush": "none: working set (A16+idx 334 MB, A32+idx 446 MB) exceeds the 126 MB L2",
             "parallelism": f"dp{args.gpus}" if args.gpus > 1 else "single GPU"}
 
@@ -273,11 +299,18 @@ def run_ours(args):
 
     rank, local, world = dist_env()
     if world > 1 or args.partition:
+        if args.precond != "identity":
+            raise SystemExit("--precond: the row-block partition runs M = identity only (DESIGN.md section 6c)")
         return run_partitioned(args)
     torch.cuda.set_device(local)
     p = problems.problem(args.config)
     reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
-    solver = f.build(f.parse_solver_spec(SPEC), reps, f.IdentityPrecond(p.n))
+    if args.precond == "identity":
+        M = f.IdentityPrecond(p.n)
+    else:  # factorised once, untimed (the reference bench times it apart)
+        M = f.BlockJacobiIlu0.factorize(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values),
+                                        f.IluConfig(4, 1.0, args.precond == "ic0", f.Precision.P16))
+    solver = f.build(f.parse_solver_spec(spec_for(args)), reps, M)
     opts = f.RunOptions(tol=TOL)
     b_dev = torch.from_numpy(p.b).cuda()
     stream = torch.cuda.current_stream()
@@ -326,7 +359,10 @@ def run_ours(args):
     prof = solver.profile()
     total_ms = sum(k[1] for k in prof)
     launches = int(sum(k[2] for k in prof))
-    top = max(prof, key=lambda k: k[1])
+    # roofline of the top STREAMING kernel (the ILU/IC sweeps are latency-bound:
+    # reported apart, per dependency level)
+    streaming = [k for k in prof if not k[0].startswith("precond_")]
+    top = max(streaming, key=lambda k: k[1])
     peak, peak_kind = _peaks()
     per_launch_ms = top[1] / top[2]
     # profile bytes are what the kernel streams (D16 column stream when in use);
@@ -355,13 +391,21 @@ def run_ours(args):
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
     }
+    pre = [k for k in prof if k[0].startswith("precond_")]
+    if pre:
+        lv = M.sweep_levels()
+        apply_ms = pre[0][1] / pre[0][2]
+        line["precond"] = {"kernel": pre[0][0], "share": round(pre[0][1] / total_ms, 4), "applies": pre[0][2],
+                           "apply_ms": round(apply_ms, 4), "sweep_levels": list(lv),
+                           "us_per_level": round(1e3 * apply_ms / (lv[0] + lv[1]), 3), "bound": "latency"}
     if not args.no_cpu_baseline:
         try:
             threads = os.cpu_count()
-            per_outer, extrap, rep = cpu_reference_sample(p, outer, threads)
+            per_outer, extrap, rep = cpu_reference_sample(p, outer, threads, args=args)
             line["cpu_baseline"] = {"value": extrap, "unit": "s", "cores": threads, "kind": "reference",
                                     "sample": f"1 outer iteration of the unmodified reference fp16-F3R solve "
-                                              f"({per_outer:.2f} s), extrapolated x{outer} outer iterations"}
+                                              f"(M = {args.precond}; {per_outer:.2f} s), extrapolated "
+                                              f"x{outer} outer iterations"}
         except Exception as e:  # keep the GPU line even if the CPU leg fails
             line["cpu_baseline"] = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"failed: {e}"}
@@ -376,6 +420,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precond", default="identity", choices=["identity", "ic0", "ilu0"],
+                    help="primary preconditioner M of the nest (default identity, the north-star path)")
     ap.add_argument("--partition", action="store_true",
                     help="use the row-block partitioned NCCL path even on one GPU")
     args = ap.parse_args()

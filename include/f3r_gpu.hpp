@@ -4,8 +4,10 @@
 //
 //   reference (include/f3r/...)                   this header
 //   SparseCsr + make_replicas  csr.hpp:23-81       f3r_gpu::DeviceReplicas
-//   ComposedSolver(spec, replicas, M)              f3r_gpu::ComposedSolver(spec, replicas)
+//   ComposedSolver(spec, replicas, M)              f3r_gpu::ComposedSolver(spec, replicas[, M])
 //     nesting.hpp:55-77
+//   IdentityPrecond / BlockJacobiIlu0::factorize   f3r_gpu::DevicePreconditioner::identity /
+//     ilu.hpp:34-84                                ::factorize (config fields as IluConfig)
 //   RunOptions  nesting.hpp:29-38                  f3r_gpu::RunOptions (same fields)
 //   ConvergenceReport  report.hpp:18-30            f3r_gpu::ConvergenceReport (same fields)
 //   RunResult{x, report}  nesting.hpp:46-49        f3r_gpu::RunResult{x (fp64), report}
@@ -130,6 +132,40 @@ class DeviceReplicas {
   std::unique_ptr<f3rg_matrix, Del> m_;
 };
 
+// The primary preconditioner M on the device: IdentityPrecond, or block-Jacobi
+// ILU(0)/IC(0) factorised on the host at fp64 exactly as BlockJacobiIlu0::factorize
+// (src/ilu.cpp:38-185) and applied by bit-exact device sweeps. Throws
+// FactorizationError with the reference's message.
+class DevicePreconditioner {
+ public:
+  static DevicePreconditioner identity(std::uint64_t n) {
+    f3rg_precond* m = nullptr;
+    check(f3rg_precond_identity(&m, n));
+    return DevicePreconditioner(m);
+  }
+  static DevicePreconditioner factorize(std::uint64_t n, const std::uint32_t* row_ptr, const std::uint32_t* col_idx,
+                                        const double* values, std::uint64_t nblocks, double alpha, bool symmetric,
+                                        int apply_precision) {
+    f3rg_csr c{n, row_ptr, col_idx, values};
+    f3rg_ilu_config cfg{nblocks, alpha, symmetric ? 1 : 0, apply_precision};
+    f3rg_precond* m = nullptr;
+    check(f3rg_ilu_factorize(&m, &c, &cfg));
+    return DevicePreconditioner(m);
+  }
+  // the reference's SparseCsr (a64) and IluConfig, without including their headers
+  template <class Csr, class Cfg>
+  static DevicePreconditioner factorize(const Csr& a64, const Cfg& cfg) {
+    return factorize(a64.rows(), a64.row_ptr().data(), a64.col_idx().data(), a64.template values_as<double>().data(),
+                     cfg.nblocks, cfg.alpha, cfg.symmetric, static_cast<int>(cfg.apply_precision));
+  }
+  std::uint64_t rows() const { return f3rg_precond_rows(m_.get()); }
+  const f3rg_precond* handle() const { return m_.get(); }
+
+ private:
+  explicit DevicePreconditioner(f3rg_precond* m) : m_(m, f3rg_precond_destroy) {}
+  std::shared_ptr<f3rg_precond> m_;
+};
+
 // ComposedSolver over device replicas. `spec` is the reference grammar
 // (src/solver_spec.cpp), e.g. "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 >
 // identity". The replicas must outlive the solver (nesting.hpp:51-54). Like the
@@ -140,6 +176,13 @@ class ComposedSolver {
   ComposedSolver(const std::string& spec, const DeviceReplicas& a) : n_(a.rows()) {
     f3rg_solver* s = nullptr;
     check(f3rg_solver_create(&s, a.handle(), spec.c_str(), F3RG_PRECOND_IDENTITY));
+    s_.reset(s);
+    id_ = f3rg_solver_id(s);
+  }
+  // with a primary preconditioner (the device keeps its own reference to it)
+  ComposedSolver(const std::string& spec, const DeviceReplicas& a, const DevicePreconditioner& m) : n_(a.rows()) {
+    f3rg_solver* s = nullptr;
+    check(f3rg_solver_create_m(&s, a.handle(), spec.c_str(), m.handle()));
     s_.reset(s);
     id_ = f3rg_solver_id(s);
   }

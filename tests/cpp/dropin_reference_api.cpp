@@ -8,11 +8,12 @@
 // library compiled from its sources (oracle/_ref/libf3r_ref.so); the binary lands
 // in oracle/_ref/ and is run by tests/test_dropin.py on the GPU box.
 //
-// usage: dropin_reference_api <log2_n> <beta> [spec]
+// usage: dropin_reference_api <log2_n> <beta> [spec] [identity|ic0|ilu0]
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <string>
 
 #include "f3r/errors.hpp"  // first: f3r_gpu then rethrows the reference's exception classes
@@ -31,9 +32,7 @@ namespace f3r {
 class GpuComposedSolver {
  public:
   GpuComposedSolver(const SolverSpec& spec, const PrecisionReplicas& a, const Preconditioner& m)
-      : dev_(f3r_gpu::DeviceReplicas::from(a.a64)), s_(spec.to_string(), dev_) {
-    if (m.rows() != a.a64.rows()) throw DimensionError("preconditioner size mismatch");
-  }
+      : dev_(f3r_gpu::DeviceReplicas::from(a.a64)), m_(device_m(a, m)), s_(spec.to_string(), dev_, m_) {}
   RunResult run(const DenseVector& b, const RunOptions& o = {}) {
     const auto& b64 = b.data<double>();  // the outermost level is fp64 on this path
     f3r_gpu::RunOptions go{o.tol, o.max_outer_restarts, o.max_outer_total, o.reset_richardson_on_restart};
@@ -56,7 +55,16 @@ class GpuComposedSolver {
   const std::string& id() const { return s_.id(); }
 
  private:
+  // the same M on the device: a BlockJacobiIlu0 is refactorised there from the fp64
+  // replica with its own config (the factorisation is deterministic and identical)
+  static f3r_gpu::DevicePreconditioner device_m(const PrecisionReplicas& a, const Preconditioner& m) {
+    if (m.rows() != a.a64.rows()) throw DimensionError("preconditioner size mismatch");
+    if (const auto* bj = dynamic_cast<const BlockJacobiIlu0*>(&m))
+      return f3r_gpu::DevicePreconditioner::factorize(a.a64, bj->config());
+    return f3r_gpu::DevicePreconditioner::identity(m.rows());
+  }
   f3r_gpu::DeviceReplicas dev_;
+  f3r_gpu::DevicePreconditioner m_;
   f3r_gpu::ComposedSolver s_;
 };
 
@@ -75,7 +83,18 @@ int main(int argc, char** argv) {
   f3r::spmv(a, ones, b);
   f3r::ScaledSystem sys = f3r::diagonal_scale(a, b);
   f3r::PrecisionReplicas reps = f3r::make_replicas(std::move(sys.matrix));
-  f3r::IdentityPrecond m(reps.a64.rows());
+  const std::string mkind = argc > 4 ? argv[4] : "identity";
+  std::unique_ptr<f3r::Preconditioner> mp;
+  if (mkind == "identity") {
+    mp = std::make_unique<f3r::IdentityPrecond>(reps.a64.rows());
+  } else {  // the reference bench's default M: 4 blocks, alpha 1, fp16 factors
+    f3r::IluConfig cfg;
+    cfg.nblocks = 4;
+    cfg.symmetric = mkind == "ic0";
+    cfg.apply_precision = f3r::Precision::P16;
+    mp = std::make_unique<f3r::BlockJacobiIlu0>(f3r::BlockJacobiIlu0::factorize(reps.a64, cfg));
+  }
+  const f3r::Preconditioner& m = *mp;
   const f3r::SolverSpec spec = f3r::parse_solver_spec(spec_text);
   f3r::RunOptions opts;
   opts.tol = 1e-10;
