@@ -202,6 +202,15 @@ int f3rg_richardson_set_precond(f3rg_richardson* r, const f3rg_precond* m);
 int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* b_host, double* x_host, double tol,
                       uint64_t max_precond_invocations, f3rg_report* rep, double* history, uint64_t hist_cap);
 
+/* ---- the reference's restarted fp64 FGMRES(m) with a terminal preconditioner
+ *      (src/fgmres.cpp:163-222: fgmres_restarted; the bench's "fgmres64"). Cycles of
+ *      `restart` steps from the current iterate until tol (estimate AND fp64 true
+ *      residual) or max_precond_invocations applications of M ("capped"). m: a
+ *      preconditioner from f3rg_precond_identity / f3rg_ilu_factorize. */
+int f3rg_fgmres_solve(const f3rg_matrix* a, const f3rg_precond* m, int restart, const double* b_host, double* x_host,
+                      double tol, uint64_t max_precond_invocations, f3rg_report* rep, double* history,
+                      uint64_t hist_cap);
+
 /* ---- row-block partition over P ranks ---------
  * Rows split by the reference's rule (src/ilu.cpp:47-54: base = n/P, remainder to the
  * leading blocks). Each rank keeps its rows of A and of every Krylov vector; SpMV

@@ -420,19 +420,34 @@ int ref_solve_m(void* h, const char* spec, void* precond, const double* b, doubl
 
 // The reference's competitor solvers (src/cg.cpp:22-171) with M = IdentityPrecond:
 // which = 0 cg_solve, 1 bicgstab_solve. Same report layout as ref_solve.
+int ref_krylov_solve_m(void* h, int which, void* precond, int restart, const double* b, double tol,
+                       uint64_t max_precond, double* x_out, double* history, uint64_t hist_cap, RefReport* rep);
 int ref_krylov_solve(void* h, int which, const double* b, double tol, uint64_t max_precond, double* x_out,
                      double* history, uint64_t hist_cap, RefReport* rep) {
+  return ref_krylov_solve_m(h, which, nullptr, 64, b, tol, max_precond, x_out, history, hist_cap, rep);
+}
+
+// which = 2: fgmres_restarted(a, M, b, restart, FgmresOptions) (src/fgmres.cpp:163-222);
+// precond: a BlockJacobiIlu0 from ref_ilu_factorize, nullptr = IdentityPrecond
+int ref_krylov_solve_m(void* h, int which, void* precond, int restart, const double* b, double tol,
+                       uint64_t max_precond, double* x_out, double* history, uint64_t hist_cap, RefReport* rep) {
   return guarded([&] {
     auto* m = static_cast<RefMatrix*>(h);
     const std::size_t n = m->reps.a64.rows();
     f3r::IdentityPrecond ident(n);
+    const f3r::Preconditioner& M =
+        precond ? static_cast<const f3r::Preconditioner&>(*static_cast<f3r::BlockJacobiIlu0*>(precond)) : ident;
     f3r::ReferenceSolveOptions opts;
     opts.tol = tol;
     opts.max_precond_invocations = max_precond;
+    f3r::FgmresOptions fo;
+    fo.tol = tol;
+    fo.max_precond_invocations = max_precond;
     const DenseVector bv = make_vec(b, n, 2);
     const auto t0 = std::chrono::steady_clock::now();
-    const f3r::ConvergenceReport r = which == 0 ? f3r::cg_solve(m->reps.a64, ident, bv, opts)
-                                                : f3r::bicgstab_solve(m->reps.a64, ident, bv, opts);
+    const f3r::ConvergenceReport r = which == 0   ? f3r::cg_solve(m->reps.a64, M, bv, opts)
+                                     : which == 1 ? f3r::bicgstab_solve(m->reps.a64, M, bv, opts)
+                                                  : f3r::fgmres_restarted(m->reps.a64, M, bv, restart, fo);
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::memset(rep, 0, sizeof(*rep));
     rep->converged = r.converged;

@@ -158,6 +158,7 @@ def lib():
     L.f3rg_ilu_factorize_host.argtypes = [C.POINTER(_Csr), C.POINTER(_IluCfg), C.POINTER(u64), C.POINTER(u64), vp, vp,
                                           vp, vp, vp, vp]
     L.f3rg_solver_create_m.argtypes = [C.POINTER(vp), vp, C.c_char_p, vp]
+    L.f3rg_fgmres_solve.argtypes = [vp, vp, i32, vp, vp, dbl, u64, C.POINTER(_Report), vp, u64]
     _lib = L
     return L
 
@@ -707,6 +708,33 @@ def bicgstab_solve(a, m: IdentityPrecond, b, opts: ReferenceSolveOptions = Refer
     return _krylov_solve(1, a, m, b, opts, x_out)
 
 
+@dataclass
+class FgmresOptions:
+    """reference FgmresOptions, include/f3r/fgmres.hpp:41-44"""
+    tol: float = 1e-8
+    max_precond_invocations: int = 19200
+
+
+def fgmres_restarted(a, m: Preconditioner, b, restart: int, opts: FgmresOptions = FgmresOptions(), x_out=None):
+    """reference fgmres_restarted (include/f3r/fgmres.hpp:46-49, src/fgmres.cpp:163-222):
+    fp64 FGMRES(restart) with the terminal preconditioner m, on the device."""
+    dev = a.dev if isinstance(a, (PrecisionReplicas, ReplicaView)) else _DeviceMatrix(a)
+    n = dev.n
+    if m.rows() != n:
+        raise DimensionError("preconditioner size does not match the matrix")
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.size != n:
+        raise DimensionError("rhs length mismatch")
+    r = _Report()
+    hist = np.zeros(int(opts.max_precond_invocations) + 2)
+    _check(lib().f3rg_fgmres_solve(dev.h, m._handle(), int(restart), b.ctypes.data,
+                                   x_out.ctypes.data if x_out is not None else None, float(opts.tol),
+                                   int(opts.max_precond_invocations), C.byref(r), hist.ctypes.data, hist.size))
+    return ConvergenceReport(bool(r.converged), int(r.outer_iterations), int(r.precond_invocations), [],
+                             list(hist[:r.n_history]), r.final_true_residual, r.wall_seconds, [], r.flag.decode(),
+                             f"fgmres{int(restart)}")
+
+
 # ------------------------------------------------------------- Richardson (richardson.hpp)
 class RichardsonState:
     """Persistent Richardson state on the device (reference RichardsonState,
@@ -771,5 +799,6 @@ __all__ = [
     "PrecisionReplicas", "make_replicas", "spmv", "Preconditioner", "IdentityPrecond", "IluConfig",
     "BlockJacobiIlu0", "ilu_factorize_host", "SolverSpec", "parse_solver_spec",
     "canonical_spec", "F3rMode", "F3rConfig", "f3r_spec", "RunOptions", "ConvergenceReport", "RunResult",
-    "ComposedSolver", "build", "build_f3r", "RichardsonState", "richardson_apply", "lib",
+    "ComposedSolver", "build", "build_f3r", "RichardsonState", "richardson_apply", "lib", "FgmresOptions",
+    "fgmres_restarted", "ReferenceSolveOptions", "cg_solve", "bicgstab_solve",
 ]

@@ -533,6 +533,35 @@ int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t 
 
 }  // extern "C"
 
+// ---- restarted fp64 FGMRES(m) with M (reference fgmres_restarted) ------------------------
+extern "C" int f3rg_fgmres_solve(const f3rg_matrix* a, const f3rg_precond* m, int restart, const double* b_host,
+                                 double* x_host, double tol, uint64_t max_precond, f3rg_report* rep, double* history,
+                                 uint64_t hist_cap) {
+  return guarded([&] {
+    if (!a || !b_host || !m) throw Error(ERR_DIMENSION, "null argument");
+    if (restart < 1) throw Error(ERR_SOLVER, "restart length must be >= 1");
+    const uint64_t n = a->m->rows();
+    const int kind = m->p->identity() ? PK_IDENTITY : m->p->config().symmetric ? PK_IC0 : PK_ILU0;
+    Solver s(parse_spec("F" + std::to_string(restart) + ":f64/f64"), a->m, kind, nullptr, m->p);
+    DevBuf b(n * 8 + 16), x(n * 8 + 16);
+    F3RG_CUDA(cudaMemcpy(b.get(), b_host, n * 8, cudaMemcpyHostToDevice));
+    RunOptions o;
+    o.tol = tol;
+    o.restart_budget = max_precond;
+    Report r = s.run(b.get<double>(), x_host ? x.get<double>() : nullptr, o, nullptr);
+    if (max_precond == 0) {  // the reference caps before the first cycle
+      r.outer_iterations = 0;
+      r.flag = "capped";
+    }
+    r.solver_id = "fgmres" + std::to_string(restart);
+    r.level_iterations.clear();
+    r.omegas_final.clear();
+    if (x_host) F3RG_CUDA(cudaMemcpy(x_host, x.get(), n * 8, cudaMemcpyDeviceToHost));
+    fill_report(r, rep);
+    for (uint64_t i = 0; history && i < r.residual_history.size() && i < hist_cap; ++i) history[i] = r.residual_history[i];
+  });
+}
+
 // ---- fp64 CG / BiCGStab -------------------------------------------------------------
 extern "C" int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* b_host, double* x_host, double tol,
                                  uint64_t max_precond, f3rg_report* rep, double* history, uint64_t hist_cap) {

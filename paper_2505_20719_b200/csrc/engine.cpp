@@ -681,8 +681,11 @@ Report Solver::run_fgmres_top(const double* b, const RunOptions& opts, cudaStrea
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
   int executions = 0;
   const int max_exec = 1 + std::max(0, opts.max_outer_restarts);
+  const bool restarted = opts.restart_budget > 0;  // fgmres_restarted (src/fgmres.cpp:163-222)
   for (;;) {
-    const unsigned long long remaining = opts.max_outer_total - rep.outer_iterations;
+    // one precondition call per Arnoldi step of the outermost level
+    const unsigned long long remaining =
+        restarted ? opts.restart_budget - rep.outer_iterations : opts.max_outer_total - rep.outer_iterations;
     if (remaining == 0) {
       rep.flag = "capped";
       break;
@@ -750,7 +753,7 @@ Report Solver::run_fgmres_top(const double* b, const RunOptions& opts, cudaStrea
     }
     rep.outer_iterations += (unsigned long long)iterations;
     if (diverged) {
-      rep.flag = "divergence at outer step " + std::to_string(div_step);
+      rep.flag = (restarted ? "divergence at step " : "divergence at outer step ") + std::to_string(div_step);
       break;
     }
     if (residual_norm < opts.tol * bnorm && true_rel(b, bnorm, s) < opts.tol) {
@@ -758,7 +761,7 @@ Report Solver::run_fgmres_top(const double* b, const RunOptions& opts, cudaStrea
       break;
     }
     ++executions;
-    if (executions >= max_exec) {
+    if (restarted ? rep.outer_iterations >= opts.restart_budget : executions >= max_exec) {
       rep.flag = "capped";
       break;
     }

@@ -238,6 +238,10 @@ struct RunOptions {
   int max_outer_restarts = 3;
   unsigned long long max_outer_total = 300;
   bool reset_richardson_on_restart = false;
+  // > 0: the reference's fgmres_restarted driver instead of ComposedSolver::run
+  // (src/fgmres.cpp:163-222): cycles repeat until tol or this many applications of
+  // the outermost level's preconditioner; no restart cap
+  unsigned long long restart_budget = 0;
 };
 
 struct Report {

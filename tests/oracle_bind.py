@@ -276,6 +276,8 @@ class Reference:
         L.ref_ilu_destroy.argtypes = [C.c_void_p]
         L.ref_ilu_apply.argtypes = [C.c_void_p, _dp, C.c_int, _dp, C.c_int]
         L.ref_richardson_apply_m.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, _dp, _dp]
+        L.ref_krylov_solve_m.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, _dp, C.c_double, C.c_uint64,
+                                         C.c_void_p, _dp, C.c_uint64, C.POINTER(_RefReport)]
         L.ref_set_threads.argtypes = [C.c_int]
         L.ref_max_threads.restype = C.c_int
 
@@ -404,12 +406,15 @@ class Reference:
                       list(rep.level_iterations[:rep.n_levels]), list(hist[:min(rep.n_history, hist_cap)]),
                       list(rep.omegas[:rep.n_omegas]), rep.flag.decode(), rep.wall_seconds, rep.id.decode(), x=x)
 
-    def krylov_solve(self, mat, which, b, tol=1e-10, max_precond=19200, hist_cap=1 << 16) -> Report:
-        """reference cg_solve (which="cg") / bicgstab_solve ("bicgstab"), src/cg.cpp:22-171, M = identity"""
+    def krylov_solve(self, mat, which, b, tol=1e-10, max_precond=19200, hist_cap=1 << 16, precond=None,
+                     restart=64) -> Report:
+        """reference cg_solve (which="cg") / bicgstab_solve ("bicgstab"), src/cg.cpp:22-171, or
+        fgmres_restarted ("fgmres", src/fgmres.cpp:163-222); M = identity or `precond`"""
         hist = np.zeros(hist_cap)
         rep = _RefReport()
-        self._check(self.lib.ref_krylov_solve(mat.h, 0 if which == "cg" else 1, _f64(b), tol, max_precond, None, hist,
-                                              hist_cap, C.byref(rep)))
+        w = {"cg": 0, "bicgstab": 1, "fgmres": 2}[which]
+        self._check(self.lib.ref_krylov_solve_m(mat.h, w, precond.h if precond is not None else None, int(restart),
+                                                _f64(b), tol, max_precond, None, hist, hist_cap, C.byref(rep)))
         return Report(bool(rep.converged), rep.outer_iterations, rep.precond_invocations, rep.final_true_residual,
                       [], list(hist[:min(rep.n_history, hist_cap)]), [], rep.flag.decode(), rep.wall_seconds,
                       rep.id.decode())

@@ -1,5 +1,6 @@
-"""The reference's fp64 competitor solvers (src/cg.cpp:22-171: cg_solve and
-bicgstab_solve, M = identity) on the device, against the UNMODIFIED reference."""
+"""The reference's fp64 competitor solvers on the device, against the UNMODIFIED
+reference: cg_solve and bicgstab_solve (src/cg.cpp:22-171, M = identity) and
+fgmres_restarted (src/fgmres.cpp:163-222, M = identity or block-Jacobi IC(0)/ILU(0))."""
 import numpy as np
 import pytest
 
@@ -86,3 +87,46 @@ def test_zero_rhs(cases):
     for solve in (f.cg_solve, f.bicgstab_solve):
         rep = solve(_dev(p), f.IdentityPrecond(p.n), np.zeros(p.n))
         assert rep.converged and rep.residual_history == [0.0] and rep.outer_iterations == 0
+
+
+@pytest.mark.parametrize("mkind", ["identity", "block-jacobi-f16", "block-jacobi-f64"])
+def test_fgmres64_matches_reference(cases, reference, mkind):
+    """the reference's fgmres_restarted (src/fgmres.cpp:163-222, the bench's "fgmres64")
+    with M = identity or its bench-default block-Jacobi IC(0)/ILU(0) (4 blocks)"""
+    import paper_2505_20719_b200 as f
+    reference.set_threads(0)
+    sym = {"poisson24", "hpcg16", "aniso16"}
+    for name, p in cases:
+        a = f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values)
+        ref_m = reference.matrix(p.row_ptr, p.col_idx, p.values)
+        if mkind == "identity":
+            M, RM = f.IdentityPrecond(p.n), None
+        else:
+            prec = 0 if mkind.endswith("f16") else 2
+            M = f.BlockJacobiIlu0.factorize(a, f.IluConfig(4, 1.0, name in sym, f.Precision(prec)))
+            RM = reference.ilu(ref_m, 4, 1.0, name in sym, prec)
+        x = np.zeros(p.n)
+        rep = f.fgmres_restarted(f.make_replicas(a), M, p.b, 64, f.FgmresOptions(tol=TOL), x_out=x)
+        ref = reference.krylov_solve(ref_m, "fgmres", p.b, tol=TOL, precond=RM, restart=64)
+        assert rep.converged == ref.converged, (name, rep.flag, ref.flag)
+        want = ref.outer_iterations
+        assert abs(rep.outer_iterations - want) <= max(1, round(0.1 * want)), (name, rep.outer_iterations, want)
+        assert rep.precond_invocations == rep.outer_iterations
+        if rep.converged:
+            assert rep.final_true_residual < TOL
+            import scipy.sparse as sp
+            A = sp.csr_matrix((p.values, p.col_idx, p.row_ptr), shape=(p.n, p.n))
+            assert np.linalg.norm(p.b - A @ x) / np.linalg.norm(p.b) < TOL * 1.0001
+        k = min(10, want, rep.outer_iterations)
+        assert np.allclose(rep.residual_history[:k + 1], ref.residual_history[:k + 1], rtol=1e-6), name
+
+
+def test_fgmres_capped_like_reference(cases, reference):
+    import paper_2505_20719_b200 as f
+    name, p = cases[3]
+    rep = f.fgmres_restarted(_dev(p), f.IdentityPrecond(p.n), p.b, 16, f.FgmresOptions(tol=1e-14,
+                                                                                        max_precond_invocations=40))
+    ref = reference.krylov_solve(reference.matrix(p.row_ptr, p.col_idx, p.values), "fgmres", p.b, tol=1e-14,
+                                 max_precond=40, restart=16)
+    assert rep.flag == ref.flag == "capped" and not rep.converged
+    assert rep.precond_invocations == ref.precond_invocations == 40
