@@ -1,6 +1,9 @@
-"""fp16-F3R against the reference's fp64 competitor solvers (CG, BiCGStab; M =
-identity) on the device, BASELINE configs: outer/iteration counts and
-time-to-solution (the paper's comparison, on B200).
+"""fp16-F3R against the reference's fp64 competitor solvers on the device, BASELINE
+configs: outer/iteration counts and time-to-solution (the paper's comparison, on
+B200). CG and BiCGStab with M = identity; FGMRES(64) (fgmres_restarted) and
+fp16-F3R with M = identity and with the reference bench's block-Jacobi default
+(IC(0) on symmetric problems, ILU(0) otherwise; 4 blocks; fp16 factors for F3R,
+fp64 for FGMRES(64) as src/bench.cpp:171-177 resolves them).
 
     python tools/competitors.py [configs...]      (default: 1 2 3 4)
 """
@@ -40,4 +43,24 @@ for cfg in [int(c) for c in sys.argv[1:]] or [1, 2, 3, 4]:
         k = solve(reps, f.IdentityPrecond(p.n), p.b, f.ReferenceSolveOptions(tol=TOL))
         out[name] = {"iterations": k.outer_iterations, "converged": k.converged, "flag": k.flag,
                      "res": k.final_true_residual, "s": time.perf_counter() - t0}
+    # FGMRES(64), and both solvers with the bench-default block-Jacobi M
+    sym = cfg in (1, 2, 4)
+    kind = "ic0" if sym else "ilu0"
+    a = f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values)
+    for label, M in (("identity", f.IdentityPrecond(p.n)),
+                     (kind, f.BlockJacobiIlu0.factorize(a, f.IluConfig(4, 1.0, sym, f.Precision.P64)))):
+        f.fgmres_restarted(reps, M, p.b, 64, f.FgmresOptions(tol=TOL))  # warm-up
+        t0 = time.perf_counter()
+        k = f.fgmres_restarted(reps, M, p.b, 64, f.FgmresOptions(tol=TOL))
+        out[f"fgmres64/{label}"] = {"iterations": k.outer_iterations, "converged": k.converged, "flag": k.flag,
+                                    "res": k.final_true_residual, "s": time.perf_counter() - t0}
+    M16 = f.BlockJacobiIlu0.factorize(a, f.IluConfig(4, 1.0, sym, f.Precision.P16))
+    spec_m = SPEC.rsplit(">", 1)[0] + f"> {kind}(blocks=4,alpha=1,prec=f16)"
+    sm = f.build(f.parse_solver_spec(spec_m), reps, M16)
+    sm.reset(); sm.run(b, f.RunOptions(tol=TOL))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sm.reset(); r = sm.run(b, f.RunOptions(tol=TOL), want_x=False).report
+    torch.cuda.synchronize()
+    out[f"f3r16/{kind}"] = {"outer": r.outer_iterations, "res": r.final_true_residual, "s": time.perf_counter() - t0}
     print(json.dumps(out), flush=True)
