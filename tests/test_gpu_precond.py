@@ -202,15 +202,17 @@ def _recorded(key):
     return d[key]
 
 
-@pytest.mark.parametrize("cfg", [1, 2])
-def test_bench_default_ic0_vs_reference_run(cuda, cfg):
-    """BASELINE configs 1/2 with the reference bench's default M (IC(0), 4 blocks, fp16)"""
+@pytest.mark.parametrize("cfg,kind", [(1, "ic0"), (2, "ic0"), (3, "ilu0"), (5, "ilu0")])
+def test_bench_default_m_vs_reference_run(cuda, cfg, kind):
+    """BASELINE configs with the reference bench's default M (IC(0) on the symmetric
+    ones, ILU(0) otherwise; 4 blocks, fp16) against the UNMODIFIED reference's
+    recorded full runs (tests/golden/reference_runs.json)"""
     import paper_2505_20719_b200 as f
     from paper_2505_20719_b200 import problems
-    ref = _recorded(f"config{cfg}/fp16-f3r-ic0")
+    ref = _recorded(f"config{cfg}/fp16-f3r-{kind}")
     p = problems.problem(cfg)
-    spec = "F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > ic0(blocks=4,alpha=1,prec=f16)"
-    M = f.BlockJacobiIlu0.factorize(_csr(p), f.IluConfig(4, 1.0, True, f.Precision.P16))
+    spec = f"F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > {kind}(blocks=4,alpha=1,prec=f16)"
+    M = f.BlockJacobiIlu0.factorize(_csr(p), f.IluConfig(4, 1.0, kind == "ic0", f.Precision.P16))
     rep = f.build(f.parse_solver_spec(spec), f.make_replicas(_csr(p)), M).run(p.b, f.RunOptions(tol=TOL)).report
     assert rep.converged and rep.final_true_residual <= TOL
     assert abs(rep.outer_iterations - ref["outer_iterations"]) <= max(1, round(0.1 * ref["outer_iterations"]))
