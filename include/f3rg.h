@@ -194,13 +194,18 @@ int f3rg_richardson_apply(f3rg_richardson* r, const void* v, void* z, uintptr_t 
 int f3rg_richardson_set_precond(f3rg_richardson* r, const f3rg_precond* m);
 
 /* ---- the reference's fp64 competitor solvers (src/cg.cpp:22-171: cg_solve,
- *      bicgstab_solve) with M = identity, on the device. which: 0 = CG, 1 = BiCGStab.
+ *      bicgstab_solve) on the device; f3rg_krylov_solve: M = identity. which: 0 = CG, 1 = BiCGStab.
  *      b, x: HOST fp64 arrays (x may be NULL). history (optional, hist_cap entries)
  *      receives the relative residuals, entry 0 = 1 (ConvergenceReport semantics).
  *      CG on an indefinite operator returns F3RG_ESOLVER, as the reference throws
  *      SolverError; breakdown / cap are report flags ("breakdown", "capped"). */
 int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* b_host, double* x_host, double tol,
                       uint64_t max_precond_invocations, f3rg_report* rep, double* history, uint64_t hist_cap);
+/* the same with the preconditioner M (cg_solve / bicgstab_solve(a, M, b, opts)): m from
+ * f3rg_ilu_factorize / f3rg_precond_identity, NULL = identity */
+int f3rg_krylov_solve_m(const f3rg_matrix* a, const f3rg_precond* m, int which, const double* b_host, double* x_host,
+                        double tol, uint64_t max_precond_invocations, f3rg_report* rep, double* history,
+                        uint64_t hist_cap);
 
 /* ---- the reference's restarted fp64 FGMRES(m) with a terminal preconditioner
  *      (src/fgmres.cpp:163-222: fgmres_restarted; the bench's "fgmres64"). Cycles of

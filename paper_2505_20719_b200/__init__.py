@@ -120,6 +120,7 @@ def lib():
     L.f3rg_solver_omega_count.restype = u64
     L.f3rg_solver_omega_count.argtypes = [vp]
     L.f3rg_krylov_solve.argtypes = [vp, i32, vp, vp, dbl, u64, C.POINTER(_Report), vp, u64]
+    L.f3rg_krylov_solve_m.argtypes = [vp, vp, i32, vp, vp, dbl, u64, C.POINTER(_Report), vp, u64]
     # row-block partition (partition.py)
     L.f3rg_part_plan.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     L.f3rg_comm_local.argtypes = [C.POINTER(vp), vp, i32]
@@ -676,7 +677,7 @@ class ReferenceSolveOptions:
     max_precond_invocations: int = 19200
 
 
-def _krylov_solve(which: int, a, m: IdentityPrecond, b, opts: ReferenceSolveOptions, x_out=None):
+def _krylov_solve(which: int, a, m: Preconditioner, b, opts: ReferenceSolveOptions, x_out=None):
     dev = a.dev if isinstance(a, (PrecisionReplicas, ReplicaView)) else _DeviceMatrix(a)
     n = dev.n
     if m.rows() != n:
@@ -688,22 +689,23 @@ def _krylov_solve(which: int, a, m: IdentityPrecond, b, opts: ReferenceSolveOpti
         raise DimensionError("x_out must be an fp64 array of length n")
     r = _Report()
     hist = np.zeros(int(opts.max_precond_invocations) + 2)
-    _check(lib().f3rg_krylov_solve(dev.h, which, b.ctypes.data, x_out.ctypes.data if x_out is not None else None,
-                                   float(opts.tol), int(opts.max_precond_invocations), C.byref(r), hist.ctypes.data,
-                                   hist.size))
+    _check(lib().f3rg_krylov_solve_m(dev.h, None if isinstance(m, IdentityPrecond) else m._handle(), which,
+                                     b.ctypes.data, x_out.ctypes.data if x_out is not None else None,
+                                     float(opts.tol), int(opts.max_precond_invocations), C.byref(r),
+                                     hist.ctypes.data, hist.size))
     return ConvergenceReport(bool(r.converged), int(r.outer_iterations), int(r.precond_invocations), [],
                              list(hist[:r.n_history]), r.final_true_residual, r.wall_seconds, [], r.flag.decode(),
                              "cg" if which == 0 else "bicgstab")
 
 
-def cg_solve(a, m: IdentityPrecond, b, opts: ReferenceSolveOptions = ReferenceSolveOptions(), x_out=None):
+def cg_solve(a, m: Preconditioner, b, opts: ReferenceSolveOptions = ReferenceSolveOptions(), x_out=None):
     """reference cg_solve (include/f3r/cg.hpp:21-22, src/cg.cpp:22-75): fp64
-    preconditioned CG, M = identity, on the device. Raises SolverError on an
+    preconditioned CG on the device, M = identity or a BlockJacobiIlu0. Raises SolverError on an
     indefinite operator, as the reference. `x_out` optionally receives x."""
     return _krylov_solve(0, a, m, b, opts, x_out)
 
 
-def bicgstab_solve(a, m: IdentityPrecond, b, opts: ReferenceSolveOptions = ReferenceSolveOptions(), x_out=None):
+def bicgstab_solve(a, m: Preconditioner, b, opts: ReferenceSolveOptions = ReferenceSolveOptions(), x_out=None):
     """reference bicgstab_solve (include/f3r/cg.hpp:28-30, src/cg.cpp:77-171)."""
     return _krylov_solve(1, a, m, b, opts, x_out)
 

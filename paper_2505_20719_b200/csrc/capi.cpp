@@ -563,12 +563,13 @@ extern "C" int f3rg_fgmres_solve(const f3rg_matrix* a, const f3rg_precond* m, in
 }
 
 // ---- fp64 CG / BiCGStab -------------------------------------------------------------
-extern "C" int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* b_host, double* x_host, double tol,
-                                 uint64_t max_precond, f3rg_report* rep, double* history, uint64_t hist_cap) {
+extern "C" int f3rg_krylov_solve_m(const f3rg_matrix* a, const f3rg_precond* m, int which, const double* b_host,
+                                   double* x_host, double tol, uint64_t max_precond, f3rg_report* rep,
+                                   double* history, uint64_t hist_cap) {
   return guarded([&] {
     if (!a || !b_host) throw Error(ERR_DIMENSION, "null argument");
     const uint64_t n = a->m->rows();
-    KrylovSolver ks(a->m);
+    KrylovSolver ks(a->m, m ? m->p : nullptr);
     DevBuf b(n * 8 + 16), x(n * 8 + 16);
     F3RG_CUDA(cudaMemcpy(b.get(), b_host, n * 8, cudaMemcpyHostToDevice));
     const Report r = ks.solve(which, b.get<double>(), x.get<double>(), tol, max_precond, nullptr);
@@ -577,6 +578,11 @@ extern "C" int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* 
     for (uint64_t i = 0; history && i < r.residual_history.size() && i < hist_cap; ++i)
       history[i] = r.residual_history[i];
   });
+}
+
+extern "C" int f3rg_krylov_solve(const f3rg_matrix* a, int which, const double* b_host, double* x_host, double tol,
+                                 uint64_t max_precond, f3rg_report* rep, double* history, uint64_t hist_cap) {
+  return f3rg_krylov_solve_m(a, nullptr, which, b_host, x_host, tol, max_precond, rep, history, hist_cap);
 }
 
 // ---- row-block partition ----------------------------------------

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 
@@ -849,7 +850,9 @@ std::vector<unsigned long long> Solver::level_invocations() {
 // ---- fp64 CG / BiCGStab (reference src/cg.cpp:22-171) ---------------------------------
 namespace f3rg {
 
-KrylovSolver::KrylovSolver(std::shared_ptr<DeviceMatrix> a) : a_(std::move(a)), n_(a_->rows()) {
+KrylovSolver::KrylovSolver(std::shared_ptr<DeviceMatrix> a, std::shared_ptr<const DevicePrecond> m)
+    : a_(std::move(a)), n_(a_->rows()), M_(std::move(m)) {
+  if (M_ && M_->rows() != n_) throw Error(ERR_DIMENSION, "preconditioner size does not match the matrix");
   F3RG_CUDA(cudaStreamCreateWithFlags(&own_, cudaStreamNonBlocking));
   for (DevBuf* b : {&x_, &r_, &p_, &q_, &s_, &t_, &rhat_, &tmp_}) b->alloc(n_ * 8 + 16);
   state_.alloc(sizeof(KState));
@@ -858,6 +861,13 @@ KrylovSolver::KrylovSolver(std::shared_ptr<DeviceMatrix> a) : a_(std::move(a)), 
   norm_.alloc(64);
   F3RG_CUDA(cudaMemset(counter_.get(), 0, counter_.bytes()));
   F3RG_CUDA(cudaHostAlloc((void**)&stage_host_, 4096, cudaHostAllocDefault));
+  if (has_m()) {  // z = M r (CG), phat / shat (BiCGStab: phat in z_)
+    z_.alloc(n_ * 8 + 16);
+    shat_.alloc(n_ * 8 + 16);
+    work_ = M_->make_work();
+    work_->prepare(M_->compute_prec(2), own_);
+    F3RG_CUDA(cudaStreamSynchronize(own_));
+  }
 }
 
 KrylovSolver::~KrylovSolver() {
@@ -909,9 +919,14 @@ Report KrylovSolver::solve(int which, const double* b, double* x_out, double tol
   h.max_precond = max_precond;
   h.hist_cap = cap;
   h.hist = hist_.get<double>();
-  if (which == 0) {  // z = M r = r, p = z, rz = (r, z)
-    F3RG_CUDA(cudaMemcpyAsync(p_.get(), r_.get(), n * 8, cudaMemcpyDeviceToDevice, s));
-    F3RG_CUDA(launch_dot(2, 2, 2, Launch{0, s}, r_.get(), r_.get(), n, norm_.get<double>(), sync));
+  if (which == 0) {  // z = M r, p = z, rz = (r, z) (src/cg.cpp:41-44)
+    const void* z0 = r_.get();
+    if (has_m()) {
+      M_->enqueue(*work_, r_.get(), 2, z_.get(), 2, s, nullptr, 0, nullptr);
+      z0 = z_.get();
+    }
+    F3RG_CUDA(cudaMemcpyAsync(p_.get(), z0, n * 8, cudaMemcpyDeviceToDevice, s));
+    F3RG_CUDA(launch_dot(2, 2, 2, Launch{0, s}, r_.get(), z0, n, norm_.get<double>(), sync));
     read(norm_.get(), 8);
     h.rz = stage_host_[0];
     h.precond = 1;
@@ -928,21 +943,40 @@ Report KrylovSolver::solve(int which, const double* b, double* x_out, double tol
   double* r = r_.get<double>();
   double* p = p_.get<double>();
   double* v = q_.get<double>();  // CG: q; BiCGStab: v
-  const int batch = 8;           // iterations enqueued per host synchronisation
+  // M's sweeps are gated on the solver's stop flag like every kernel of a batch
+  const int* stop = reinterpret_cast<const int*>(reinterpret_cast<const char*>(S) + offsetof(KState, stop));
+  auto apply_m = [&](const double* in, double* out) {
+    M_->enqueue(*work_, in, 2, out, 2, s, stop, 1, nullptr);
+  };
+  // CG after its checks: z = M r, rz', beta (src/cg.cpp:69-72), then p = z + beta p
+  auto cg_next = [&]() {
+    if (has_m()) {
+      apply_m(r, z_.get<double>());
+      F3RG_CUDA(launch_cg_rz(Launch{0, s}, r, z_.get<double>(), n, S, sync));
+      F3RG_CUDA(launch_cg_p(Launch{0, s}, p, z_.get<double>(), n, S));
+    } else {
+      F3RG_CUDA(launch_cg_next(Launch{0, s}, S));
+      F3RG_CUDA(launch_cg_p(Launch{0, s}, p, r, n, S));
+    }
+  };
+  double* phat = has_m() ? z_.get<double>() : p;
+  double* shat = has_m() ? shat_.get<double>() : s_.get<double>();
+  const int batch = 8;  // iterations enqueued per host synchronisation
   for (;;) {
     for (int k = 0; k < batch; ++k) {
       if (which == 0) {
         F3RG_CUDA(launch_cg_spmv(Launch{0, s}, A, T, p, v, S, sync));
         F3RG_CUDA(launch_cg_update(Launch{0, s}, x, r, p, v, n, S, sync));
-        F3RG_CUDA(launch_cg_next(Launch{0, s}, S));
-        F3RG_CUDA(launch_cg_p(Launch{0, s}, p, r, n, S));
+        cg_next();
       } else {
         F3RG_CUDA(launch_bi_rho(Launch{0, s}, rhat_.get<double>(), r, n, S, sync));
         F3RG_CUDA(launch_bi_p(Launch{0, s}, p, v, r, n, S));
-        F3RG_CUDA(launch_bi_v(Launch{0, s}, A, T, p, v, rhat_.get<double>(), S, sync));
+        if (has_m()) apply_m(p, phat);  // phat = M p (src/cg.cpp:120)
+        F3RG_CUDA(launch_bi_v(Launch{0, s}, A, T, phat, v, rhat_.get<double>(), S, sync));
         F3RG_CUDA(launch_bi_s(Launch{0, s}, s_.get<double>(), r, v, n, S));
-        F3RG_CUDA(launch_bi_t(Launch{0, s}, A, T, s_.get<double>(), t_.get<double>(), S, sync));
-        F3RG_CUDA(launch_bi_update(Launch{0, s}, x, r, p, s_.get<double>(), t_.get<double>(), n, S, sync));
+        if (has_m()) apply_m(s_.get<double>(), shat);  // shat = M s (:131)
+        F3RG_CUDA(launch_bi_t(Launch{0, s}, A, T, s_.get<double>(), shat, t_.get<double>(), S, sync));
+        F3RG_CUDA(launch_bi_update(Launch{0, s}, x, r, phat, s_.get<double>(), shat, t_.get<double>(), n, S, sync));
       }
     }
     read(S, sizeof h);
@@ -957,10 +991,7 @@ Report KrylovSolver::solve(int which, const double* b, double* x_out, double tol
       }
       // the reference carries on with the iteration (cap test, then CG's z/rz/beta/p)
       F3RG_CUDA(launch_krylov_resume(Launch{0, s}, S));
-      if (which == 0) {
-        F3RG_CUDA(launch_cg_next(Launch{0, s}, S));
-        F3RG_CUDA(launch_cg_p(Launch{0, s}, p, r, n, S));
-      }
+      if (which == 0) cg_next();
       continue;
     }
     if (h.stop == KS_INDEFINITE) throw Error(ERR_SOLVER, "cg: indefinite operator detected");

@@ -343,10 +343,11 @@ class Solver {
   std::vector<std::unique_ptr<ProfRec>> prof_;
 };
 
-// ---- fp64 competitor solvers (reference src/cg.cpp:22-171), M = identity ------------
+// ---- fp64 competitor solvers (reference src/cg.cpp:22-171), M = identity or block-Jacobi ----
 class KrylovSolver {
  public:
-  explicit KrylovSolver(std::shared_ptr<DeviceMatrix> a);
+  // m: the preconditioner (null = IdentityPrecond)
+  explicit KrylovSolver(std::shared_ptr<DeviceMatrix> a, std::shared_ptr<const DevicePrecond> m = nullptr);
   ~KrylovSolver();
   KrylovSolver(const KrylovSolver&) = delete;
   KrylovSolver& operator=(const KrylovSolver&) = delete;
@@ -360,7 +361,10 @@ class KrylovSolver {
   double true_rel(const double* b, double bnorm, cudaStream_t s);
   std::shared_ptr<DeviceMatrix> a_;
   uint64_t n_ = 0;
-  DevBuf x_, r_, p_, q_, s_, t_, rhat_, tmp_, hist_, state_, partials_, counter_, norm_;
+  DevBuf x_, r_, p_, q_, s_, t_, rhat_, tmp_, hist_, state_, partials_, counter_, norm_, z_, shat_;
+  std::shared_ptr<const DevicePrecond> M_;
+  std::unique_ptr<SweepWork> work_;
+  bool has_m() const { return M_ && !M_->identity(); }
   double* stage_host_ = nullptr;
   cudaStream_t own_ = nullptr;
 };

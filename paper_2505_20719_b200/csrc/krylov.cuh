@@ -1,5 +1,6 @@
 // krylov.cuh -- the reference's fp64 competitor solvers on the device (reference
-// src/cg.cpp:22-171: cg_solve, bicgstab_solve) with M = identity, on the same SpMV
+// src/cg.cpp:22-171: cg_solve, bicgstab_solve) with M = identity or a block-Jacobi
+// ILU(0)/IC(0) (its sweeps run between these kernels, trsv.cuh), on the same SpMV
 // engine. Every scalar recurrence (alpha, beta, rho, omega, breakdown and stop
 // tests) runs in the last CTA of the kernel that completes its reduction, so the
 // host enqueues a batch of iterations and synchronises once per batch; a stop
@@ -115,7 +116,26 @@ __global__ void k_cg_next(KState* S) {
   S->rz = S->rr;
 }
 
-// p = z + beta p (add_scaled(z, beta, p, p), z = r)
+// with M: rz' = (r, z), z = M r computed by the sweeps; beta = rz'/rz (src/cg.cpp:69-72)
+__global__ void __launch_bounds__(256) k_cg_rz(const double* r, const double* z, uint64_t n, KState* S, Sync sync) {
+  pdl_wait();
+  __shared__ double scratch[64];
+  __shared__ double tot[1];
+  if (S->stop) return;
+  double v[1] = {0.0};
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    v[0] = __dadd_rn(v[0], __dmul_rn(r[i], z[i]));
+  pdl_trigger();
+  if (!reduce_f64<1>(v, sync, scratch, tot)) return;
+  if (threadIdx.x == 0) {
+    S->precond += 1;
+    S->beta = __ddiv_rn(tot[0], S->rz);
+    S->rz = tot[0];
+  }
+}
+
+// p = z + beta p (add_scaled(z, beta, p, p); z = r when M = identity)
 __global__ void __launch_bounds__(256) k_cg_p(double* p, const double* r, uint64_t n, const KState* S) {
   pdl_wait();
   if (S->stop) return;
@@ -205,14 +225,14 @@ __global__ void __launch_bounds__(256) k_bi_s(double* s, const double* r, const 
 // shat = M s = s; t = A shat; omega = (t, s) / (t, t), or the t = 0 cases
 // (src/cg.cpp:131-147)
 template <int IDX>
-__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_bi_t(CsrDev A, TilesDev T, const double* s, double* t,
-                                                            KState* S, Sync sync) {
+__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_bi_t(CsrDev A, TilesDev T, const double* s,
+                                                            const double* shat, double* t, KState* S, Sync sync) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ double scratch[64 * 3];
   __shared__ double tot[3];
   if (S->stop) return;
-  GatherPlain<P64, P64> g{s};
+  GatherPlain<P64, P64> g{shat};
   EpiBiT e{s, t, 0.0, 0.0, 0.0, 0.0};
   spmv_tiles<P64, P64, IDX>(A, T, g, e, smem);
   double d[3] = {e.tt, e.ts, e.ss};
@@ -231,7 +251,8 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_bi_t(CsrDev A, TilesDev
 
 // x += alpha phat; x += omega shat; r = s - omega t; ||r|| (src/cg.cpp:148-160)
 __global__ void __launch_bounds__(256) k_bi_update(double* x, double* r, const double* p, const double* s,
-                                                   const double* t, uint64_t n, KState* S, Sync sync) {
+                                                   const double* shat, const double* t, uint64_t n, KState* S,
+                                                   Sync sync) {
   pdl_wait();
   __shared__ double scratch[64];
   __shared__ double tot[1];
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(256) k_bi_update(double* x, double* r, const d
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const double si = s[i];
     double xi = __dadd_rn(__dmul_rn(a, p[i]), x[i]);
-    x[i] = __dadd_rn(__dmul_rn(w, si), xi);
+    x[i] = __dadd_rn(__dmul_rn(w, shat[i]), xi);
     const double ri = __dadd_rn(si, __dmul_rn(nw, t[i]));
     r[i] = ri;
     v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));

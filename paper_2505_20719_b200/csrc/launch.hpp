@@ -108,16 +108,17 @@ cudaError_t launch_cg_spmv(Launch l, const CsrDev& A, const TilesDev& T, const d
 cudaError_t launch_cg_update(Launch l, double* x, double* r, const double* p, const double* q, uint64_t n, KState* S,
                              SyncH sync);
 cudaError_t launch_cg_next(Launch l, KState* S);
+cudaError_t launch_cg_rz(Launch l, const double* r, const double* z, uint64_t n, KState* S, SyncH sync);
 cudaError_t launch_cg_p(Launch l, double* p, const double* r, uint64_t n, const KState* S);
 cudaError_t launch_bi_rho(Launch l, const double* rhat, const double* r, uint64_t n, KState* S, SyncH sync);
 cudaError_t launch_bi_p(Launch l, double* p, const double* v, const double* r, uint64_t n, const KState* S);
 cudaError_t launch_bi_v(Launch l, const CsrDev& A, const TilesDev& T, const double* p, double* v, const double* rhat,
                         KState* S, SyncH sync);
 cudaError_t launch_bi_s(Launch l, double* s, const double* r, const double* v, uint64_t n, const KState* S);
-cudaError_t launch_bi_t(Launch l, const CsrDev& A, const TilesDev& T, const double* s, double* t, KState* S,
-                        SyncH sync);
-cudaError_t launch_bi_update(Launch l, double* x, double* r, const double* p, const double* s, const double* t,
-                             uint64_t n, KState* S, SyncH sync);
+cudaError_t launch_bi_t(Launch l, const CsrDev& A, const TilesDev& T, const double* s, const double* shat, double* t,
+                        KState* S, SyncH sync);
+cudaError_t launch_bi_update(Launch l, double* x, double* r, const double* p, const double* s, const double* shat,
+                             const double* t, uint64_t n, KState* S, SyncH sync);
 cudaError_t launch_krylov_resume(Launch l, KState* S);
 
 // ---- BLAS-1 / SpMV (kernel-level entry points) ----------------------------------

@@ -39,6 +39,10 @@ cudaError_t launch_cg_update(Launch l, double* x, double* r, const double* p, co
 
 cudaError_t launch_cg_next(Launch l, KState* S) { return launch_k1(k_cg_next, l.stream, S); }
 
+cudaError_t launch_cg_rz(Launch l, const double* r, const double* z, uint64_t n, KState* S, SyncH sync) {
+  return launch_k(k_cg_rz, red_grid(), 0, l.stream, r, z, n, S, to_sync(sync));
+}
+
 cudaError_t launch_cg_p(Launch l, double* p, const double* r, uint64_t n, const KState* S) {
   return launch_k(k_cg_p, stream_grid(), 0, l.stream, p, r, n, S);
 }
@@ -68,22 +72,22 @@ cudaError_t launch_bi_s(Launch l, double* s, const double* r, const double* v, u
   return launch_k(k_bi_s, stream_grid(), 0, l.stream, s, r, v, n, S);
 }
 
-cudaError_t launch_bi_t(Launch l, const CsrDev& A, const TilesDev& T, const double* s, double* t, KState* S,
-                        SyncH sync) {
+cudaError_t launch_bi_t(Launch l, const CsrDev& A, const TilesDev& T, const double* s, const double* shat, double* t,
+                        KState* S, SyncH sync) {
   cudaError_t err = cudaSuccess;
   with_idx64(A, [&](auto I) {
     constexpr int IDX = decltype(I)::value;
     constexpr int SM = TileCfg<P64, IDX>::SMEM_BYTES;
     auto kern = k_bi_t<IDX>;
     static const int occ = occupancy_blocks(kern, SM);  // also sets the dynamic smem limit
-    err = launch_k(kern, tile_grid(occ, T.ntiles), SM, l.stream, A, T, s, t, S, to_sync(sync));
+    err = launch_k(kern, tile_grid(occ, T.ntiles), SM, l.stream, A, T, s, shat, t, S, to_sync(sync));
   });
   return err;
 }
 
-cudaError_t launch_bi_update(Launch l, double* x, double* r, const double* p, const double* s, const double* t,
-                             uint64_t n, KState* S, SyncH sync) {
-  return launch_k(k_bi_update, red_grid(), 0, l.stream, x, r, p, s, t, n, S, to_sync(sync));
+cudaError_t launch_bi_update(Launch l, double* x, double* r, const double* p, const double* s, const double* shat,
+                             const double* t, uint64_t n, KState* S, SyncH sync) {
+  return launch_k(k_bi_update, red_grid(), 0, l.stream, x, r, p, s, shat, t, n, S, to_sync(sync));
 }
 
 cudaError_t launch_krylov_resume(Launch l, KState* S) { return launch_k1(k_krylov_resume, l.stream, S); }

@@ -130,3 +130,32 @@ def test_fgmres_capped_like_reference(cases, reference):
                                  max_precond=40, restart=16)
     assert rep.flag == ref.flag == "capped" and not rep.converged
     assert rep.precond_invocations == ref.precond_invocations == 40
+
+
+@pytest.mark.parametrize("which", ["cg", "bicgstab"])
+@pytest.mark.parametrize("prec", [2, 0])
+def test_preconditioned_krylov_matches_reference(cases, reference, which, prec):
+    """cg_solve / bicgstab_solve with the reference bench's block-Jacobi M (IC(0) on the
+    symmetric problems, ILU(0) otherwise; 4 blocks; fp64 or fp16 factors)"""
+    import paper_2505_20719_b200 as f
+    reference.set_threads(0)
+    sym = {"poisson24", "hpcg16", "aniso16"}
+    for name, p in cases:
+        if which == "cg" and name not in sym:
+            continue
+        a = f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values)
+        ref_m = reference.matrix(p.row_ptr, p.col_idx, p.values)
+        M = f.BlockJacobiIlu0.factorize(a, f.IluConfig(4, 1.0, name in sym, f.Precision(prec)))
+        RM = reference.ilu(ref_m, 4, 1.0, name in sym, prec)
+        x = np.zeros(p.n)
+        solve = f.cg_solve if which == "cg" else f.bicgstab_solve
+        rep = solve(f.make_replicas(a), M, p.b, f.ReferenceSolveOptions(tol=TOL), x_out=x)
+        ref = reference.krylov_solve(ref_m, which, p.b, tol=TOL, precond=RM)
+        assert rep.converged == ref.converged, (name, rep.flag, ref.flag)
+        want = ref.outer_iterations
+        assert abs(rep.outer_iterations - want) <= max(1, round(0.1 * want)), (name, rep.outer_iterations, want)
+        assert rep.precond_invocations == ref.precond_invocations or abs(rep.outer_iterations - want) > 0
+        if rep.converged:
+            assert rep.final_true_residual < TOL
+        k = min(8, want, rep.outer_iterations)
+        assert np.allclose(rep.residual_history[:k + 1], ref.residual_history[:k + 1], rtol=1e-6), name

@@ -1,9 +1,9 @@
 """fp16-F3R against the reference's fp64 competitor solvers on the device, BASELINE
 configs: outer/iteration counts and time-to-solution (the paper's comparison, on
-B200). CG and BiCGStab with M = identity; FGMRES(64) (fgmres_restarted) and
-fp16-F3R with M = identity and with the reference bench's block-Jacobi default
+B200). CG, BiCGStab, FGMRES(64) (fgmres_restarted) and fp16-F3R, each with
+M = identity and with the reference bench's block-Jacobi default
 (IC(0) on symmetric problems, ILU(0) otherwise; 4 blocks; fp16 factors for F3R,
-fp64 for FGMRES(64) as src/bench.cpp:171-177 resolves them).
+fp64 for the fp64 solvers, as src/bench.cpp:171-177 resolves them).
 
     python tools/competitors.py [configs...]      (default: 1 2 3 4)
 """
@@ -47,8 +47,16 @@ for cfg in [int(c) for c in sys.argv[1:]] or [1, 2, 3, 4]:
     sym = cfg in (1, 2, 4)
     kind = "ic0" if sym else "ilu0"
     a = f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values)
-    for label, M in (("identity", f.IdentityPrecond(p.n)),
-                     (kind, f.BlockJacobiIlu0.factorize(a, f.IluConfig(4, 1.0, sym, f.Precision.P64)))):
+    M64 = f.BlockJacobiIlu0.factorize(a, f.IluConfig(4, 1.0, sym, f.Precision.P64))
+    for name, solve in (("cg", f.cg_solve), ("bicgstab", f.bicgstab_solve)):
+        if name == "cg" and not sym:
+            continue
+        solve(reps, M64, p.b, f.ReferenceSolveOptions(tol=TOL))  # warm-up
+        t0 = time.perf_counter()
+        k = solve(reps, M64, p.b, f.ReferenceSolveOptions(tol=TOL))
+        out[f"{name}/{kind}"] = {"iterations": k.outer_iterations, "converged": k.converged, "flag": k.flag,
+                                 "res": k.final_true_residual, "s": time.perf_counter() - t0}
+    for label, M in (("identity", f.IdentityPrecond(p.n)), (kind, M64)):
         f.fgmres_restarted(reps, M, p.b, 64, f.FgmresOptions(tol=TOL))  # warm-up
         t0 = time.perf_counter()
         k = f.fgmres_restarted(reps, M, p.b, 64, f.FgmresOptions(tol=TOL))
