@@ -274,6 +274,19 @@ def run_partitioned(args):
         e2e_t.append(time.perf_counter() - t0)
     e2 = torch.tensor([float(np.mean(e2e_t))], device="cuda")
     dist.all_reduce(e2, op=dist.ReduceOp.MAX)
+    # per-kernel timing of one eager solve on every rank (the exchanges pair up):
+    # launch count and the top kernel's roofline, rank 0's
+    part.solver.set_profile(True)
+    part.reset()
+    part.run(b_own, x_own, opts, sp)
+    part.solver.set_profile(False)
+    prof = part.solver.profile()
+    launches = int(sum(k[2] for k in prof))
+    streaming = [k for k in prof if k[3] > 0]
+    top = max(streaming, key=lambda k: k[1])
+    peak, peak_kind = _peaks()
+    per_launch_ms = top[1] / top[2]
+    gbs = top[3] / top[2] / (per_launch_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
@@ -282,7 +295,11 @@ def run_partitioned(args):
         "outer_iterations": rep.outer_iterations, "final_true_residual": rep.final_true_residual,
         "e2e": {"value": float(e2.item()), "unit": "s", "h2d_bytes_per_step": int(p.n * 8),
                 "d2h_bytes_per_step": int(p.n * 8)},
-        "gpu_launches": None, "clocks": clk.summary(),
+        "gpu_launches": launches * args.steps, "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "kernel": top[0], "achieved": round(gbs, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
+                     "bytes": "streamed bytes of rank 0's rows (its ext-layout CSR)",
+                     "avg_launch_us": per_launch_ms * 1e3},
         "partition": {"rows_rank0": pl.r1 - pl.r0, "halo_rank0": pl.n_lo + pl.n_hi},
     }
     if rank == 0:
