@@ -124,7 +124,10 @@ __device__ __forceinline__ unsigned next_epoch(unsigned e0) {
   return e;
 }
 
-constexpr int kSweepChunk = 16;  // entries in flight per lane (a 27-point row: one round)
+#ifndef F3RG_SWEEP_CHUNK
+#define F3RG_SWEEP_CHUNK 16
+#endif
+constexpr int kSweepChunk = F3RG_SWEEP_CHUNK;  // entries in flight per lane (a 27-point row: one round)
 
 // Process this warp's slices. init(row) -> T_<C> starting value; epi(row, value)
 // after the row is published.
