@@ -93,6 +93,25 @@ uint64_t f3rg_matrix_nnz(const f3rg_matrix* a);
 /* replica values widened to fp64 into host memory (nnz doubles) */
 int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host);
 
+/* ---- problem setup -------------------------------------------
+ * f3rg_matrix_create_scaled: diagonal_scale(A, b) (src/scaling.cpp:11-38) computed on
+ * the device from the UNSCALED fp64 CSR -- d_i = 1/sqrt|a_ii|, a~_ij = (a_ij d_i) d_j,
+ * b~ = b d, bit-identical to the reference -- and the replicas of the scaled matrix.
+ * b_host / b_scaled_host / d_host (n each) are optional. F3RG_EFACTORIZATION on a
+ * missing or zero diagonal, with the reference's message. */
+int f3rg_matrix_create_scaled(f3rg_matrix** out, const f3rg_csr* a64, const double* b_host, double* b_scaled_host,
+                              double* d_host);
+/* Matrix Market coordinate files (read_matrix_market / write_matrix_market,
+ * src/matrix_market.cpp:33-127): real / integer / pattern, general / symmetric;
+ * F3RG_EPARSE with the reference's messages. The host CSR is owned by the handle;
+ * f3rg_host_csr_view points an f3rg_csr at its arrays. */
+typedef struct f3rg_host_csr f3rg_host_csr;
+int f3rg_read_matrix_market(const char* path, f3rg_host_csr** out);
+int f3rg_host_csr_view(const f3rg_host_csr* h, f3rg_csr* view);
+uint64_t f3rg_host_csr_nnz(const f3rg_host_csr* h);
+void f3rg_host_csr_destroy(f3rg_host_csr* h);
+int f3rg_write_matrix_market(const char* path, const f3rg_csr* a64);
+
 /* ---- solver spec grammar (replaces parse_solver_spec / SolverSpec::to_string,
  *      src/solver_spec.cpp:147-212) */
 int f3rg_spec_canonical(const char* spec, char* out, size_t cap);

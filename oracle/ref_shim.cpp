@@ -16,6 +16,7 @@
 // representable at the stated precision (0 = f16, 1 = f32, 2 = f64).
 
 #include <chrono>
+#include <fstream>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -30,6 +31,7 @@
 #include "f3r/dense_vector.hpp"
 #include "f3r/fgmres.hpp"
 #include "f3r/ilu.hpp"
+#include "f3r/matrix_market.hpp"
 #include "f3r/nesting.hpp"
 #include "f3r/operator.hpp"
 #include "f3r/richardson.hpp"
@@ -460,6 +462,20 @@ int ref_krylov_solve_m(void* h, int which, void* precond, int restart, const dou
     std::strncpy(rep->flag, r.flag.c_str(), sizeof(rep->flag) - 1);
     std::strncpy(rep->id, r.solver_id.c_str(), sizeof(rep->id) - 1);
     (void)x_out;
+  });
+}
+
+// read_matrix_market(std::ifstream(path)) (src/matrix_market.cpp:33-113); call with
+// null arrays for n / nnz, then again with arrays
+int ref_read_matrix_market(const char* path, uint64_t* n, uint64_t* nnz, uint32_t* rp, uint32_t* ci, double* v) {
+  return guarded([&] {
+    std::ifstream in(path);
+    const f3r::SparseCsr a = f3r::read_matrix_market(in);
+    *n = a.rows();
+    *nnz = a.nnz();
+    if (rp) std::memcpy(rp, a.row_ptr().data(), (a.rows() + 1) * 4);
+    if (ci) std::memcpy(ci, a.col_idx().data(), a.nnz() * 4);
+    if (v) std::memcpy(v, a.values_as<double>().data(), a.nnz() * 8);
   });
 }
 

@@ -159,6 +159,13 @@ def lib():
     L.f3rg_ilu_factorize_host.argtypes = [C.POINTER(_Csr), C.POINTER(_IluCfg), C.POINTER(u64), C.POINTER(u64), vp, vp,
                                           vp, vp, vp, vp]
     L.f3rg_solver_create_m.argtypes = [C.POINTER(vp), vp, C.c_char_p, vp]
+    L.f3rg_matrix_create_scaled.argtypes = [C.POINTER(vp), C.POINTER(_Csr), vp, vp, vp]
+    L.f3rg_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(vp)]
+    L.f3rg_host_csr_view.argtypes = [vp, C.POINTER(_Csr)]
+    L.f3rg_host_csr_nnz.restype = u64
+    L.f3rg_host_csr_nnz.argtypes = [vp]
+    L.f3rg_host_csr_destroy.argtypes = [vp]
+    L.f3rg_write_matrix_market.argtypes = [C.c_char_p, C.POINTER(_Csr)]
     L.f3rg_fgmres_solve.argtypes = [vp, vp, i32, vp, vp, dbl, u64, C.POINTER(_Report), vp, u64]
     _lib = L
     return L
@@ -322,11 +329,14 @@ class SparseCsr:
 
 
 class _DeviceMatrix:
-    def __init__(self, a: SparseCsr):
+    def __init__(self, a: SparseCsr, handle=None):
         L = lib()
         self.h = C.c_void_p()
-        csr = _Csr(a.n, a.row_ptr.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data)
-        _check(L.f3rg_matrix_create(C.byref(self.h), C.byref(csr)))
+        if handle is not None:
+            self.h = handle
+        else:
+            csr = _Csr(a.n, a.row_ptr.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data)
+            _check(L.f3rg_matrix_create(C.byref(self.h), C.byref(csr)))
         self.n = a.n
         self.nnz_ = a.nnz()
 
@@ -362,9 +372,9 @@ class PrecisionReplicas:
     """reference PrecisionReplicas (include/f3r/csr.hpp:72-78): one device copy of the
     indices, fp64 / fp32 / fp16 value arrays (RNE demotions of a64)."""
 
-    def __init__(self, a64: SparseCsr):
+    def __init__(self, a64: SparseCsr, _dev=None):
         self.host = a64
-        self.dev = _DeviceMatrix(a64)
+        self.dev = _dev if _dev is not None else _DeviceMatrix(a64)
         self.a64 = ReplicaView(self.dev, Precision.P64)
         self.a32 = ReplicaView(self.dev, Precision.P32)
         self.a16 = ReplicaView(self.dev, Precision.P16)
@@ -378,6 +388,56 @@ class PrecisionReplicas:
 
 def make_replicas(a64: SparseCsr) -> PrecisionReplicas:
     return PrecisionReplicas(a64)
+
+
+@dataclass
+class ScaledSystem:
+    """reference ScaledSystem (include/f3r/scaling.hpp): the scaled matrix -- here its
+    device replicas --, the scaled right-hand side and d"""
+    replicas: PrecisionReplicas
+    rhs: np.ndarray
+    d: np.ndarray
+
+
+def diagonal_scale(a: SparseCsr, b) -> ScaledSystem:
+    """reference diagonal_scale(A, b) (src/scaling.cpp:11-38) computed on the device
+    from the unscaled matrix, bit-identical; the replicas are built from the scaled
+    values in the same pass. Raises FactorizationError on a missing / zero diagonal."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.size != a.n:
+        raise DimensionError("diagonal scaling: rhs length mismatch")
+    h = C.c_void_p()
+    bs, d = np.zeros(a.n), np.zeros(a.n)
+    csr = _Csr(a.n, a.row_ptr.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data)
+    _check(lib().f3rg_matrix_create_scaled(C.byref(h), C.byref(csr), b.ctypes.data, bs.ctypes.data, d.ctypes.data))
+    dev = _DeviceMatrix(a, handle=h)
+    vals = np.zeros(a.nnz())
+    _check(lib().f3rg_matrix_values(h, 2, vals.ctypes.data))
+    return ScaledSystem(PrecisionReplicas(SparseCsr(a.n, a.row_ptr, a.col_idx, vals), _dev=dev), bs, d)
+
+
+def read_matrix_market(path: str) -> SparseCsr:
+    """reference read_matrix_market (src/matrix_market.cpp:33-113); raises ParseError"""
+    L = lib()
+    h = C.c_void_p()
+    _check(L.f3rg_read_matrix_market(str(path).encode(), C.byref(h)))
+    try:
+        v = _Csr()
+        _check(L.f3rg_host_csr_view(h, C.byref(v)))
+        nnz = int(L.f3rg_host_csr_nnz(h))
+        n = int(v.n)
+        rp = np.ctypeslib.as_array(C.cast(v.row_ptr, C.POINTER(C.c_uint32)), shape=(n + 1,)).copy()
+        ci = np.ctypeslib.as_array(C.cast(v.col_idx, C.POINTER(C.c_uint32)), shape=(max(nnz, 1),))[:nnz].copy()
+        va = np.ctypeslib.as_array(C.cast(v.values, C.POINTER(C.c_double)), shape=(max(nnz, 1),))[:nnz].copy()
+        return SparseCsr(n, rp, ci, va)
+    finally:
+        L.f3rg_host_csr_destroy(h)
+
+
+def write_matrix_market(path: str, a: SparseCsr) -> None:
+    """reference write_matrix_market (src/matrix_market.cpp:115-127)"""
+    csr = _Csr(a.n, a.row_ptr.ctypes.data, a.col_idx.ctypes.data, a.values.ctypes.data)
+    _check(lib().f3rg_write_matrix_market(str(path).encode(), C.byref(csr)))
 
 
 def spmv(a: ReplicaView, x: DenseVector, y: DenseVector) -> None:
@@ -802,5 +862,6 @@ __all__ = [
     "BlockJacobiIlu0", "ilu_factorize_host", "SolverSpec", "parse_solver_spec",
     "canonical_spec", "F3rMode", "F3rConfig", "f3r_spec", "RunOptions", "ConvergenceReport", "RunResult",
     "ComposedSolver", "build", "build_f3r", "RichardsonState", "richardson_apply", "lib", "FgmresOptions",
-    "fgmres_restarted", "ReferenceSolveOptions", "cg_solve", "bicgstab_solve",
+    "fgmres_restarted", "ReferenceSolveOptions", "cg_solve", "bicgstab_solve", "ScaledSystem", "diagonal_scale",
+    "read_matrix_market", "write_matrix_market",
 ]

@@ -33,8 +33,8 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 CXX = "g++"
 
 CU_SRCS = ["launch_t16.cu", "launch_t32.cu", "launch_t64.cu", "launch_level.cu", "launch_rich.cu", "launch_blas.cu",
-           "launch_krylov.cu", "launch_precond.cu"]
-CPP_SRCS = ["engine.cpp", "spec.cpp", "capi.cpp", "problems.cpp", "partition.cpp", "exchange.cpp", "precond.cpp"]
+           "launch_krylov.cu", "launch_precond.cu", "launch_setup.cu"]
+CPP_SRCS = ["engine.cpp", "spec.cpp", "capi.cpp", "problems.cpp", "partition.cpp", "exchange.cpp", "precond.cpp", "mmio.cpp"]
 
 
 def _gomp_flags():

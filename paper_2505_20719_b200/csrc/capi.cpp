@@ -776,3 +776,29 @@ int f3rg_solve_part_device(f3rg_solver* s, const double* b_own, double* x_own, c
 }
 
 }  // extern "C"
+
+namespace f3rg {
+void set_last_error(const std::string& m) { g_err = m; }
+}  // namespace f3rg
+
+// ---- diagonal scaling on the device (reference diagonal_scale, src/scaling.cpp:11-38) ----
+extern "C" int f3rg_matrix_create_scaled(f3rg_matrix** out, const f3rg_csr* a, const double* b_host,
+                                         double* b_scaled_host, double* d_host) {
+  return guarded([&] {
+    if (!out || !a) throw Error(ERR_DIMENSION, "null argument");
+    const uint64_t n = a->n;
+    DevBuf d(n * 8 + 16);
+    auto h = std::make_unique<f3rg_matrix>();
+    DeviceMatrix::Scale sc;
+    sc.d_dev = d.get<double>();
+    h->m = std::make_shared<DeviceMatrix>(n, a->row_ptr, a->col_idx, a->values, sc);
+    if (b_host && b_scaled_host) {
+      DevBuf b(n * 8 + 16), bs(n * 8 + 16);
+      F3RG_CUDA(cudaMemcpy(b.get(), b_host, n * 8, cudaMemcpyHostToDevice));
+      F3RG_CUDA(launch_scale_rhs(Launch{}, b.get<double>(), d.get<double>(), bs.get<double>(), n));
+      F3RG_CUDA(cudaMemcpy(b_scaled_host, bs.get(), n * 8, cudaMemcpyDeviceToHost));
+    }
+    if (d_host) F3RG_CUDA(cudaMemcpy(d_host, d.get(), n * 8, cudaMemcpyDeviceToHost));
+    *out = h.release();
+  });
+}

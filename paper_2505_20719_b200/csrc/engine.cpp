@@ -62,7 +62,34 @@ void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci, uint64_t n
 DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values,
                            uint64_t ncols)
     : n_(n), nnz_(row_ptr ? row_ptr[n] : 0) {
-  validate_csr(n, row_ptr, col_idx, ncols);
+  init(row_ptr, col_idx, values, ncols, nullptr);
+}
+
+DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values,
+                           Scale scale)
+    : n_(n), nnz_(row_ptr ? row_ptr[n] : 0) {
+  init(row_ptr, col_idx, values, 0, &scale);
+}
+
+void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, uint64_t ncols,
+                        const Scale* scale) {
+  validate_csr(n_, row_ptr, col_idx, ncols);
+  // diagonal positions for the device scaling (the reference's diagonal_index
+  // lookup and its missing-diagonal error, src/scaling.cpp:14-16)
+  std::vector<uint32_t> dpos;
+  if (scale) {
+    dpos.resize(n_ + 1);
+    for (uint64_t i = 0; i < n_; ++i) {
+      const uint32_t* b = col_idx + row_ptr[i];
+      const uint32_t* e = col_idx + row_ptr[i + 1];
+      const uint32_t* it = std::lower_bound(b, e, (uint32_t)i);
+      if (it == e || *it != i)
+        throw Error(ERR_FACTORIZATION, "diagonal scaling: missing diagonal entry in row " + std::to_string(i));
+      dpos[i] = (uint32_t)(it - col_idx);
+      if (values[dpos[i]] == 0.0)
+        throw Error(ERR_FACTORIZATION, "diagonal scaling: zero diagonal entry in row " + std::to_string(i));
+    }
+  }
   // padded so the 16-byte-granular bulk copies never read past an allocation
   rp_.alloc((n_ + 1) * 4 + 32);
   ci_.alloc(nnz_ * 4 + 32);
@@ -75,6 +102,14 @@ DeviceMatrix::DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* 
     F3RG_CUDA(cudaMemset(val_[p].get(), 0, val_[p].bytes()));
   }
   if (nnz_) F3RG_CUDA(cudaMemcpy(val_[2].get(), values, nnz_ * 8, cudaMemcpyHostToDevice));
+  if (scale && n_) {
+    DevBuf dp(n_ * 4 + 16), d(n_ * 8 + 16), bad(16);
+    F3RG_CUDA(cudaMemcpy(dp.get(), dpos.data(), n_ * 4, cudaMemcpyHostToDevice));
+    F3RG_CUDA(cudaMemset(bad.get(), 0xff, 8));
+    F3RG_CUDA(launch_diag_scale(Launch{}, rp_.get<uint32_t>(), ci_.get<uint32_t>(), val_[2].get<double>(),
+                                dp.get<uint32_t>(), d.get<double>(), n_, bad.get<unsigned long long>()));
+    if (scale->d_dev) F3RG_CUDA(cudaMemcpy(scale->d_dev, d.get(), n_ * 8, cudaMemcpyDeviceToDevice));
+  }
   // replicas: element-wise RNE demotion on the device (cvt.rn.f32.f64 / cvt.rn.f16.f64)
   F3RG_CUDA(launch_copy(2, 1, Launch{}, val_[2].get(), val_[1].get(), nnz_));
   F3RG_CUDA(launch_copy(2, 0, Launch{}, val_[2].get(), val_[0].get(), nnz_));

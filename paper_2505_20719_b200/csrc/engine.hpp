@@ -121,6 +121,13 @@ class DeviceMatrix {
   // ncols > n: a rank's rows of a partitioned matrix, columns in its ext layout
   DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values,
                uint64_t ncols = 0);
+  // the same for diagonal_scale(A) (src/scaling.cpp:11-38) computed on the device from
+  // the unscaled values: the replicas are those of the scaled matrix; d (n) is left
+  // in d_dev (device, may be null). Throws Error(ERR_FACTORIZATION) like the reference
+  struct Scale {
+    double* d_dev = nullptr;
+  };
+  DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, Scale scale);
   uint64_t rows() const { return n_; }
   uint64_t nnz() const { return nnz_; }
   CsrDev csr() const;
@@ -129,6 +136,8 @@ class DeviceMatrix {
   bool d16() const { return dcol_.get() != nullptr; }  // 16-bit delta column stream in use
 
  private:
+  void init(const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, uint64_t ncols,
+            const Scale* scale);
   uint64_t n_ = 0, nnz_ = 0;
   DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_, pk_;
   uint32_t ntiles_[3] = {0, 0, 0};

@@ -121,6 +121,13 @@ cudaError_t launch_bi_update(Launch l, double* x, double* r, const double* p, co
                              const double* t, uint64_t n, KState* S, SyncH sync);
 cudaError_t launch_krylov_resume(Launch l, KState* S);
 
+// ---- problem setup on the device (launch_setup.cu) ----------------------------------
+// diagonal scaling in place: d_i = 1/sqrt|a_ii|, a_ij = (a_ij d_i) d_j; *bad = first
+// row with a zero diagonal (the caller initialises it to ~0)
+cudaError_t launch_diag_scale(Launch l, const uint32_t* rp, const uint32_t* ci, double* vals, const uint32_t* dpos,
+                              double* d, uint64_t n, unsigned long long* bad);
+cudaError_t launch_scale_rhs(Launch l, const double* b, const double* d, double* out, uint64_t n);
+
 // ---- BLAS-1 / SpMV (kernel-level entry points) ----------------------------------
 cudaError_t launch_fill(int p, Launch l, void* x, uint64_t n, double value);
 cudaError_t launch_copy(int px, int py, Launch l, const void* x, void* y, uint64_t n);

@@ -1,0 +1,51 @@
+// launch_setup.cu -- problem setup on the device: the symmetric
+// diagonal scaling of reference src/scaling.cpp:11-38,
+//   d_i = 1 / sqrt(|a_ii|),  a~_ij = (a_ij * d_i) * d_j,  b~_i = b_i * d_i,
+// element-wise with the same IEEE operations in the same order (correctly rounded
+// sqrt and division on both sides), so the scaled system is bit-identical.
+#include "dispatch.cuh"
+
+namespace f3rg {
+
+// d from the diagonal entries (dpos[i] = position of a_ii); a zero diagonal records
+// the smallest offending row in *bad (initialised to ~0 by the caller)
+__global__ void __launch_bounds__(256) k_scale_d(const double* vals, const uint32_t* dpos, double* d, uint64_t n,
+                                                 unsigned long long* bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double aii = vals[dpos[i]];
+    if (aii == 0.0) atomicMin(bad, (unsigned long long)i);
+    d[i] = __ddiv_rn(1.0, __dsqrt_rn(fabs(aii)));
+  }
+}
+
+// a~_ij = (a_ij * d_i) * d_j, one thread per row (rows walk their entries in order)
+__global__ void __launch_bounds__(256) k_scale_vals(const uint32_t* rp, const uint32_t* ci, double* vals,
+                                                    const double* d, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double di = d[i];
+    for (uint32_t k = rp[i]; k < rp[i + 1]; ++k) vals[k] = __dmul_rn(__dmul_rn(vals[k], di), d[ci[k]]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scale_rhs(const double* b, const double* d, double* out, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = __dmul_rn(b[i], d[i]);
+}
+
+cudaError_t launch_diag_scale(Launch l, const uint32_t* rp, const uint32_t* ci, double* vals, const uint32_t* dpos,
+                              double* d, uint64_t n, unsigned long long* bad) {
+  const int g = l.grid ? l.grid : stream_grid();
+  k_scale_d<<<g, kThreads, 0, l.stream>>>(vals, dpos, d, n, bad);
+  k_scale_vals<<<g, kThreads, 0, l.stream>>>(rp, ci, vals, d, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_rhs(Launch l, const double* b, const double* d, double* out, uint64_t n) {
+  const int g = l.grid ? l.grid : stream_grid();
+  k_scale_rhs<<<g, kThreads, 0, l.stream>>>(b, d, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace f3rg

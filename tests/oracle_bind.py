@@ -278,6 +278,8 @@ class Reference:
         L.ref_richardson_apply_m.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, _dp, _dp]
         L.ref_krylov_solve_m.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, _dp, C.c_double, C.c_uint64,
                                          C.c_void_p, _dp, C.c_uint64, C.POINTER(_RefReport)]
+        L.ref_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_void_p,
+                                             C.c_void_p, C.c_void_p]
         L.ref_set_threads.argtypes = [C.c_int]
         L.ref_max_threads.restype = C.c_int
 
@@ -418,6 +420,17 @@ class Reference:
         return Report(bool(rep.converged), rep.outer_iterations, rep.precond_invocations, rep.final_true_residual,
                       [], list(hist[:min(rep.n_history, hist_cap)]), [], rep.flag.decode(), rep.wall_seconds,
                       rep.id.decode())
+
+    def read_matrix_market(self, path):
+        """(row_ptr, col_idx, values) of the reference reader; RuntimeError on ParseError"""
+        n, nnz = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.ref_read_matrix_market(str(path).encode(), C.byref(n), C.byref(nnz), None, None, None))
+        rp = np.zeros(n.value + 1, np.uint32)
+        ci = np.zeros(max(1, nnz.value), np.uint32)
+        va = np.zeros(max(1, nnz.value))
+        self._check(self.lib.ref_read_matrix_market(str(path).encode(), C.byref(n), C.byref(nnz), rp.ctypes.data,
+                                                    ci.ctypes.data, va.ctypes.data))
+        return rp, ci[:nnz.value], va[:nnz.value]
 
     def spec_canonical(self, spec):
         buf = C.create_string_buffer(512)
