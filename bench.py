@@ -123,6 +123,41 @@ def column_stream_saving(p):
     return 4.0 * p.nnz - (2.0 * p.nnz + 4.0 * p.n)
 
 
+def spmv_per_precision(f, torch, reps, p, reps_n=20):
+    """The metric's second half, "SpMV HBM GB/s per precision": the standalone device
+    SpMV (f3rg_spmv, reference spmv src/csr.cpp:138-147) at each precision triple of
+    the path, timed with CUDA events over `reps_n` back-to-back launches (inputs
+    resident; the 223-446 MB matrix streams exceed the 126 MB L2). GB/s by SURVEY
+    8(d)'s algorithmic bytes nnz (sA + 4) + 4 (n + 1) + n (sx + sy) -- the reference's
+    u32 CSR -- and by the bytes actually streamed (D16/P16 column streams)."""
+    size = {0: 2, 1: 4, 2: 8}
+    peak, _ = _peaks()
+    saving = column_stream_saving(p)
+    out = []
+    for pa, px, py, role in ((2, 2, 2, "L1 / true residual"), (1, 1, 1, "L2"), (0, 1, 1, "L3"),
+                             (0, 0, 0, "Richardson operand")):
+        x = f.DenseVector(torch.rand(p.n, device="cuda", dtype=torch.float64).to(f.torch_dtype(px)))
+        y = f.DenseVector(p.n, f.Precision(py))
+        A = reps.at(f.Precision(pa))
+        for _ in range(3):
+            f.spmv(A, x, y)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps_n):
+            f.spmv(A, x, y)
+        e1.record()
+        torch.cuda.synchronize()
+        us = 1e3 * e0.elapsed_time(e1) / reps_n
+        algo = p.nnz * (size[pa] + 4) + 4 * (p.n + 1) + p.n * (size[px] + size[py])
+        streamed = algo - saving
+        out.append({"precision": f"A f{8 * size[pa]}, x f{8 * size[px]}, y f{8 * size[py]}", "role": role,
+                    "us": round(us, 2), "algorithmic_gbs": round(algo / us / 1e3, 1),
+                    "streamed_gbs": round(streamed / us / 1e3, 1), "frac": round(algo / us / 1e3 / peak, 4),
+                    "frac_streamed": round(streamed / us / 1e3 / peak, 4)})
+    return out
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
@@ -408,6 +443,7 @@ def run_ours(args):
         "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
     }
+    line["spmv_per_precision"] = spmv_per_precision(f, torch, reps, p)
     pre = [k for k in prof if k[0].startswith("precond_")]
     if pre:
         lv = M.sweep_levels()
