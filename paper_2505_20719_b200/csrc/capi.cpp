@@ -165,7 +165,7 @@ IluConfig to_cfg(const f3rg_ilu_config* c) {
 
 // the fp64 CSR of a device matrix, back in host memory (setup only)
 void download(const DeviceMatrix& m, std::vector<uint32_t>& rp, std::vector<uint32_t>& ci, std::vector<double>& v) {
-  const CsrDev c = m.csr();
+  const CsrDev c = m.csr_plain();
   rp.resize(m.rows() + 1);
   ci.resize(m.nnz());
   v.resize(m.nnz());

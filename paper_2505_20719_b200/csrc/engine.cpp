@@ -124,26 +124,90 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
         d16 = false;
         break;
       }
-  if (d16) {
+  // D16 / P16 streams of one row order (rp/ci on the host, the fp16 values on the device)
+  auto delta_streams = [&](const uint32_t* rp, const uint32_t* ci, const DevBuf& v16, DevBuf& dcol, DevBuf& first,
+                           DevBuf& pk) {
     std::vector<uint16_t> dc(nnz_ + 16, 0);
     std::vector<uint32_t> fc(n_ + 16, 0);
     for (uint64_t i = 0; i < n_; ++i) {
-      if (row_ptr[i] < row_ptr[i + 1]) fc[i] = col_idx[row_ptr[i]];
-      for (uint32_t k = row_ptr[i] + 1; k < row_ptr[i + 1]; ++k) dc[k] = (uint16_t)(col_idx[k] - col_idx[k - 1]);
+      if (rp[i] < rp[i + 1]) fc[i] = ci[rp[i]];
+      for (uint32_t k = rp[i] + 1; k < rp[i + 1]; ++k) dc[k] = (uint16_t)(ci[k] - ci[k - 1]);
     }
-    dcol_.alloc(dc.size() * 2);
-    first_.alloc(fc.size() * 4);
-    F3RG_CUDA(cudaMemcpy(dcol_.get(), dc.data(), dc.size() * 2, cudaMemcpyHostToDevice));
-    F3RG_CUDA(cudaMemcpy(first_.get(), fc.data(), fc.size() * 4, cudaMemcpyHostToDevice));
+    dcol.alloc(dc.size() * 2);
+    first.alloc(fc.size() * 4);
+    F3RG_CUDA(cudaMemcpy(dcol.get(), dc.data(), dc.size() * 2, cudaMemcpyHostToDevice));
+    F3RG_CUDA(cudaMemcpy(first.get(), fc.data(), fc.size() * 4, cudaMemcpyHostToDevice));
     if (p16) {  // F3RG_COLUMNS=d16 keeps the separate fp16 value + delta streams
-      pk_.alloc(nnz_ * 4 + 32);
-      F3RG_CUDA(cudaMemset(pk_.get(), 0, pk_.bytes()));
-      F3RG_CUDA(launch_pack16(Launch{}, val_[0].get(), dcol_.get<uint16_t>(), pk_.get<uint32_t>(), nnz_));
+      pk.alloc(nnz_ * 4 + 32);
+      F3RG_CUDA(cudaMemset(pk.get(), 0, pk.bytes()));
+      F3RG_CUDA(launch_pack16(Launch{}, v16.get(), dcol.get<uint16_t>(), pk.get<uint32_t>(), nnz_));
+    }
+  };
+  if (d16) delta_streams(row_ptr, col_idx, val_[0], dcol_, first_, pk_);
+  // tile shape: short-row tiles (one gather chunk per row, four CTAs per SM) for
+  // matrices averaging <= 12 entries per row -- the 7-point operators; the
+  // 27-point and unstructured ones keep the regular shape (F3RG_SHAPE=0/1 forces)
+  const char* shp = std::getenv("F3RG_SHAPE");
+  shape_ = shp && *shp ? (std::atoi(shp) != 0) : (n_ > 0 && nnz_ <= 12 * n_);
+  std::vector<uint32_t> r0, k0;
+  // Sorted-row tiles for irregular row lengths: a tile takes as long as its longest
+  // row (one thread per row, sequential sums), so when the fp16 tiles' thread-slot
+  // load sum(max row length x rows) exceeds 1.5x nnz (config 5: 3.6x) the tile
+  // engine streams a copy whose rows are ordered by length (descending, stable)
+  // inside windows of sigma = 8192 rows (config 5: 1.13x). F3RG_SORT_ROWS=0/1 forces.
+  bool sort_rows = false;
+  if (n_ > 0 && nnz_ > 0) {
+    const char* so = std::getenv("F3RG_SORT_ROWS");
+    if (so && *so) {
+      sort_rows = std::atoi(so) != 0;
+    } else {
+      build_tiles(n_, row_ptr, tile_max_rows(), tile_max_nnz(0 /* fp16 */, shape_), r0, k0);
+      double load = 0;
+      for (size_t t = 0; t + 1 < r0.size(); ++t) {
+        uint32_t mx = 0;
+        for (uint32_t i = r0[t]; i < r0[t + 1]; ++i) mx = std::max(mx, row_ptr[i + 1] - row_ptr[i]);
+        load += (double)mx * (r0[t + 1] - r0[t]);
+      }
+      sort_rows = load > 1.5 * (double)nnz_;
     }
   }
-  std::vector<uint32_t> r0, k0;
+  const uint32_t* trp = row_ptr;  // row pointers the tiles are cut from
+  std::vector<uint32_t> srp;
+  if (sort_rows) {
+    const char* sg = std::getenv("F3RG_SORT_SIGMA");
+    const uint64_t sigma = sg && *sg ? std::max<long long>(1, std::atoll(sg)) : 8192;
+    std::vector<uint32_t> perm(n_);
+    for (uint64_t i = 0; i < n_; ++i) perm[i] = (uint32_t)i;
+    auto len = [&](uint32_t i) { return row_ptr[i + 1] - row_ptr[i]; };
+    for (uint64_t w = 0; w < n_; w += sigma)
+      std::stable_sort(perm.begin() + w, perm.begin() + std::min(n_, w + sigma),
+                       [&](uint32_t a, uint32_t b) { return len(a) > len(b); });
+    srp.assign(n_ + 1, 0);
+    std::vector<uint32_t> sci(nnz_ + 16, 0);
+    for (uint64_t q = 0; q < n_; ++q) {
+      const uint32_t i = perm[q];
+      srp[q + 1] = srp[q] + len(i);
+      std::copy(col_idx + row_ptr[i], col_idx + row_ptr[i + 1], sci.begin() + srp[q]);
+    }
+    perm_.alloc(n_ * 4 + 16);
+    srp_.alloc((n_ + 1) * 4 + 32);
+    sci_.alloc(nnz_ * 4 + 32);
+    F3RG_CUDA(cudaMemset(srp_.get(), 0, srp_.bytes()));
+    F3RG_CUDA(cudaMemset(sci_.get(), 0, sci_.bytes()));
+    F3RG_CUDA(cudaMemcpy(perm_.get(), perm.data(), n_ * 4, cudaMemcpyHostToDevice));
+    F3RG_CUDA(cudaMemcpy(srp_.get(), srp.data(), (n_ + 1) * 4, cudaMemcpyHostToDevice));
+    F3RG_CUDA(cudaMemcpy(sci_.get(), sci.data(), nnz_ * 4, cudaMemcpyHostToDevice));
+    for (int p = 0; p < 3; ++p) {  // the (scaled, demoted) values, moved on the device bit for bit
+      sval_[p].alloc(nnz_ * psize(p) + 32);
+      F3RG_CUDA(cudaMemset(sval_[p].get(), 0, sval_[p].bytes()));
+      F3RG_CUDA(launch_permute_rows(Launch{}, (int)psize(p), rp_.get<uint32_t>(), srp_.get<uint32_t>(),
+                                    perm_.get<uint32_t>(), val_[p].get(), sval_[p].get(), n_));
+    }
+    if (d16) delta_streams(srp.data(), sci.data(), sval_[0], sdcol_, sfirst_, spk_);
+    trp = srp.data();
+  }
   for (int p = 0; p < 3; ++p) {
-    build_tiles(n_, row_ptr, tile_max_rows(), tile_max_nnz(p), r0, k0);
+    build_tiles(n_, trp, tile_max_rows(), tile_max_nnz(p, shape_), r0, k0);
     ntiles_[p] = (uint32_t)(r0.size() - 1);
     tr0_[p].alloc(r0.size() * 4);
     tk0_[p].alloc(k0.size() * 4);
@@ -153,7 +217,7 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
   F3RG_CUDA(cudaDeviceSynchronize());
 }
 
-CsrDev DeviceMatrix::csr() const {
+CsrDev DeviceMatrix::csr_plain() const {
   CsrDev c;
   c.n = n_;
   c.nnz = nnz_;
@@ -166,11 +230,27 @@ CsrDev DeviceMatrix::csr() const {
   return c;
 }
 
+CsrDev DeviceMatrix::csr() const {
+  if (!perm_.get()) return csr_plain();
+  CsrDev c;
+  c.n = n_;
+  c.nnz = nnz_;
+  c.rp = srp_.get<const uint32_t>();
+  c.ci = sci_.get<const uint32_t>();
+  for (int p = 0; p < 3; ++p) c.val[p] = sval_[p].get();
+  c.dcol = sdcol_.get<const uint16_t>();
+  c.first = sfirst_.get<const uint32_t>();
+  c.pk = spk_.get<const uint32_t>();
+  return c;
+}
+
 TilesDev DeviceMatrix::tiles(int p) const {
   TilesDev t;
   t.r0 = tr0_[p].get<const uint32_t>();
   t.k0 = tk0_[p].get<const uint32_t>();
   t.ntiles = ntiles_[p];
+  t.shape = (uint32_t)shape_;
+  t.perm = perm_.get<const uint32_t>();
   return t;
 }
 

@@ -110,7 +110,7 @@ const char* precision_name(int p);
 // than max_nnz forms its own tile. Outputs r0/k0 of length ntiles+1.
 void build_tiles(uint64_t n, const uint32_t* rp, uint32_t max_rows, uint32_t max_nnz, std::vector<uint32_t>& r0,
                  std::vector<uint32_t>& k0);
-uint32_t tile_max_nnz(int pa);
+uint32_t tile_max_nnz(int pa, int shape = 0);
 uint32_t tile_max_rows();
 
 // ---- device matrix (reference SparseCsr + PrecisionReplicas, include/f3r/csr.hpp) ----
@@ -130,17 +130,24 @@ class DeviceMatrix {
   DeviceMatrix(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, Scale scale);
   uint64_t rows() const { return n_; }
   uint64_t nnz() const { return nnz_; }
+  // the CSR the tile kernels stream, always paired with tiles(p): the row-sorted
+  // copy when the matrix has one (tiles(p).perm), else the matrix as uploaded
   CsrDev csr() const;
+  CsrDev csr_plain() const;  // the matrix in its own row order
   TilesDev tiles(int p) const;
+  bool sorted_rows() const { return perm_.get() != nullptr; }
   const void* values(int p) const { return val_[p].get(); }
   bool d16() const { return dcol_.get() != nullptr; }  // 16-bit delta column stream in use
+  int shape() const { return shape_; }  // tile shape: 0 regular, 1 short rows
 
  private:
   void init(const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, uint64_t ncols,
             const Scale* scale);
   uint64_t n_ = 0, nnz_ = 0;
   DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_, pk_;
+  DevBuf perm_, srp_, sci_, sval_[3], sdcol_, sfirst_, spk_;  // row-sorted copy (irregular rows)
   uint32_t ntiles_[3] = {0, 0, 0};
+  int shape_ = 0;
 };
 
 void validate_csr(uint64_t n, const uint32_t* rp, const uint32_t* ci, uint64_t ncols = 0);

@@ -6,9 +6,14 @@
 namespace f3rg {
 
 template <class F>
-static void with_idx64(const CsrDev& A, F&& go) {
-  if (A.dcol) go(PC<1>{});
-  else go(PC<0>{});
+static void with_idx64(const CsrDev& A, const TilesDev& T, F&& go) {
+  if (T.shape) {
+    if (A.dcol) go(PC<5>{});
+    else go(PC<4>{});
+  } else {
+    if (A.dcol) go(PC<1>{});
+    else go(PC<0>{});
+  }
 }
 
 // persistent grid: co-resident CTAs (occ, cached by the caller per kernel
@@ -22,7 +27,7 @@ static int tile_grid(int occ, uint32_t ntiles) {
 cudaError_t launch_cg_spmv(Launch l, const CsrDev& A, const TilesDev& T, const double* p, double* q, KState* S,
                            SyncH sync) {
   cudaError_t err = cudaSuccess;
-  with_idx64(A, [&](auto I) {
+  with_idx64(A, T, [&](auto I) {
     constexpr int IDX = decltype(I)::value;
     constexpr int SM = TileCfg<P64, IDX>::SMEM_BYTES;
     auto kern = k_cg_spmv<IDX>;
@@ -58,7 +63,7 @@ cudaError_t launch_bi_p(Launch l, double* p, const double* v, const double* r, u
 cudaError_t launch_bi_v(Launch l, const CsrDev& A, const TilesDev& T, const double* p, double* v, const double* rhat,
                         KState* S, SyncH sync) {
   cudaError_t err = cudaSuccess;
-  with_idx64(A, [&](auto I) {
+  with_idx64(A, T, [&](auto I) {
     constexpr int IDX = decltype(I)::value;
     constexpr int SM = TileCfg<P64, IDX>::SMEM_BYTES;
     auto kern = k_bi_v<IDX>;
@@ -75,7 +80,7 @@ cudaError_t launch_bi_s(Launch l, double* s, const double* r, const double* v, u
 cudaError_t launch_bi_t(Launch l, const CsrDev& A, const TilesDev& T, const double* s, const double* shat, double* t,
                         KState* S, SyncH sync) {
   cudaError_t err = cudaSuccess;
-  with_idx64(A, [&](auto I) {
+  with_idx64(A, T, [&](auto I) {
     constexpr int IDX = decltype(I)::value;
     constexpr int SM = TileCfg<P64, IDX>::SMEM_BYTES;
     auto kern = k_bi_t<IDX>;

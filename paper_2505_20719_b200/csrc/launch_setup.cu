@@ -48,4 +48,34 @@ cudaError_t launch_scale_rhs(Launch l, const double* b, const double* d, double*
   return cudaGetLastError();
 }
 
+// Row permutation of a CSR value array (sorted-row tiles, engine.cpp
+// DeviceMatrix::init): new row q is old row perm[q], dst[rp_new[q] + t] =
+// src[rp_old[perm[q]] + t]; one warp per row, E-byte elements copied bit for bit.
+template <class E>
+__global__ void __launch_bounds__(256) k_permute_rows(const uint32_t* rp_old, const uint32_t* rp_new,
+                                                      const uint32_t* perm, const E* src, E* dst, uint64_t n) {
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  const unsigned lane = threadIdx.x & 31u;
+  for (uint64_t q = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; q < n; q += warps) {
+    const uint32_t o = rp_old[perm[q]], b = rp_new[q], len = rp_new[q + 1] - b;
+    for (uint32_t t = lane; t < len; t += 32) dst[b + t] = src[o + t];
+  }
+}
+
+cudaError_t launch_permute_rows(Launch l, int esize, const uint32_t* rp_old, const uint32_t* rp_new,
+                                const uint32_t* perm, const void* src, void* dst, uint64_t n) {
+  const int g = l.grid ? l.grid : stream_grid();
+  switch (esize) {
+    case 2: k_permute_rows<<<g, kThreads, 0, l.stream>>>(rp_old, rp_new, perm, static_cast<const uint16_t*>(src),
+                                                          static_cast<uint16_t*>(dst), n); break;
+    case 4: k_permute_rows<<<g, kThreads, 0, l.stream>>>(rp_old, rp_new, perm, static_cast<const uint32_t*>(src),
+                                                          static_cast<uint32_t*>(dst), n); break;
+    case 8: k_permute_rows<<<g, kThreads, 0, l.stream>>>(rp_old, rp_new, perm,
+                                                          static_cast<const unsigned long long*>(src),
+                                                          static_cast<unsigned long long*>(dst), n); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace f3rg

@@ -14,14 +14,19 @@
 namespace f3rg {
 
 // column stream of a launch: P16 (packed fp16 value + delta) for the fp16 replica
-// when present, else D16, else u32
-template <int PA, class F>
-inline void dispatch_idx(const CsrDev& A, F&& go) {
+// when present, else D16, else u32; plus the matrix's tile shape (IDX bit 2)
+template <int PA, int SH, class F>
+inline void dispatch_col(const CsrDev& A, F&& go) {
   if constexpr (PA == P16) {
-    if (A.pk) return go(std::integral_constant<int, 2>{});
+    if (A.pk) return go(std::integral_constant<int, 2 | SH>{});
   }
-  if (A.dcol) go(std::integral_constant<int, 1>{});
-  else go(std::integral_constant<int, 0>{});
+  if (A.dcol) go(std::integral_constant<int, 1 | SH>{});
+  else go(std::integral_constant<int, 0 | SH>{});
+}
+template <int PA, class F>
+inline void dispatch_idx(const CsrDev& A, const TilesDev& T, F&& go) {
+  if (T.shape) dispatch_col<PA, 4>(A, go);
+  else dispatch_col<PA, 0>(A, go);
 }
 
 template <class K>
@@ -58,7 +63,7 @@ cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const 
       });
     });
   };
-  dispatch_idx<PA>(A, go);
+  dispatch_idx<PA>(A, T, go);
   return err;
 }
 
@@ -85,7 +90,7 @@ cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const T
       });
     });
   };
-  dispatch_idx<PA>(A, go);
+  dispatch_idx<PA>(A, T, go);
   return err;
 }
 
@@ -105,7 +110,7 @@ cudaError_t launch_spmv_t(int px, int py, Launch l, const CsrDev& A, const Tiles
       });
     });
   };
-  dispatch_idx<PA>(A, go);
+  dispatch_idx<PA>(A, T, go);
   return err;
 }
 
@@ -144,7 +149,7 @@ cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const
       });
     });
   };
-  dispatch_idx<PA>(A, go);
+  dispatch_idx<PA>(A, T, go);
   return err;
 }
 
@@ -174,7 +179,7 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
       });
     });
   };
-  dispatch_idx<PA>(A, go);
+  dispatch_idx<PA>(A, T, go);
   return err;
 }
 
@@ -203,7 +208,7 @@ cudaError_t launch_richm_phase_t(int pw, int pv, Launch l, const CsrDev& A, cons
       });
     });
   };
-  dispatch_idx<PA>(A, go);
+  dispatch_idx<PA>(A, T, go);
   return err;
 }
 

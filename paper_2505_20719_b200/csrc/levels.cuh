@@ -257,7 +257,7 @@ __device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& 
 // partials are written (to `dots`); the following k_cgs reduces them.
 // V: slot 0 of the basis (owned rows); ld: slot stride; z: the SpMV input (ext layout)
 template <int PA, int PZ, int PW, int IDX>
-__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t ld, int j,
+__global__ void __launch_bounds__(256, tile_minb(IDX)) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t ld, int j,
                                                    LevelState* L, Gate gate, Sync sync, double* dots, int defer,
                                                    Dist dist) {
   pdl_wait();
@@ -677,7 +677,7 @@ struct EpiResidual {
 // also written to *out_norm.
 // x: ext layout (gathered); b, r: owned rows
 template <int PA, int PX, int PW, int IDX>
-__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
+__global__ void __launch_bounds__(256, tile_minb(IDX)) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
                                                   LevelState* L, double* out_norm, Sync sync, Dist dist) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];

@@ -29,7 +29,7 @@ namespace f3rg {
 #ifndef F3RG_RICH_CHUNK
 #define F3RG_RICH_CHUNK 9
 #endif
-constexpr int rich_chunk(int idx) { return idx == 2 ? F3RG_RICH_CHUNK : 0; }
+constexpr int rich_chunk(int idx) { return idx == 2 ? F3RG_RICH_CHUNK : 0; }  // short shape: its own chunk
 
 // Right-hand side of the call: v_i = demote(s * parent_v_i) (s optional). v is in
 // the ext layout (row-block partition): gathers index it by ext column, row-local
@@ -122,7 +122,7 @@ struct EpiResid {
 // calls and the per-call bookkeeping run as k_rich_phase launches with the
 // cross-rank exchanges between them
 template <int PA, int PW, int PV, int IDX>
-__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
+__global__ void __launch_bounds__(256, tile_minb(IDX)) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
                                                     void* out, uint64_t n, RichState* RS, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, unsigned* bar_count,
                                                     unsigned* bar_gen, const IoSlot* io, uint64_t voff, int flags) {
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richardson(CsrDev A, Ti
 enum { PH_RESID = 0, PH_DOTS = 1, PH_UPDATE = 2, PH_BOOK = 3 };
 
 template <int PA, int PW, int PV, int IDX>
-__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_rich_phase(CsrDev A, TilesDev T, int phase, int k, const void* v,
+__global__ void __launch_bounds__(256, tile_minb(IDX)) k_rich_phase(CsrDev A, TilesDev T, int phase, int k, const void* v,
                                                     const double* v_scale, uint64_t off, void* out, uint64_t n,
                                                     RichState* RS, void* R, void* Za, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, Dist dist) {
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_rich_phase(CsrDev A, Ti
 enum { RM_START = 0, RM_RESID = 1, RM_DOTS = 2, RM_UPDATE = 3, RM_BOOK = 4 };
 
 template <int PA, int PW, int PV, int IDX>
-__global__ void __launch_bounds__(256, F3RG_TILE_MINB) k_richm_phase(CsrDev A, TilesDev T, int phase, int k,
+__global__ void __launch_bounds__(256, tile_minb(IDX)) k_richm_phase(CsrDev A, TilesDev T, int phase, int k,
                                                                      const void* v, const double* v_scale,
                                                                      void* out, uint64_t n, RichState* RS, void* R,
                                                                      void* P, void* Za, Gate gate, int level,

@@ -19,7 +19,10 @@
 // walk does one shared-memory load per entry instead of two (same bytes as D16).
 //
 // Tiles: contiguous row ranges with <= NT rows and <= TNNZ nonzeros (built on the
-// host, spec.cpp build_tiles). A row longer than TNNZ gets a tile of its own and is
+// host, spec.cpp build_tiles). Matrices with irregular row lengths are streamed
+// from a row-sorted copy (rows ordered by length inside windows of sigma rows, as
+// SELL-C-sigma does, so a tile's rows finish together); T.perm maps a tile row back
+// to its matrix row for the epilogue. Each row's sum is unchanged. A row longer than TNNZ gets a tile of its own and is
 // summed straight from global memory by one thread (same order, slow, never hit by
 // the benchmark matrices).
 #pragma once
@@ -41,21 +44,55 @@
 #ifndef F3RG_TNNZ16  // entries per fp16 tile (256 rows of a 27-point stencil)
 #define F3RG_TNNZ16 7168
 #endif
+#ifndef F3RG_TNNZ32
+#define F3RG_TNNZ32 6912
+#endif
+#ifndef F3RG_TNNZ64
+#define F3RG_TNNZ64 4096
+#endif
+// short-row shape (IDX bit 2; matrices with <= 12 entries per row on
+// average, the 7-point operators of configs 1/3/4): one gather chunk per row,
+// fewer registers and smaller tiles so four CTAs share an SM
+// (tools/variant_sweep.py m4_c8: config 4 1231 -> 836 ms, config 3 156 -> 132 ms)
+#ifndef F3RG_SHORT_MINB
+#define F3RG_SHORT_MINB 4
+#endif
+#ifndef F3RG_SHORT_CHUNK
+#define F3RG_SHORT_CHUNK 8
+#endif
+#ifndef F3RG_SHORT_TNNZ16
+#define F3RG_SHORT_TNNZ16 4352
+#endif
+#ifndef F3RG_SHORT_TNNZ32
+#define F3RG_SHORT_TNNZ32 3200
+#endif
+#ifndef F3RG_SHORT_TNNZ64
+#define F3RG_SHORT_TNNZ64 2048
+#endif
 #ifndef F3RG_P16_CHUNK  // P16 rows keep the chunk's values in registers too
 #define F3RG_P16_CHUNK 9
 #endif
 
 namespace f3rg {
 
-template <int PA, int IDX = 0>
+// IDX of the tiled kernels: bits 0-1 = column stream (0 u32, 1 D16, 2 P16),
+// bit 2 = short-row shape
+constexpr int idx_col(int idx) { return idx & 3; }
+constexpr bool idx_short(int idx) { return (idx & 4) != 0; }
+constexpr int tile_minb(int idx) { return idx_short(idx) ? F3RG_SHORT_MINB : F3RG_TILE_MINB; }
+
+template <int PA, int IDX_ = 0>
 struct TileCfg {
+  static constexpr int IDX = idx_col(IDX_);
+  static constexpr bool SHORT = idx_short(IDX_);
   static constexpr int NT = 256;  // threads = max rows per tile
   static constexpr int SA = (int)sizeof(T_<PA>);
   // Three CTAs per SM (F3RG_TILE_MINB; 2 stages of <= ~31 KB for fp16 D16/P16
   // tiles). The tile table is shared by all column formats, so TNNZ depends on PA
   // only: fp16 / fp32 tiles hold 256 rows of a 27-point stencil, fp64 ones 151.
   // Stage count and chunk size are from tools/variant_sweep.py on config 2.
-  static constexpr int TNNZ = PA == P16 ? F3RG_TNNZ16 : PA == P32 ? 6912 : 4096;
+  static constexpr int TNNZ = SHORT ? (PA == P16 ? F3RG_SHORT_TNNZ16 : PA == P32 ? F3RG_SHORT_TNNZ32 : F3RG_SHORT_TNNZ64)
+                                   : (PA == P16 ? F3RG_TNNZ16 : PA == P32 ? F3RG_TNNZ32 : F3RG_TNNZ64);
   static constexpr int VAL = 16 / SA;  // value elements per 16 B
   static constexpr int CS = IDX == 1 ? 2 : 4;
   static constexpr int CAL = 16 / CS;  // column elements per 16 B
@@ -72,9 +109,10 @@ struct TileCfg {
 // shared memory and calls epi.row(row, acc) for every row with acc at
 // C = promote(PA, gather precision).
 // CH: gather chunk (0 = default: F3RG_CHUNK, or F3RG_P16_CHUNK for the P16 stream)
-template <int PA, int C, int IDX, int CH = 0, class Gather, class Epi>
+template <int PA, int C, int IDX_, int CH = 0, class Gather, class Epi>
 __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
-  using Cfg = TileCfg<PA, IDX>;
+  using Cfg = TileCfg<PA, IDX_>;
+  constexpr int IDX = Cfg::IDX;
   using TA = T_<PA>;
   using TC = typename std::conditional<IDX == 1, uint16_t, uint32_t>::type;
   constexpr int ST = Cfg::STAGES, VAL = Cfg::VAL, CAL = Cfg::CAL;
@@ -127,7 +165,7 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   // up to CHUNK gathers of a row are issued before the first is consumed (one
   // latency round per CHUNK entries); groups of 8 are unpredicated, only the last
   // partial group is predicated
-  constexpr int CHUNK = CH ? CH : IDX == 2 ? F3RG_P16_CHUNK : F3RG_CHUNK;
+  constexpr int CHUNK = CH ? CH : Cfg::SHORT ? F3RG_SHORT_CHUNK : IDX == 2 ? F3RG_P16_CHUNK : F3RG_CHUNK;
   // groups of GS unpredicated loads (8, or the whole chunk when it is not a multiple
   // of 8: a 27-point row is exactly 3 chunks of 9)
   constexpr int GS = CHUNK % 8 == 0 ? 8 : CHUNK, NG = CHUNK / GS;
@@ -139,9 +177,12 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
     const uint32_t r0 = T.r0[tp], r1 = T.r0[tp + 1], k0 = T.k0[tp], k1 = T.k0[tp + 1];
     const bool longrow = k1 - k0 > (uint32_t)Cfg::TNNZ;
     const uint32_t row = r0 + tid;
+    // the epilogue's row: the matrix row itself, or perm[row] for sorted-row tiles
+    const uint32_t erow = longrow ? (T.perm ? __ldg(T.perm + r0) : r0)
+                                  : (T.perm && row < r1 ? __ldg(T.perm + row) : row);
     // row-local epilogue operands do not depend on the tile: start them now so
     // their latency hides behind the tile transfer and the row sum
-    if (longrow ? tid == 0 : row < r1) e.prefetch(longrow ? r0 : row);
+    if (longrow ? tid == 0 : row < r1) e.prefetch(erow);
     mbar_wait(&bars[s], par);
     if (!longrow) {
       const uint8_t* sp = stage_ptr(s);
@@ -205,7 +246,7 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
             }
           }
         }
-        e.row(row, acc);
+        e.row(erow, acc);
       }
     } else if (tid == 0) {
       T_<C> acc = Ar<C>::zero();
@@ -229,7 +270,7 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
         }
         acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(a), g.value(g.load(c))));
       }
-      e.row(r0, acc);
+      e.row(erow, acc);
     }
     __syncthreads();
     if (tid == 0) {

@@ -49,13 +49,16 @@ def test_spmv_bit_exact_all_precisions(probs, oracle, pa):
                 assert np.array_equal(got, want), (name, pa, px, py, np.abs(got - want).max())
 
 
+@pytest.mark.parametrize("shape", ["0", "1"])
 @pytest.mark.parametrize("columns", ["u32", "d16"])
-def test_spmv_both_column_streams(cuda, oracle, columns, monkeypatch):
-    """the u32 index stream and the 16-bit delta stream (D16) give identical bits"""
+def test_spmv_both_column_streams(cuda, oracle, columns, shape, monkeypatch):
+    """the u32 index stream and the 16-bit delta stream (D16) give identical bits,
+    with the regular and the short-row tile shape (spmv.cuh TileCfg)"""
     import paper_2505_20719_b200 as f
     from paper_2505_20719_b200 import problems
     if columns == "u32":
         monkeypatch.setenv("F3RG_COLUMNS", "u32")
+    monkeypatch.setenv("F3RG_SHAPE", shape)
     p = problems.problem(4, grid=20)
     reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
     a = (p.n, p.row_ptr, p.col_idx)
@@ -74,7 +77,7 @@ def test_spmv_long_rows_and_empty_rows(cuda, oracle):
     n = 9000
     lens = rng.integers(0, 40, n)
     lens[5] = 0
-    lens[17] = 8999  # longer than every tile capacity (TNNZ 7168 / 6912 / 4096)
+    lens[17] = 8999  # longer than every tile capacity (TNNZ <= 7168)
     lens[18] = 5000  # longer than an fp64 tile only
     lens[19] = 0
     rows, cols = [], []
@@ -87,19 +90,47 @@ def test_spmv_long_rows_and_empty_rows(cuda, oracle):
     va = rng.uniform(-1, 1, ci.size)
     a = (n, rp, ci)
     import os
-    for fmt in ("", "d16", "u32"):
+    for fmt, shape, srt in (("", "0", "0"), ("d16", "0", "0"), ("u32", "0", "0"), ("", "1", "0"),
+                            ("u32", "1", "0"), ("", "0", "1"), ("u32", "1", "1")):
         os.environ["F3RG_COLUMNS"] = fmt
+        os.environ["F3RG_SHAPE"] = shape  # regular / short-row tiles
+        os.environ["F3RG_SORT_ROWS"] = srt  # matrix row order / row-sorted stream
         try:
             reps = f.make_replicas(f.SparseCsr(n, rp, ci, va))
         finally:
             os.environ.pop("F3RG_COLUMNS")
+            os.environ.pop("F3RG_SHAPE")
+            os.environ.pop("F3RG_SORT_ROWS")
         for pa in PRECS:
             vals = oracle.round_vec(pa, va)
             for px, py in ((pa, pa), (0, 1), (2, 2)):
                 x = rand_vec(oracle, px, n, 11)
                 y = f.DenseVector(n, py)
                 f.spmv(reps.at(pa), f.DenseVector(x, px), y)
-                assert np.array_equal(y.numpy(), oracle.spmv(a, vals, pa, x, px, py)), (fmt, pa, px, py)
+                assert np.array_equal(y.numpy(), oracle.spmv(a, vals, pa, x, px, py)), (fmt, shape, srt, pa, px, py)
+
+
+@pytest.mark.parametrize("sigma", ["64", "1000000"])
+def test_spmv_sorted_rows_bit_exact(probs, oracle, sigma, monkeypatch):
+    """the row-sorted tile stream (rows ordered by length inside windows of sigma
+    rows, the epilogue writing through the permutation) is bit-exact with the
+    oracle on every small problem, precision triple and column stream"""
+    import paper_2505_20719_b200 as f
+    monkeypatch.setenv("F3RG_SORT_ROWS", "1")
+    monkeypatch.setenv("F3RG_SORT_SIGMA", sigma)
+    for name, p, _ in probs:
+        a = (p.n, p.row_ptr, p.col_idx)
+        for fmt in ("", "u32"):
+            monkeypatch.setenv("F3RG_COLUMNS", fmt)
+            reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
+            for pa, px, py in [(0, 0, 0), (0, 1, 1), (1, 1, 1), (2, 2, 2), (2, 1, 2), (0, 2, 0)]:
+                x = rand_vec(oracle, px, p.n, 5 + pa)
+                y = f.DenseVector(p.n, py)
+                f.spmv(reps.at(pa), f.DenseVector(x, px), y)
+                want = oracle.spmv(a, oracle.round_vec(pa, p.values), pa, x, px, py)
+                assert np.array_equal(y.numpy(), want), (name, sigma, fmt, pa, px, py)
+            # the replica values read back in the matrix's own row order
+            assert np.array_equal(reps.at(0).values(), oracle.round_vec(0, p.values)), name
 
 
 def test_elementwise_bit_exact(cuda, oracle):

@@ -89,6 +89,25 @@ def test_column_streams_solve_identically(probs, monkeypatch):
         assert np.array_equal(r1.x, r2.x), fmt
 
 
+@pytest.mark.parametrize("shape,sort_rows", [("0", "0"), ("1", "0"), ("0", "1")])
+def test_tile_shapes_match_oracle(probs, oracle, shape, sort_rows, monkeypatch):
+    """every small problem solved with the regular and with the short-row tile shape
+    forced (spmv.cuh TileCfg; the default picks by mean row length), and with the
+    row-sorted tile stream forced: the SpMVs are bit-exact either way, only the
+    per-CTA grouping of the dot partials moves"""
+    import paper_2505_20719_b200 as f
+    monkeypatch.setenv("F3RG_SHAPE", shape)
+    monkeypatch.setenv("F3RG_SORT_ROWS", sort_rows)
+    monkeypatch.setenv("F3RG_SORT_SIGMA", "512")
+    for name, p in probs:
+        s, _ = _solver(p, F3R16)
+        rep = s.run(p.b, f.RunOptions(tol=TOL)).report
+        ref = oracle.solve((p.n, p.row_ptr, p.col_idx), p.values, F3R16, p.b, tol=TOL)
+        assert rep.converged and rep.final_true_residual <= TOL, (name, shape, rep.final_true_residual)
+        assert abs(rep.outer_iterations - ref.outer_iterations) <= max(1, round(0.1 * ref.outer_iterations)), \
+            (name, shape, rep.outer_iterations, ref.outer_iterations)
+
+
 def _reference_run(config):
     import json
     import os

@@ -19,16 +19,23 @@ VARIANTS = {
     "m3_s2_c16": ["F3RG_TILE_MINB=3", "F3RG_D16_STAGES=2", "F3RG_CHUNK=16"],
     "m3_s2_c8": ["F3RG_TILE_MINB=3", "F3RG_D16_STAGES=2", "F3RG_CHUNK=8", "F3RG_P16_CHUNK=8"],
     "m4_t5k": ["F3RG_TILE_MINB=4", "F3RG_TNNZ16=5120"],
+    # short-row (7-point, configs 1/3/4) candidates: more CTAs per SM, one chunk per row
+    "m5_c8": ["F3RG_TILE_MINB=5", "F3RG_CHUNK=8", "F3RG_P16_CHUNK=8", "F3RG_TNNZ16=3328",
+              "F3RG_TNNZ32=2560", "F3RG_TNNZ64=1536"],
+    "m6_c8": ["F3RG_TILE_MINB=6", "F3RG_CHUNK=8", "F3RG_P16_CHUNK=8", "F3RG_TNNZ16=2816",
+              "F3RG_TNNZ32=2048", "F3RG_TNNZ64=1280"],
+    "m4_c8": ["F3RG_TILE_MINB=4", "F3RG_CHUNK=8", "F3RG_P16_CHUNK=8", "F3RG_TNNZ16=4352",
+              "F3RG_TNNZ32=3200", "F3RG_TNNZ64=2048"],
 }
 if os.environ.get("SWEEP"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP"].split(",")}
 
 CHILD = r"""
-import sys, time, json, torch
+import os, sys, time, json, torch
 sys.path.insert(0, %r)
 import paper_2505_20719_b200 as f
 from paper_2505_20719_b200 import problems
-p = problems.problem(2)
+p = problems.problem(int(os.environ.get("SWEEP_CONFIG", "2")))
 reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
 s = f.build(f.parse_solver_spec("F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > identity"), reps, f.IdentityPrecond(p.n))
 b = torch.from_numpy(p.b).cuda()
@@ -57,9 +64,12 @@ def build():
 
 
 def run():
-    for name in VARIANTS:
+    names = list(VARIANTS)
+    if os.environ.get("SWEEP_DEFAULT"):
+        names = ["default"] + names
+    for name in names:
         lib = os.path.join(ROOT, "paper_2505_20719_b200", "lib", "variants", f"libf3rg_{name}.so")
-        env = dict(os.environ, F3RG_LIB=lib)
+        env = dict(os.environ, F3RG_LIB=lib) if name != "default" else dict(os.environ)
         r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=600)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
         print(name, line, flush=True)
