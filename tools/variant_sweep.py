@@ -26,6 +26,10 @@ VARIANTS = {
               "F3RG_TNNZ32=2048", "F3RG_TNNZ64=1280"],
     "m4_c8": ["F3RG_TILE_MINB=4", "F3RG_CHUNK=8", "F3RG_P16_CHUNK=8", "F3RG_TNNZ16=4352",
               "F3RG_TNNZ32=3200", "F3RG_TNNZ64=2048"],
+    # gather-heavy (config 5): smaller tiles leave more of the SM's 256 KB to L1
+    "g_half": ["F3RG_TNNZ16=3584", "F3RG_TNNZ32=3456", "F3RG_TNNZ64=2048"],
+    "g_quarter": ["F3RG_TNNZ16=1792", "F3RG_TNNZ32=1728", "F3RG_TNNZ64=1024"],
+    "g_half_c24": ["F3RG_TNNZ16=3584", "F3RG_TNNZ32=3456", "F3RG_TNNZ64=2048", "F3RG_CHUNK=24"],
 }
 if os.environ.get("SWEEP"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["SWEEP"].split(",")}
