@@ -148,7 +148,8 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
   // matrices averaging <= 12 entries per row -- the 7-point operators; the
   // 27-point and unstructured ones keep the regular shape (F3RG_SHAPE=0/1 forces)
   const char* shp = std::getenv("F3RG_SHAPE");
-  shape_ = shp && *shp ? (std::atoi(shp) != 0) : (n_ > 0 && nnz_ <= 12 * n_);
+  const bool forced_shape = shp && *shp;
+  shape_ = forced_shape ? std::min(2, std::max(0, std::atoi(shp))) : (n_ > 0 && nnz_ <= 12 * n_);
   std::vector<uint32_t> r0, k0;
   // Sorted-row tiles for irregular row lengths: a tile takes as long as its longest
   // row (one thread per row, sequential sums), so when the fp16 tiles' thread-slot
@@ -171,6 +172,8 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
       sort_rows = load > 1.5 * (double)nnz_;
     }
   }
+  // irregular rows are gather-bound rows (config 5): half-size tiles leave L1 room
+  if (sort_rows && !forced_shape && shape_ == 0) shape_ = 2;
   const uint32_t* trp = row_ptr;  // row pointers the tiles are cut from
   std::vector<uint32_t> srp;
   if (sort_rows) {

@@ -138,7 +138,7 @@ class DeviceMatrix {
   bool sorted_rows() const { return perm_.get() != nullptr; }
   const void* values(int p) const { return val_[p].get(); }
   bool d16() const { return dcol_.get() != nullptr; }  // 16-bit delta column stream in use
-  int shape() const { return shape_; }  // tile shape: 0 regular, 1 short rows
+  int shape() const { return shape_; }  // tile shape: 0 regular, 1 short rows, 2 gather-bound
 
  private:
   void init(const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, uint64_t ncols,

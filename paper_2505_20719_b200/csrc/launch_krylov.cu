@@ -7,9 +7,12 @@ namespace f3rg {
 
 template <class F>
 static void with_idx64(const CsrDev& A, const TilesDev& T, F&& go) {
-  if (T.shape) {
+  if (T.shape == 1) {
     if (A.dcol) go(PC<5>{});
     else go(PC<4>{});
+  } else if (T.shape == 2) {
+    if (A.dcol) go(PC<9>{});
+    else go(PC<8>{});
   } else {
     if (A.dcol) go(PC<1>{});
     else go(PC<0>{});

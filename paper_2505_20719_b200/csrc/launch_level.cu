@@ -19,7 +19,8 @@ int stream_grid() { return sm_count() * 8; }
 // tile shape of the host tile builder = the device TileCfg (spmv.cuh)
 uint32_t tile_max_rows() { return TileCfg<P16>::NT; }
 uint32_t tile_max_nnz(int pa, int shape) {
-  if (shape) return pa == P16 ? TileCfg<P16, 4>::TNNZ : pa == P32 ? TileCfg<P32, 4>::TNNZ : TileCfg<P64, 4>::TNNZ;
+  if (shape == 1) return pa == P16 ? TileCfg<P16, 4>::TNNZ : pa == P32 ? TileCfg<P32, 4>::TNNZ : TileCfg<P64, 4>::TNNZ;
+  if (shape == 2) return pa == P16 ? TileCfg<P16, 8>::TNNZ : pa == P32 ? TileCfg<P32, 8>::TNNZ : TileCfg<P64, 8>::TNNZ;
   return pa == P16 ? TileCfg<P16>::TNNZ : pa == P32 ? TileCfg<P32>::TNNZ : TileCfg<P64>::TNNZ;
 }
 static int env_int(const char* name, int dflt) {

@@ -25,7 +25,8 @@ inline void dispatch_col(const CsrDev& A, F&& go) {
 }
 template <int PA, class F>
 inline void dispatch_idx(const CsrDev& A, const TilesDev& T, F&& go) {
-  if (T.shape) dispatch_col<PA, 4>(A, go);
+  if (T.shape == 1) dispatch_col<PA, 4>(A, go);
+  else if (T.shape == 2) dispatch_col<PA, 8>(A, go);
   else dispatch_col<PA, 0>(A, go);
 }
 

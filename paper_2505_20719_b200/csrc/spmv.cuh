@@ -69,6 +69,19 @@
 #ifndef F3RG_SHORT_TNNZ64
 #define F3RG_SHORT_TNNZ64 2048
 #endif
+// gather-bound shape (IDX bit 3; matrices whose rows needed sorting, config 5):
+// the regular shape with half-size tiles, so the SM's 256 KB leaves more room to
+// the L1 that serves the scattered x gathers (tools/spmv_probe.py on config 5,
+// profiles/r01d_config5_tile_sweep.jsonl: fp64 SpMV 9157 -> 4161 us, fp32 5797 -> 3101)
+#ifndef F3RG_GATHER_TNNZ16
+#define F3RG_GATHER_TNNZ16 3584
+#endif
+#ifndef F3RG_GATHER_TNNZ32
+#define F3RG_GATHER_TNNZ32 3456
+#endif
+#ifndef F3RG_GATHER_TNNZ64
+#define F3RG_GATHER_TNNZ64 2048
+#endif
 #ifndef F3RG_P16_CHUNK  // P16 rows keep the chunk's values in registers too
 #define F3RG_P16_CHUNK 9
 #endif
@@ -76,23 +89,27 @@
 namespace f3rg {
 
 // IDX of the tiled kernels: bits 0-1 = column stream (0 u32, 1 D16, 2 P16),
-// bit 2 = short-row shape
+// bit 2 = short-row shape, bit 3 = gather-bound shape
 constexpr int idx_col(int idx) { return idx & 3; }
 constexpr bool idx_short(int idx) { return (idx & 4) != 0; }
+constexpr bool idx_gather(int idx) { return (idx & 8) != 0; }
 constexpr int tile_minb(int idx) { return idx_short(idx) ? F3RG_SHORT_MINB : F3RG_TILE_MINB; }
 
 template <int PA, int IDX_ = 0>
 struct TileCfg {
   static constexpr int IDX = idx_col(IDX_);
   static constexpr bool SHORT = idx_short(IDX_);
+  static constexpr bool GATHER = idx_gather(IDX_);
   static constexpr int NT = 256;  // threads = max rows per tile
   static constexpr int SA = (int)sizeof(T_<PA>);
   // Three CTAs per SM (F3RG_TILE_MINB; 2 stages of <= ~31 KB for fp16 D16/P16
   // tiles). The tile table is shared by all column formats, so TNNZ depends on PA
   // only: fp16 / fp32 tiles hold 256 rows of a 27-point stencil, fp64 ones 151.
   // Stage count and chunk size are from tools/variant_sweep.py on config 2.
-  static constexpr int TNNZ = SHORT ? (PA == P16 ? F3RG_SHORT_TNNZ16 : PA == P32 ? F3RG_SHORT_TNNZ32 : F3RG_SHORT_TNNZ64)
-                                   : (PA == P16 ? F3RG_TNNZ16 : PA == P32 ? F3RG_TNNZ32 : F3RG_TNNZ64);
+  static constexpr int TNNZ =
+      SHORT    ? (PA == P16 ? F3RG_SHORT_TNNZ16 : PA == P32 ? F3RG_SHORT_TNNZ32 : F3RG_SHORT_TNNZ64)
+      : GATHER ? (PA == P16 ? F3RG_GATHER_TNNZ16 : PA == P32 ? F3RG_GATHER_TNNZ32 : F3RG_GATHER_TNNZ64)
+               : (PA == P16 ? F3RG_TNNZ16 : PA == P32 ? F3RG_TNNZ32 : F3RG_TNNZ64);
   static constexpr int VAL = 16 / SA;  // value elements per 16 B
   static constexpr int CS = IDX == 1 ? 2 : 4;
   static constexpr int CAL = 16 / CS;  // column elements per 16 B

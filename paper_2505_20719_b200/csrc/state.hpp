@@ -32,7 +32,8 @@ struct TilesDev {
   // replica then starts on the part the L2 still holds (set per launch site, so
   // every solve is still bitwise reproducible)
   uint32_t reverse = 0;
-  // tile shape the tiles were cut for: 0 regular, 1 short rows (spmv.cuh TileCfg)
+  // tile shape the tiles were cut for: 0 regular, 1 short rows, 2 gather-bound
+  // (spmv.cuh TileCfg)
   uint32_t shape = 0;
   // sorted-row tiles (irregular row lengths): tile row q is matrix row perm[q]; the
   // CsrDev handed with these tiles stores the rows in that order. Null = identity

@@ -49,11 +49,11 @@ def test_spmv_bit_exact_all_precisions(probs, oracle, pa):
                 assert np.array_equal(got, want), (name, pa, px, py, np.abs(got - want).max())
 
 
-@pytest.mark.parametrize("shape", ["0", "1"])
+@pytest.mark.parametrize("shape", ["0", "1", "2"])
 @pytest.mark.parametrize("columns", ["u32", "d16"])
 def test_spmv_both_column_streams(cuda, oracle, columns, shape, monkeypatch):
     """the u32 index stream and the 16-bit delta stream (D16) give identical bits,
-    with the regular and the short-row tile shape (spmv.cuh TileCfg)"""
+    with the regular, the short-row and the gather-bound tile shape (spmv.cuh TileCfg)"""
     import paper_2505_20719_b200 as f
     from paper_2505_20719_b200 import problems
     if columns == "u32":
@@ -91,7 +91,8 @@ def test_spmv_long_rows_and_empty_rows(cuda, oracle):
     a = (n, rp, ci)
     import os
     for fmt, shape, srt in (("", "0", "0"), ("d16", "0", "0"), ("u32", "0", "0"), ("", "1", "0"),
-                            ("u32", "1", "0"), ("", "0", "1"), ("u32", "1", "1")):
+                            ("u32", "1", "0"), ("", "0", "1"), ("u32", "1", "1"), ("", "2", "1"),
+                            ("u32", "2", "0")):
         os.environ["F3RG_COLUMNS"] = fmt
         os.environ["F3RG_SHAPE"] = shape  # regular / short-row tiles
         os.environ["F3RG_SORT_ROWS"] = srt  # matrix row order / row-sorted stream

@@ -89,7 +89,7 @@ def test_column_streams_solve_identically(probs, monkeypatch):
         assert np.array_equal(r1.x, r2.x), fmt
 
 
-@pytest.mark.parametrize("shape,sort_rows", [("0", "0"), ("1", "0"), ("0", "1")])
+@pytest.mark.parametrize("shape,sort_rows", [("0", "0"), ("1", "0"), ("0", "1"), ("2", "1")])
 def test_tile_shapes_match_oracle(probs, oracle, shape, sort_rows, monkeypatch):
     """every small problem solved with the regular and with the short-row tile shape
     forced (spmv.cuh TileCfg; the default picks by mean row length), and with the
