@@ -395,11 +395,14 @@ def run_ours(args):
     b_host = torch.from_numpy(p.b).pin_memory().numpy()
     x_host = torch.empty(p.n, dtype=torch.float64).pin_memory().numpy()
     e2e_t = []
-    for _ in range(max(1, min(args.steps, 5))):
+    # one untimed warm-up through the host-buffer entry point (its first call
+    # builds the pinned-staging graph), then the timed steps
+    for it in range(1 + max(1, min(args.steps, 5))):
         t0 = time.perf_counter()
         solver.reset()
         r2 = solver.run(b_host, opts, out=x_host)
-        e2e_t.append(time.perf_counter() - t0)
+        if it:
+            e2e_t.append(time.perf_counter() - t0)
     e2e = float(np.mean(e2e_t))
     assert r2.report.converged
 
