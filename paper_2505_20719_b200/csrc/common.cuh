@@ -121,6 +121,16 @@ __device__ __forceinline__ T_<P> ldcg(const void* p, uint64_t i) {
     return __ldcg(static_cast<const T_<P>*>(p) + i);
   }
 }
+// L1-cached load of data written earlier in the same kernel, after a grid barrier
+// (no SM holds a stale line of it: nothing reads it before the barrier)
+template <int P>
+__device__ __forceinline__ T_<P> ldca(const void* p, uint64_t i) {
+  if constexpr (P == P16) {
+    return __ushort_as_half(__ldca(static_cast<const unsigned short*>(p) + i));
+  } else {
+    return __ldca(static_cast<const T_<P>*>(p) + i);
+  }
+}
 template <int P>
 __device__ __forceinline__ void st(void* p, uint64_t i, T_<P> v) {
   static_cast<T_<P>*>(p)[i] = v;

@@ -152,8 +152,24 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_richardson(CsrDev A, Ti
     if (m == 1) {
       for (uint64_t i = gtid; i < n; i += gstride) st<PW>(out, i, AW::add(AW::mul(w0, rhs.row(i)), AW::zero()));
     } else {
-      // step 1 with z1 on the fly, then steps 2..m-1 ping-ponging through scratch
-      {
+      // step 1 with z1 on the fly, then steps 2..m-1 ping-ponging through scratch.
+      // Gather-bound matrices (config 5, IDX bit 3), m = 2 on one rank: z1 is
+      // materialised at the storage precision first, so the scattered gathers read
+      // 2-byte z1 through L1 instead of the wider v (same z1 bits; the +0 is
+      // immaterial as an SpMV operand, see GatherZ1)
+      bool done = false;
+      if constexpr (idx_gather(IDX)) {
+        if (m == 2 && !(flags & 1) && voff == 0) {
+          for (uint64_t i = gtid; i < n; i += gstride)
+            st<PW>(RS->Za, i, AW::add(AW::mul(w0, rhs.row(i)), AW::zero()));
+          grid_barrier(bar_count, bar_gen);
+          GatherCA<PW, C> g{RS->Za};
+          EpiStep<PV, PW, C, false> e{rhs, w0, cvt<PW>(RS->omegas[1]), RS->Za, out, {}, {}};
+          spmv_tiles<PA, C, IDX, rich_chunk(IDX)>(A, T, g, e, smem);
+          done = true;
+        }
+      }
+      if (!done) {
         GatherZ1<PV, PW, C> g{rhs, w0};
         EpiStep<PV, PW, C, true> e{rhs, w0, cvt<PW>(RS->omegas[1]), nullptr, m == 2 ? out : RS->Za, {}, {}};
         spmv_tiles<PA, C, IDX, rich_chunk(IDX)>(A, T, g, e, smem);

@@ -324,6 +324,15 @@ struct GatherCG {
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(r); }
 };
 
+// same, L1-cached: a vector written earlier in the same kernel before a grid barrier
+template <int PX, int C>
+struct GatherCA {
+  using Raw = T_<PX>;
+  const void* x;
+  __device__ __forceinline__ Raw load(uint32_t c) const { return ldca<PX>(x, c); }
+  __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(r); }
+};
+
 // ---- epilogues --------------------------------------------------------------------
 // Epilogue contract: prefetch(i) is called for the thread's row before the tile
 // lands (issue independent loads there), row(i, acc) after its sum is complete.

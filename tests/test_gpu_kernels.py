@@ -212,12 +212,18 @@ def test_dimension_errors(cuda):
         f.make_replicas(f.SparseCsr(2, [0, 2, 2], [1, 0], [1.0, 1.0]))  # decreasing columns
 
 
-def test_richardson_state_sequence(cuda, oracle):
+@pytest.mark.parametrize("shape", ["", "2"])
+def test_richardson_state_sequence(cuda, oracle, shape, monkeypatch):
     """richardson_apply over 130 calls (updates at calls 64 and 128): weights and
     counters follow the reference's schedule; outputs bit-exact on every
-    non-update call and within fp16 tolerance overall."""
+    non-update call and within fp16 tolerance overall. shape "2": the gather-bound
+    tile shape with the row-sorted stream, whose plain calls materialise z1 first"""
     import paper_2505_20719_b200 as f
     from paper_2505_20719_b200 import problems
+    if shape:
+        monkeypatch.setenv("F3RG_SHAPE", shape)
+        monkeypatch.setenv("F3RG_SORT_ROWS", "1")
+        monkeypatch.setenv("F3RG_SORT_SIGMA", "256")
     p = problems.problem(2, grid=16)
     reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
     a = (p.n, p.row_ptr, p.col_idx)
