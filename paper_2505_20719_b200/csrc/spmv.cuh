@@ -72,12 +72,13 @@
 // gather-bound shape (IDX bit 3; matrices whose rows needed sorting, config 5):
 // the regular shape with half-size tiles, so the SM's 256 KB leaves more room to
 // the L1 that serves the scattered x gathers (tools/spmv_probe.py on config 5,
-// profiles/r01d_config5_tile_sweep.jsonl: fp64 SpMV 9157 -> 4161 us, fp32 5797 -> 3101)
+// profiles/r01d_config5_tile_sweep.jsonl: fp64 SpMV 9157 -> 4161 us, fp16 1945 -> 1858 us
+// at half size; fp32 5797 -> 2733 us at quarter size, its best)
 #ifndef F3RG_GATHER_TNNZ16
 #define F3RG_GATHER_TNNZ16 3584
 #endif
 #ifndef F3RG_GATHER_TNNZ32
-#define F3RG_GATHER_TNNZ32 3456
+#define F3RG_GATHER_TNNZ32 1728
 #endif
 #ifndef F3RG_GATHER_TNNZ64
 #define F3RG_GATHER_TNNZ64 2048
