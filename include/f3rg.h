@@ -84,6 +84,12 @@ typedef struct {
 const char* f3rg_last_error(void);
 const char* f3rg_version(void);
 void f3rg_default_run_options(f3rg_run_options* opts); /* tol 1e-8, 3, 300, 0 */
+/* Validation mode: every dot / norm of the single-GPU solve is summed sequentially in
+ * index order, exactly as the reference's dot_core (src/vector_ops.cpp:20-28), instead
+ * of the default fixed-shape tree. Slow (one dependent add per element); for parity
+ * runs on long vectors. Applies to solvers and kernels launched (or graphs captured)
+ * after the call; the default comes from F3RG_SEQ_REDUCTIONS. Returns the old value. */
+int f3rg_set_seq_reductions(int on);
 
 /* ---- matrices (replaces SparseCsr(...) + make_replicas, src/csr.cpp:40-69,130-136) */
 int f3rg_matrix_create(f3rg_matrix** out, const f3rg_csr* a64);

@@ -98,6 +98,7 @@ def lib():
     L = C.CDLL(LIB_PATH)
     vp, u64, i32, dbl = C.c_void_p, C.c_uint64, C.c_int, C.c_double
     L.f3rg_last_error.restype = C.c_char_p
+    L.f3rg_set_seq_reductions.argtypes = [i32]
     L.f3rg_version.restype = C.c_char_p
     L.f3rg_matrix_create.argtypes = [C.POINTER(vp), C.POINTER(_Csr)]
     L.f3rg_matrix_destroy.argtypes = [vp]
@@ -294,6 +295,28 @@ def dot_at_least(x: DenseVector, y: DenseVector, floor_precision: Precision) -> 
     _check(lib().f3rg_dot(x.ptr(), x.precision(), y.ptr(), y.precision(), x.size(), int(floor_precision),
                           C.byref(out), _stream()))
     return out.value
+
+
+class seq_reductions:
+    """Validation mode: every dot / norm summed sequentially in index order, as the
+    reference's dot_core (src/vector_ops.cpp:20-28), instead of the fixed-shape
+    tree. Applies to kernels launched and solvers built inside the block:
+
+        with seq_reductions():
+            solver = build(spec, reps, M)
+            run = solver.run(b, opts)
+    """
+
+    def __init__(self, on: bool = True):
+        self.on = on
+        self.old = None
+
+    def __enter__(self):
+        self.old = lib().f3rg_set_seq_reductions(1 if self.on else 0)
+        return self
+
+    def __exit__(self, *a):
+        lib().f3rg_set_seq_reductions(self.old)
 
 
 def dot(x: DenseVector, y: DenseVector) -> float:

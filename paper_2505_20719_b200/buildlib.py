@@ -32,8 +32,10 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 CXX = "g++"
 
-CU_SRCS = ["launch_t16.cu", "launch_t32.cu", "launch_t64.cu", "launch_level.cu", "launch_rich.cu", "launch_blas.cu",
-           "launch_krylov.cu", "launch_precond.cu", "launch_setup.cu"]
+CU_SRCS = ["launch_level.cu", "launch_rich.cu", "launch_blas.cu", "launch_krylov.cu", "launch_precond.cu",
+           "launch_setup.cu"]
+# launch_tile_inst.cu is compiled once per (matrix precision, kernel family): 18 units
+TILE_INST = [(pa, fam) for pa in range(3) for fam in range(6)]
 CPP_SRCS = ["engine.cpp", "spec.cpp", "capi.cpp", "problems.cpp", "partition.cpp", "exchange.cpp", "precond.cpp", "mmio.cpp"]
 
 
@@ -89,22 +91,27 @@ def _build_lib(force, jobs, verbose, dflags):
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     hdr_time = _newest(headers)
     jobs_list = []
-    for src in CU_SRCS + CPP_SRCS:
+    units = [(src, src + ".o", []) for src in CU_SRCS + CPP_SRCS]
+    units += [("launch_tile_inst.cu", f"launch_tile_inst_p{pa}_f{fam}.cu.o",
+               [f"-DF3RG_INST_PA={pa}", f"-DF3RG_INST_FAMILY={fam}"]) for pa, fam in TILE_INST]
+    for src, oname, udefs in units:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(OBJDIR, src + ".o")
+        obj = os.path.join(OBJDIR, oname)
         if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(path), hdr_time):
             continue
         if src.endswith(".cu"):
-            cmd = [NVCC] + NVCC_FLAGS + dflags + ["-c", path, "-o", obj]
+            cmd = [NVCC] + NVCC_FLAGS + dflags + udefs + ["-c", path, "-o", obj]
         else:
             cmd = [CXX] + CXX_FLAGS + dflags + _gomp_flags() + ["-c", path, "-o", obj]
         jobs_list.append((cmd, obj + ".log"))
+    # the heaviest units first, so the pool's tail is short
+    jobs_list.sort(key=lambda j: 0 if "launch_tile_inst" in j[1] else 1)
     if jobs_list:
         with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
             futs = [ex.submit(_run, c, log) for c, log in jobs_list]
             for f in futs:
                 f.result()
-    objs = [os.path.join(OBJDIR, s + ".o") for s in CU_SRCS + CPP_SRCS]
+    objs = [os.path.join(OBJDIR, o) for _, o, _ in units]
     if force or jobs_list or not os.path.exists(LIB) or os.path.getmtime(LIB) < _newest(objs):
         cmd = [CXX, "-shared", "-o", LIB] + objs + [f"-L{CUDA_HOME}/lib64", "-lcudart_static", "-ldl", "-lrt",
                                                      "-lpthread"] + _gomp_flags() + _stdcxx_flags() + \

@@ -75,7 +75,11 @@ __global__ void __launch_bounds__(256) k_dot(const void* x, const void* y, uint6
     block_sum<C, 1>(acc, scratch);
     if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<C>::wide(acc[0]);
     if (!last_block(sync.counter)) return;
-    reduce_partials<C, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (sync.seq) {
+      seq_sums<C>(n, 1, [&](uint64_t i, int) { return Ar<C>::mul(cvt<C>(ld<PX>(x, i)), cvt<C>(ld<PY>(y, i))); }, tot);
+    } else {
+      reduce_partials<C, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    }
     if (publish_local(dist, 1, tot)) return;
   } else {
     combine_ranks<C>(dist, 1, tot);

@@ -110,6 +110,12 @@ extern "C" {
 const char* f3rg_last_error(void) { return g_err.c_str(); }
 const char* f3rg_version(void) { return "f3rg 0.1 (sm_100a)"; }
 
+int f3rg_set_seq_reductions(int on) {
+  const int old = f3rg::seq_reductions();
+  f3rg::set_seq_reductions(on);
+  return old;
+}
+
 void f3rg_default_run_options(f3rg_run_options* o) {
   o->tol = 1e-8;
   o->max_outer_restarts = 3;

@@ -47,6 +47,53 @@ template <> struct Cvt<P16> {
 template <int To, class S>
 __device__ __forceinline__ T_<To> cvt(S x) { return Cvt<To>::of(x); }
 
+// ---- hypot as the reference's std::hypot computes it ------------------------------
+// The Givens rotations call std::hypot at the basis precision (src/fgmres.cpp:105),
+// i.e. glibc's hypot / hypotf on the x86-64 reference build. Both are restated here
+// so the device rotations are bit-identical (checked against the host libm over
+// 4e7 random pairs, every binade and sign; tests/test_gpu_seq.py):
+//  * hypotf: the binary32 result of the binary64 expression sqrt(x*x + y*y) (both
+//    squares exact, one rounding each for the sum, the sqrt and the narrowing);
+//  * hypot (glibc >= 2.35, dbl-64/e_hypot.c without FMA): Borges' corrected kernel
+//    ("An Improved Algorithm for hypot(a,b)", 2019) with range scaling by 2^600.
+__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  double t1, t2;
+  if (h <= __dmul_rn(2.0, ay)) {
+    const double delta = __dsub_rn(h, ay);
+    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+    t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+  } else {
+    const double delta = __dsub_rn(h, ax);
+    t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
+  }
+  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+}
+__device__ __forceinline__ double ref_hypot(double x, double y) {
+  if (isinf(x) || isinf(y)) return __longlong_as_double(0x7ff0000000000000ll);
+  if (isnan(x) || isnan(y)) return x + y;
+  x = fabs(x);
+  y = fabs(y);
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  constexpr double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+  if (ax > kLarge) {
+    if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+    return __ddiv_rn(hypot_kernel(__dmul_rn(ax, kScale), __dmul_rn(ay, kScale)), kScale);
+  }
+  if (ay < kTiny) {
+    if (ax >= __ddiv_rn(ay, kEps)) return __dadd_rn(ax, ay);
+    return __dmul_rn(hypot_kernel(__ddiv_rn(ax, kScale), __ddiv_rn(ay, kScale)), kScale);
+  }
+  if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+  return hypot_kernel(ax, ay);
+}
+__device__ __forceinline__ float ref_hypotf(float x, float y) {
+  if (isinf(x) || isinf(y)) return __int_as_float(0x7f800000);
+  const double xd = x, yd = y;
+  return __double2float_rn(__dsqrt_rn(__dadd_rn(__dmul_rn(xd, xd), __dmul_rn(yd, yd))));
+}
+
 // ---- one rounded op at precision C --------------------------------------------
 template <int C> struct Ar;
 template <> struct Ar<P64> {
@@ -58,7 +105,7 @@ template <> struct Ar<P64> {
   __device__ static T sub(T a, T b) { return __dsub_rn(a, b); }
   __device__ static T div(T a, T b) { return __ddiv_rn(a, b); }
   __device__ static T sqrt(T a) { return __dsqrt_rn(a); }
-  __device__ static T hypot(T a, T b) { return ::hypot(a, b); }
+  __device__ static T hypot(T a, T b) { return ref_hypot(a, b); }
   __device__ static T neg(T a) { return -a; }
   __device__ static double wide(T a) { return a; }
   __device__ static bool finite(T a) { return isfinite(a); }
@@ -72,7 +119,7 @@ template <> struct Ar<P32> {
   __device__ static T sub(T a, T b) { return __fsub_rn(a, b); }
   __device__ static T div(T a, T b) { return __fdiv_rn(a, b); }
   __device__ static T sqrt(T a) { return __fsqrt_rn(a); }
-  __device__ static T hypot(T a, T b) { return ::hypotf(a, b); }
+  __device__ static T hypot(T a, T b) { return ref_hypotf(a, b); }
   __device__ static T neg(T a) { return -a; }
   __device__ static double wide(T a) { return (double)a; }
   __device__ static bool finite(T a) { return isfinite(a); }
@@ -86,7 +133,7 @@ template <> struct Ar<P16> {
   __device__ static T sub(T a, T b) { return __hsub_rn(a, b); }
   __device__ static T div(T a, T b) { return __float2half_rn(__fdiv_rn(__half2float(a), __half2float(b))); }
   __device__ static T sqrt(T a) { return __float2half_rn(__fsqrt_rn(__half2float(a))); }
-  __device__ static T hypot(T a, T b) { return __float2half_rn(::hypotf(__half2float(a), __half2float(b))); }
+  __device__ static T hypot(T a, T b) { return __float2half_rn(ref_hypotf(__half2float(a), __half2float(b))); }
   __device__ static T neg(T a) { return __hneg(a); }
   __device__ static double wide(T a) { return (double)__half2float(a); }
   __device__ static bool finite(T a) { return (__half_as_ushort(a) & 0x7c00u) != 0x7c00u; }
@@ -292,6 +339,73 @@ __device__ void reduce_partials(const double* partials, int G, int stride, doubl
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) out[k] = Ar<C>::wide(acc[k]);
+  }
+  __syncthreads();
+}
+
+// ---- sequential reductions (validation mode) --------------------------------------
+// The reference sums every dot and norm on one thread in index order (dot_core,
+// src/vector_ops.cpp:20-28): acc = fl_C(acc + fl_C(x_i * y_i)), i = 0 .. n-1. With
+// sequential reductions on (F3RG_SEQ_REDUCTIONS=1 / f3rg_set_seq_reductions) the
+// CTA that completes a reduction recomputes it in exactly that order from the
+// operands in memory and replaces the tree result -- slow (one dependent add per
+// element), bit-identical to the reference. It exists to validate parity on long
+// vectors, where the two orders part.
+template <int C>
+__device__ __forceinline__ T_<C> shfl_idx(T_<C> v, int src) {
+  if constexpr (C == P16) {
+    return __ushort_as_half(__shfl_sync(0xffffffffu, __half_as_ushort(v), src));
+  } else {
+    return __shfl_sync(0xffffffffu, v, src);
+  }
+}
+
+// One warp: the sequential sum of term(i), i < n. Lanes fetch and form the terms of
+// 256 consecutive elements (the next batch's loads are in flight while the current
+// one is summed); every lane then carries the same dependent chain, so the result
+// is valid in all lanes. Terms past n are skipped, never added as zeros (-0 + +0 = +0).
+template <int C, class F>
+__device__ __forceinline__ T_<C> warp_seq_sum(uint64_t n, const F& term) {
+  constexpr int U = 8;
+  const int lane = threadIdx.x & 31;
+  T_<C> acc = Ar<C>::zero();
+  T_<C> cur[U], nxt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t i = (uint64_t)u * 32 + lane;
+    cur[u] = i < n ? term(i) : Ar<C>::zero();
+  }
+  for (uint64_t base = 0; base < n; base += 32 * U) {
+    const uint64_t nb = base + 32 * U;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = nb + (uint64_t)u * 32 + lane;
+      nxt[u] = i < n ? term(i) : Ar<C>::zero();
+    }
+    const uint64_t lim = n - base;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int s = 0; s < 32; ++s) {
+        const T_<C> t = shfl_idx<C>(cur[u], s);
+        if ((uint64_t)(u * 32 + s) < lim) acc = Ar<C>::add(acc, t);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+  }
+  return acc;
+}
+
+// nv <= 8 sequential sums by one whole CTA (warp k runs sum k); term(i, k) is the
+// k-th sum's term at element i. out[k] (shared, doubles holding C values) is valid
+// for all threads after the call.
+template <int C, class F>
+__device__ void seq_sums(uint64_t n, int nv, const F& term, double* out) {
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if (w < nv) {
+    const T_<C> s = warp_seq_sum<C>(n, [&](uint64_t i) { return term(i, w); });
+    if ((threadIdx.x & 31) == 0) out[w] = Ar<C>::wide(s);
   }
   __syncthreads();
 }

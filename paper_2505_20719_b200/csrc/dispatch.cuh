@@ -24,7 +24,8 @@ inline void with_p(int p, F&& f) {
   }
 }
 
-inline Sync to_sync(SyncH s) { return Sync{s.partials, s.counter}; }
+// seq: sequential index-order reductions (validation mode, launch.hpp)
+inline Sync to_sync(SyncH s) { return Sync{s.partials, s.counter, seq_reductions()}; }
 inline Gate to_gate(GateH g) { return Gate{g.dead, g.n}; }
 inline Dist to_dist(DistH d) { return Dist{d.mode, d.P, d.loc, d.all}; }
 

@@ -321,6 +321,8 @@ Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_ki
       if (L.kind == LK_RICHARDSON && L.m > 2)
         throw Error(ERR_UNSUPPORTED, "row-block partition: Richardson levels with m > 2 are not implemented");
   }
+  if (ex_ && seq_reductions())
+    throw Error(ERR_UNSUPPORTED, "sequential reductions are a single-rank validation mode");
   build_levels();
   // the in-process transport synchronises ranks on the host between kernels, so it
   // launches eagerly; NCCL exchanges are stream work and go into the graph
@@ -417,7 +419,8 @@ void Solver::build_levels() {
         F3RG_CUDA(cudaMemset(L.R.get(), 0, L.R.bytes()));
         F3RG_CUDA(cudaMemset(L.Za.get(), 0, L.Za.bytes()));
       }
-      L.Zb.alloc(m > 2 ? L.vbytes(n_) + 16 : 16);
+      // Zb: step ping-pong for m > 2; s = A p of update calls under sequential reductions
+      L.Zb.alloc(L.vbytes(n_) + 16);
       if (has_m()) L.P.alloc(L.vbytes(n_) + 16);
       RichState h;
       h.m = m;

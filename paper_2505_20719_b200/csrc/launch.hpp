@@ -40,6 +40,10 @@ struct Launch {
 // grid used for streaming (BLAS-1 style) kernels and for tile kernels (per value
 // precision and whether the kernel is the cooperative Richardson one)
 int stream_grid();
+// sequential index-order reductions (validation mode, common.cuh seq_sums): the
+// value in effect when a kernel is launched or captured into a graph
+int seq_reductions();
+void set_seq_reductions(int on);
 int max_partial_blocks();
 int sm_count();
 

@@ -1,4 +1,5 @@
 // launch_level.cu -- launchers for the FGMRES level kernels (levels.cuh).
+#include <atomic>
 #include <cstdlib>
 
 #include "dispatch.cuh"
@@ -42,6 +43,12 @@ bool pdl_enabled() {
   return on;
 }
 int max_partial_blocks() { return sm_count() * 8; }
+static std::atomic<int>& seq_flag() {
+  static std::atomic<int> f{env_int("F3RG_SEQ_REDUCTIONS", 0) != 0};
+  return f;
+}
+int seq_reductions() { return seq_flag().load(std::memory_order_relaxed); }
+void set_seq_reductions(int on) { seq_flag().store(on != 0, std::memory_order_relaxed); }
 
 cudaError_t launch_level_start(int ps, int pw, Launch l, void* src, const double* src_scale, int writeback, void* dst,
                                uint64_t n, LevelState* L, int* dead, GateH gate, int level, unsigned long long* cnt,

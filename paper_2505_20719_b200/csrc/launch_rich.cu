@@ -1,5 +1,5 @@
 // launch_rich.cu -- runtime dispatch of the tiled kernels on the matrix precision
-// (the instantiations live in launch_t16/32/64.cu).
+// (the instantiations live in launch_tile_inst.cu).
 #include "launch_tile_decl.hpp"
 
 namespace f3rg {

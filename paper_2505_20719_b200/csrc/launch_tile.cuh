@@ -1,6 +1,6 @@
 // launch_tile.cuh -- launchers of every TMA-tiled kernel (SpMV + fused epilogues)
-// for ONE matrix precision PA, instantiated in launch_t16.cu / launch_t32.cu /
-// launch_t64.cu so the heavy template bodies compile in parallel. Only
+// for ONE matrix precision PA, instantiated per (precision, kernel family) by
+// launch_tile_inst.cu so the heavy template bodies compile in parallel. Only
 // combinations the engine can produce are instantiated (a child level's vector
 // precision never exceeds its parent's); the column format (u32 or D16) follows
 // the matrix.
@@ -212,22 +212,5 @@ cudaError_t launch_richm_phase_t(int pw, int pv, Launch l, const CsrDev& A, cons
   dispatch_idx<PA>(A, T, go);
   return err;
 }
-
-#define F3RG_TILE_INSTANTIATE(PA)                                                                                  \
-  template cudaError_t launch_spmv_dots_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*, void*, \
-                                              uint64_t, int, LevelState*, GateH, SyncH, double*, int, int*, DistH); \
-  template cudaError_t launch_residual_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*,         \
-                                             const double*, void*, LevelState*, double*, SyncH, DistH);            \
-  template cudaError_t launch_spmv_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*, void*);     \
-  template cudaError_t launch_richardson_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, const void*,       \
-                                               const double*, void*, uint64_t, RichState*, GateH, int,             \
-                                               unsigned long long*, SyncH, unsigned*, unsigned*, const IoSlot*,    \
-                                               uint64_t, int);                                                     \
-  template cudaError_t launch_rich_phase_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, int, int,          \
-                                               const void*, const double*, uint64_t, void*, uint64_t, RichState*,  \
-                                               void*, void*, GateH, int, unsigned long long*, SyncH, DistH);        \
-  template cudaError_t launch_richm_phase_t<PA>(int, int, Launch, const CsrDev&, const TilesDev&, int, int,         \
-                                                const void*, const double*, void*, uint64_t, RichState*, void*,     \
-                                                void*, void*, GateH, int, unsigned long long*, SyncH);
 
 }  // namespace f3rg

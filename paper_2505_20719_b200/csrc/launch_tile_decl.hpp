@@ -1,5 +1,5 @@
 // launch_tile_decl.hpp -- declarations of the per-precision tiled-kernel launchers
-// (defined in launch_tile.cuh, instantiated in launch_t16/32/64.cu).
+// (defined in launch_tile.cuh, instantiated by launch_tile_inst.cu).
 #pragma once
 
 #include "launch.hpp"

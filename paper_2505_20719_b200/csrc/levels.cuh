@@ -46,6 +46,7 @@ struct Gate {
 struct Sync {
   double* partials;   // gridDim.x * kMaxPart
   unsigned* counter;  // last-block counter
+  int seq;            // sequential index-order reductions (validation mode, common.cuh seq_sums)
 };
 
 // Cross-rank completion of a reduction under the row-block partition (P > 1,
@@ -134,7 +135,14 @@ __global__ void __launch_bounds__(256) k_level_start(void* src, const double* sr
     block_sum<PW, 1>(acc, scratch);
     if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
     if (!last_block(sync.counter)) return;
-    reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (sync.seq) {
+      seq_sums<PW>(n, 1, [&](uint64_t i, int) {
+        const T_<PW> d = ldcg<PW>(dst, i);
+        return Ar<PW>::mul(d, d);
+      }, tot);
+    } else {
+      reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    }
     if (publish_local(dist, 1, tot)) return;
   } else {
     combine_ranks<PW>(dist, 1, tot);
@@ -245,7 +253,15 @@ __device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& 
     for (int k = 0; k < 8; ++k) dots[(size_t)blockIdx.x * kMaxPart + k] = k < ND ? Ar<PW>::wide(dd[k]) : 0.0;
   if (defer) return;
   if (!last_block(sync.counter)) return;
-  reduce_partials<PW, ND>(dots, gridDim.x, kMaxPart, res, scratch);
+  if (sync.seq) {  // h_k = dot(w, v_k) in index order, v_k = fl(s_k w_k) (src/fgmres.cpp:71-73)
+    const uint64_t n = A.n;
+    seq_sums<PW>(n, ND, [&](uint64_t i, int k) {
+      const T_<PW> vk = Ar<PW>::mul(cvt<PW>(L->scale[k]), ldcg<PW>(V, (uint64_t)k * ld + i));
+      return Ar<PW>::mul(ldcg<PW>(e.w, i), vk);
+    }, res);
+  } else {
+    reduce_partials<PW, ND>(dots, gridDim.x, kMaxPart, res, scratch);
+  }
   if (publish_local(dist, ND, res)) return;
   if (threadIdx.x == 0)
     for (int k = 0; k < ND; ++k) L->H[(size_t)j * (L->m + 1) + k] = res[k];
@@ -314,7 +330,14 @@ __global__ void __launch_bounds__(256) k_multi_dot(const void* V, uint64_t n, ui
   if (threadIdx.x == 0)
     for (int k = 0; k < 8; ++k) sync.partials[(size_t)blockIdx.x * kMaxPart + k] = Ar<PW>::wide(d[k]);
   if (!last_block(sync.counter)) return;
-  reduce_partials<PW, 8>(sync.partials, gridDim.x, kMaxPart, res, scratch);
+  if (sync.seq) {
+    seq_sums<PW>(n, nd, [&](uint64_t i, int k) {
+      const T_<PW> vk = Ar<PW>::mul(cvt<PW>(L->scale[k0 + k]), ldcg<PW>(V, (uint64_t)(k0 + k) * ldv + i));
+      return Ar<PW>::mul(ldcg<PW>(V, (uint64_t)(j + 1) * ldv + i), vk);
+    }, res);
+  } else {
+    reduce_partials<PW, 8>(sync.partials, gridDim.x, kMaxPart, res, scratch);
+  }
   if (publish_local(dist, nd, res)) return;
   if (threadIdx.x == 0)
     for (int k = 0; k < nd; ++k) L->H[(size_t)j * (L->m + 1) + k0 + k] = res[k];
@@ -470,7 +493,15 @@ __device__ __forceinline__ void cgs_body(void* V, uint64_t n, uint64_t ldv, int 
     if (threadIdx.x == 0) gj_tol[0] = __ldcg(L->g + j), gj_tol[1] = L->tol, gj_tol[2] = L->bnorm;
   }
   if (dist.mode != 2) {
-    reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);  // ends with __syncthreads
+    if (sync.seq) {  // ||w||^2 in index order (norm2, src/fgmres.cpp:77)
+      T_<PW>* w = static_cast<T_<PW>*>(V) + (size_t)(j + 1) * ldv;
+      seq_sums<PW>(n, 1, [&](uint64_t i, int) {
+        const T_<PW> wi = ldcg<PW>(w, i);
+        return A::mul(wi, wi);
+      }, tot);
+    } else {
+      reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);  // ends with __syncthreads
+    }
     if (publish_local(dist, 1, tot)) return;
   } else {
     combine_ranks<PW>(dist, 1, tot);
@@ -692,7 +723,14 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_residual(CsrDev A, Tile
     block_sum<PW, 1>(acc, scratch);
     if (threadIdx.x == 0) sync.partials[(size_t)blockIdx.x * kMaxPart] = Ar<PW>::wide(acc[0]);
     if (!last_block(sync.counter)) return;
-    reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (sync.seq) {
+      seq_sums<PW>(A.n, 1, [&](uint64_t i, int) {
+        const T_<PW> ri = ldcg<PW>(r, i);
+        return Ar<PW>::mul(ri, ri);
+      }, tot);
+    } else {
+      reduce_partials<PW, 1>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    }
     if (publish_local(dist, 1, tot)) return;
   } else {
     combine_ranks<PW>(dist, 1, tot);

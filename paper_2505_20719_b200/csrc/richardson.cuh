@@ -93,12 +93,14 @@ struct EpiDotsRs {
   T_<CD> num, den;
   T_<PW> rr;
   T_<PV> vraw;
+  void* S = nullptr;  // sequential reductions: s materialised for the in-order recomputation
   __device__ __forceinline__ void prefetch(uint32_t i) {
     if (R) rr = ldcg<PW>(R, i);
     else vraw = rhs.raw_row(i);
   }
   __device__ __forceinline__ void row(uint32_t i, T_<C> acc) {
     const T_<PW> s = cvt<PW>(acc);
+    if (S) st<PW>(S, i, s);
     const T_<PW> r = R ? rr : rhs.apply(vraw);
     num = Ar<CD>::add(num, Ar<CD>::mul(cvt<CD>(r), cvt<CD>(s)));
     den = Ar<CD>::add(den, Ar<CD>::mul(cvt<CD>(s), cvt<CD>(s)));
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_richardson(CsrDev A, Ti
       }
       {
         EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? RS->R : nullptr, Ar<CD>::zero(), Ar<CD>::zero(), {}, {}};
+        if (sync.seq) e.S = RS->Zb;
         if (k == 0) {
           struct GatherRhs {
             using Raw = T_<PV>;
@@ -216,6 +219,20 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_richardson(CsrDev A, Ti
         grid_barrier(bar_count, bar_gen);
         // every CTA reduces the partials in the same fixed order -> identical w'
         reduce_partials<CD, 2>(sync.partials, gridDim.x, kMaxPart, red, scratch);
+        if (sync.seq) {  // (r, s), (s, s) in index order (dot_at_least, src/richardson.cpp:32-33)
+          grid_barrier(bar_count, bar_gen);  // every CTA is done with the partials
+          if (blockIdx.x == 0) {
+            seq_sums<CD>(n, 2, [&](uint64_t i, int q) {
+              const T_<CD> sv = cvt<CD>(ldcg<PW>(RS->Zb, i));
+              const T_<CD> rv = q ? sv : cvt<CD>(k > 0 ? ldcg<PW>(RS->R, i) : rhs.row(i));
+              return Ar<CD>::mul(rv, sv);
+            }, red);
+            if (threadIdx.x == 0) sync.partials[0] = red[0], sync.partials[1] = red[1];
+          }
+          grid_barrier(bar_count, bar_gen);
+          if (threadIdx.x == 0) red[0] = __ldcg(sync.partials), red[1] = __ldcg(sync.partials + 1);
+          __syncthreads();
+        }
       }
       const double num = red[0], den = red[1];
       double wk;
@@ -410,6 +427,7 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_richm_phase(CsrDev A, T
     if (!update) return;
     GatherCG<PW, C> g{P};
     EpiDotsRs<PV, PW, C, CD> e{rhs, R, Ar<CD>::zero(), Ar<CD>::zero(), {}, {}};
+    if (sync.seq) e.S = RS->Zb;
     spmv_tiles<PA, C, IDX, rich_chunk(IDX)>(A, T, g, e, smem);
     T_<CD> acc[2] = {e.num, e.den};
     block_sum<CD, 2>(acc, scratch);
@@ -418,7 +436,14 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_richm_phase(CsrDev A, T
       sync.partials[(size_t)blockIdx.x * kMaxPart + 1] = Ar<CD>::wide(acc[1]);
     }
     if (!last_block(sync.counter)) return;
-    reduce_partials<CD, 2>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    if (sync.seq) {
+      seq_sums<CD>(n, 2, [&](uint64_t i, int q) {
+        const T_<CD> sv = cvt<CD>(ldcg<PW>(RS->Zb, i));
+        return Ar<CD>::mul(q ? sv : cvt<CD>(ldcg<PW>(R, i)), sv);
+      }, tot);
+    } else {
+      reduce_partials<CD, 2>(sync.partials, gridDim.x, kMaxPart, tot, scratch);
+    }
     if (threadIdx.x == 0) {
       const double num = tot[0], den = tot[1];
       if (den == 0.0 || !isfinite(num) || !isfinite(den)) {
