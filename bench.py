@@ -1,23 +1,27 @@
 #!/usr/bin/env python
 """bench.py -- time-to-solution of the fp16-F3R solve (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
 
 One "step" = one complete fp16-F3R solve (F100:f64/f64 > F8:f32/f32 > F4:f16/f32 >
-R2:f16,c=64, identity M) of BASELINE config 2 (27-point 128^3, n = 2,097,152,
-nnz = 55,742,968, x_true ~ U[-1,1] seed 1) to relative residual 1e-10, from a
-zero initial guess, inputs resident in HBM. The matrix replicas (A16 + indices
-alone: 334 MB) exceed the 126 MB L2, so no explicit flush is needed between steps.
+R2:f16,c=64, identity M) to relative residual 1e-10 from a zero initial guess,
+inputs resident in HBM. Default workload: BASELINE config 5, the largest
+configuration that fits one GPU (unstructured n = 20,000,000, ~6.0e8 entries,
+seed 4); --config 1..4 select the others. Every config's matrix streams exceed the
+126 MB L2 except config 1's (L2-resident), so no flush is
+needed between steps. Inputs come from the binary CSR cache (csr_cache.py,
+written once per host by lib/f3rg_gen), the same bytes for both arms.
 
 Printed JSON line (rank 0): value = mean time-to-solution (s, lower is better),
 e2e = the same solve through the C ABI with host buffers (pinned b in, x out),
 roofline = the dominant kernel's achieved HBM GB/s (algorithmic bytes, SURVEY.md
 §8(d)) over the measured copy peak, cpu_baseline = the unmodified reference CPU
-solver on this host (one outer iteration, extrapolated to the full count).
+solver on this host: a bounded sample (SAMPLES_PER_OUTER) scaled by its own
+recorded outer count.
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, built from
-/root/reference/proj/src) on all host threads; each step = one outer iteration
-of the same config, value extrapolated to the reference's full outer count.
+/root/reference/proj/src) on all host threads, fed from the binary CSR cache
+(this process never maps libf3rg.so); each step = the same bounded sample.
 """
 from __future__ import annotations
 
@@ -100,27 +104,29 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
 
 
-# DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from the
-# committed `ncu --set full` capture of config 2 (profiles/r01_ncu_full.md, P16 rows)
-TRAFFIC = {"richardson[f16,f16,f32]": 256101120.0, "spmv_dots[f16,f16,f32]": 261074688.0}
+PSIZE = {0: 2, 1: 4, 2: 8}
+PNAME = {"f16": 0, "f32": 1, "f64": 2}
+
+
+def traffic_table():
+    """measured DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of the top kernels, per config, from the committed `ncu --set full` captures
+    (profiles/traffic.json, written by tools/summarize_ncu.py)"""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        return {}
 
 
 def streams_matrix(kernel):
     return kernel.split("[")[0] in ("richardson", "spmv_dots", "spmv", "residual")
 
 
-def column_stream_saving(p):
-    """u32 column bytes minus D16 bytes (u16 deltas + u32 first column per row) when
-    the engine uses the D16 stream (every in-row gap < 2^16, F3RG_COLUMNS unset)."""
-    if os.environ.get("F3RG_COLUMNS") == "u32" or p.nnz == 0:
-        return 0.0
-    rp = p.row_ptr.astype(np.int64)
-    gaps = np.diff(p.col_idx.astype(np.int64))
-    inrow = np.ones(len(gaps), dtype=bool)
-    inrow[rp[1:-1][(rp[1:-1] > 0) & (rp[1:-1] < p.nnz)] - 1] = False
-    if len(gaps) and gaps[inrow].max(initial=0) > 0xFFFF:
-        return 0.0
-    return 4.0 * p.nnz - (2.0 * p.nnz + 4.0 * p.n)
+def column_stream_saving(reps, p, pa):
+    """the reference's u32-CSR bytes of one pass over replica pa (SURVEY 8(d):
+    nnz (sA + 4) + 4 (n + 1)) minus the bytes the device actually streams (its
+    compressed column stream, f3rg_matrix_stream_bytes)"""
+    return float(p.nnz * (PSIZE[pa] + 4) + 4 * (p.n + 1) - reps.stream_bytes(pa))
 
 
 def spmv_per_precision(f, torch, reps, p, reps_n=20):
@@ -130,9 +136,8 @@ def spmv_per_precision(f, torch, reps, p, reps_n=20):
     resident; the 223-446 MB matrix streams exceed the 126 MB L2). GB/s by SURVEY
     8(d)'s algorithmic bytes nnz (sA + 4) + 4 (n + 1) + n (sx + sy) -- the reference's
     u32 CSR -- and by the bytes actually streamed (D16/P16 column streams)."""
-    size = {0: 2, 1: 4, 2: 8}
+    size = PSIZE
     peak, _ = _peaks()
-    saving = column_stream_saving(p)
     out = []
     for pa, px, py, role in ((2, 2, 2, "L1 / true residual"), (1, 1, 1, "L2"), (0, 1, 1, "L3"),
                              (0, 0, 0, "Richardson operand")):
@@ -150,7 +155,7 @@ def spmv_per_precision(f, torch, reps, p, reps_n=20):
         torch.cuda.synchronize()
         us = 1e3 * e0.elapsed_time(e1) / reps_n
         algo = p.nnz * (size[pa] + 4) + 4 * (p.n + 1) + p.n * (size[px] + size[py])
-        streamed = algo - saving
+        streamed = algo - column_stream_saving(reps, p, pa)
         out.append({"precision": f"A f{8 * size[pa]}, x f{8 * size[px]}, y f{8 * size[py]}", "role": role,
                     "us": round(us, 2), "algorithmic_gbs": round(algo / us / 1e3, 1),
                     "streamed_gbs": round(streamed / us / 1e3, 1), "frac": round(algo / us / 1e3 / peak, 4),
@@ -170,19 +175,46 @@ def reference_runs():
         return {}
 
 
-def cpu_reference_sample(p, outer_full: int, threads: int, sample_outer: int = 1, args=None):
-    """Times the UNMODIFIED reference solve for `sample_outer` outer iterations
-    (RunOptions.max_outer_total, include/f3r/nesting.hpp:35); returns seconds per
-    outer iteration and the extrapolated time-to-solution."""
-    from oracle_bind import Reference
-    r = Reference()
-    r.set_threads(threads)
-    m = r.matrix(p.row_ptr, p.col_idx, p.values)
-    M = _ref_m(r, m, args)
-    rep = r.solve(m, spec_for(args) if args else SPEC, p.b, tol=TOL, max_outer_total=sample_outer, want_x=False,
-                  precond=M)
-    per_outer = rep.wall_seconds / max(1, rep.outer_iterations)
-    return per_outer, per_outer * outer_full, rep
+# Reference CPU sample per step, sized so one step is ~5-15 s on the box's cores:
+# a full outer iteration (configs 1-2), one L2 Arnoldi step = 1/8 of an outer
+# iteration (configs 3-4: one F4 > R2 invocation below it), or one L3 Arnoldi step
+# = 1/32 (config 5: one Richardson call plus its fp16-matrix SpMV and Gram-Schmidt).
+# Each sample is a ComposedSolver::run of the unmodified reference with the
+# nest's lower levels as its levels and max_outer_total = 1 (include/f3r/nesting.hpp:35).
+SAMPLES_PER_OUTER = {1: 1, 2: 1, 3: 8, 4: 8, 5: 32}
+
+
+def sample_spec(args, per_outer):
+    levels = [t.strip() for t in spec_for(args).split(">")]
+    return " > ".join(levels[{1: 0, 8: 1, 32: 2}[per_outer]:])
+
+
+def sample_desc(per_outer):
+    return {1: "1 outer iteration", 8: "1 L2 Arnoldi step (1/8 of an outer iteration)",
+            32: "1 innermost-FGMRES Arnoldi step (1/32 of an outer iteration: one fp16 Richardson call, "
+                "one fp16-matrix SpMV and its Gram-Schmidt)"}[per_outer]
+
+
+class ReferenceSampler:
+    """the UNMODIFIED reference (oracle/_ref/libf3r_ref.so) on this host's cores,
+    fed from the binary CSR cache (csr_cache: this process never maps libf3rg.so)"""
+
+    def __init__(self, args, p, threads):
+        from oracle_bind import Reference
+        self.r = Reference()
+        self.r.set_threads(threads)
+        self.m = self.r.matrix(p.row_ptr, p.col_idx, p.values)
+        self.M = _ref_m(self.r, self.m, args)
+        self.b = np.ascontiguousarray(p.b)
+        self.per_outer = SAMPLES_PER_OUTER.get(args.config, 1)
+        self.spec = sample_spec(args, self.per_outer)
+
+    def step(self):
+        rep = self.r.solve(self.m, self.spec, self.b, tol=TOL, max_outer_total=1, want_x=False, precond=self.M)
+        return rep.wall_seconds
+
+    def full(self, args):
+        return self.r.solve(self.m, spec_for(args), self.b, tol=TOL, want_x=False, precond=self.M)
 
 
 def _ref_m(r, m, args):
@@ -197,53 +229,85 @@ def _mode_key(args):
     return "fp16-f3r" if args.precond == "identity" else f"fp16-f3r-{args.precond}"
 
 
+def cpu_context(args):
+    """the reference's recorded full runs of the three F3R modes (src/nesting.cpp:359-386)
+    for this config: SURVEY 8(d)'s context beside the fp16-F3R baseline"""
+    runs = reference_runs()
+    out = {}
+    for mode in ("fp16-f3r", "fp32-f3r", "fp64-f3r"):
+        r = runs.get(f"config{args.config}/{mode}")
+        if r:
+            out[mode] = {"seconds": r["wall_seconds"], "outer": r["outer_iterations"], "threads": r["threads"],
+                         "where": "full run in the build container (tests/golden/reference_runs.json)"}
+    return out
+
+
+def reference_outer(args, smp):
+    """the reference's own outer count for this config (recorded full run); None if
+    there is none and the sample is sub-outer (a full run would take too long)"""
+    runs = reference_runs().get(f"config{args.config}/{_mode_key(args)}", {})
+    outer_full = int(runs.get("outer_iterations", 0)) or None
+    if outer_full is None and smp.per_outer == 1:
+        outer_full = smp.full(args).outer_iterations  # small config: measure the count once
+    return outer_full
+
+
 def run_reference_arm(args):
     rank, _, world = dist_env()
     if rank != 0:
         return
-    from paper_2505_20719_b200 import problems
-    p = problems.problem(args.config)
-    threads = os.cpu_count()
-    runs = reference_runs().get(f"config{args.config}/{_mode_key(args)}", {})
-    outer_full = int(runs.get("outer_iterations", 0)) or None
-    from oracle_bind import Reference, reference_available
+    from oracle_bind import reference_available
+
+    from paper_2505_20719_b200 import csr_cache  # reads the cache; never loads libf3rg.so
     if not reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libf3r_ref.so not built"}))
         return
-    r = Reference()
-    r.set_threads(threads)
-    m = r.matrix(p.row_ptr, p.col_idx, p.values)
-    M = _ref_m(r, m, args)
-    spec = spec_for(args)
-    if outer_full is None:  # no committed full run for this config: measure it once
-        full = r.solve(m, spec, p.b, tol=TOL, want_x=False, precond=M)
-        outer_full = full.outer_iterations
-    for _ in range(min(args.warmup, 1)):
-        r.solve(m, spec, p.b, tol=TOL, max_outer_total=1, want_x=False, precond=M)
-    times = []
-    for _ in range(args.steps):
-        rep = r.solve(m, spec, p.b, tol=TOL, max_outer_total=1, want_x=False, precond=M)
-        times.append(rep.wall_seconds)
-    per_outer = float(np.mean(times))
-    value = per_outer * outer_full
-    sample = (f"1 outer iteration (of {outer_full}) of the reference fp16-F3R solve per step, "
-              f"config {args.config}; value = mean x {outer_full}")
+    p = csr_cache.load(args.config)
+    threads = os.cpu_count()
+    smp = ReferenceSampler(args, p, threads)
+    outer_full = reference_outer(args, smp)
+    if outer_full is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"no recorded full reference run for config "
+                          f"{args.config} ({_mode_key(args)}) to scale the sample by"}))
+        return
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        smp.step()
+    times = [smp.step() for _ in range(args.steps)]
+    per_step = float(np.mean(times))
+    value = per_step * smp.per_outer * outer_full
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": min(args.warmup, 1), "ms_per_step": per_outer * 1e3, "higher_is_better": False,
+        "warmup": warm, "ms_per_step": per_step * 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "mixed f64/f32/f16 (software binary16)",
         "data": "synthetic", "config": _config(args, p),
-        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "reference", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "reference",
+                         "sample": sample_text(args, smp, outer_full)},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "inputs": f"binary CSR cache {os.path.basename(p.path)} (lib/f3rg_gen)",
     }
     print(json.dumps(line))
+
+
+def sample_text(args, smp, outer_full):
+    return (f"{sample_desc(smp.per_outer)} of the unmodified reference fp16-F3R solve per step "
+            f"(ComposedSolver::run of '{smp.spec}', max_outer_total 1), config {args.config}; "
+            f"value = mean x {smp.per_outer} x {outer_full} outer iterations (the reference's own count)")
+
+
+def l2_note(p):
+    a16 = p.nnz * 6 + 4 * (p.n + 1)  # fp16 values + u32 indices + row pointers
+    if a16 > 126e6:
+        return (f"none: every pass streams a matrix replica of >= {a16 / 1e6:.0f} MB (fp16 + u32 indices), "
+                f"larger than the 126 MB L2")
+    return f"none: the {a16 / 1e6:.0f} MB fp16 replica is L2-resident (config 1 caveat, SURVEY 8(d))"
 
 
 def _config(args, p):
     mname = "identity" if args.precond == "identity" else f"block-Jacobi {args.precond}, 4 blocks, fp16 factors"
     return {"workload": f"BASELINE config {args.config}: fp16-F3R solve to 1e-10 (M = {mname})", "n": p.n,
             "nnz": p.nnz, "solver": spec_for(args), "problem": p.name, "tol": TOL,
-            "l2_flush": "none: working set (A16+idx 334 MB, A32+idx 446 MB) exceeds the 126 MB L2",
+            "l2_flush": l2_note(p),
             "parallelism": f"dp{args.gpus}" if args.gpus > 1 else "single GPU"}
 
 
@@ -256,7 +320,7 @@ def run_partitioned(args):
     import torch.distributed as dist
 
     import paper_2505_20719_b200 as f
-    from paper_2505_20719_b200 import partition, problems
+    from paper_2505_20719_b200 import csr_cache, partition
 
     rank, local, world = dist_env()
     torch.cuda.set_device(local)
@@ -264,7 +328,7 @@ def run_partitioned(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("cpu:gloo,cuda:nccl", rank=rank, world_size=world)
-    p = problems.problem(args.config)
+    p = csr_cache.load(args.config)
     a = f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values)
     uid = [partition.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
@@ -317,6 +381,7 @@ def run_partitioned(args):
     part.solver.set_profile(False)
     prof = part.solver.profile()
     launches = int(sum(k[2] for k in prof))
+    halos, reds = part.solver.collectives()
     streaming = [k for k in prof if k[3] > 0]
     top = max(streaming, key=lambda k: k[1])
     peak, peak_kind = _peaks()
@@ -335,7 +400,9 @@ def run_partitioned(args):
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(gbs / peak, 4), "traffic": None,
                      "bytes": "streamed bytes of rank 0's rows (its ext-layout CSR)",
                      "avg_launch_us": per_launch_ms * 1e3},
-        "partition": {"rows_rank0": pl.r1 - pl.r0, "halo_rank0": pl.n_lo + pl.n_hi},
+        "partition": {"rows_rank0": pl.r1 - pl.r0, "halo_rank0": pl.n_lo + pl.n_hi,
+                      "collectives_per_outer": {"halo_exchanges": halos / max(1, rep.outer_iterations),
+                                                "reductions": reds / max(1, rep.outer_iterations)}},
     }
     if rank == 0:
         print(json.dumps(line))
@@ -347,7 +414,7 @@ def run_ours(args):
     import torch
 
     import paper_2505_20719_b200 as f
-    from paper_2505_20719_b200 import problems
+    from paper_2505_20719_b200 import csr_cache
 
     rank, local, world = dist_env()
     if world > 1 or args.partition:
@@ -355,7 +422,7 @@ def run_ours(args):
             raise SystemExit("--precond: the row-block partition runs M = identity only (DESIGN.md section 6c)")
         return run_partitioned(args)
     torch.cuda.set_device(local)
-    p = problems.problem(args.config)
+    p = csr_cache.load(args.config)  # the same bytes the reference arm reads
     reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
     if args.precond == "identity":
         M = f.IdentityPrecond(p.n)
@@ -364,7 +431,7 @@ def run_ours(args):
                                         f.IluConfig(4, 1.0, args.precond == "ic0", f.Precision.P16))
     solver = f.build(f.parse_solver_spec(spec_for(args)), reps, M)
     opts = f.RunOptions(tol=TOL)
-    b_dev = torch.from_numpy(p.b).cuda()
+    b_dev = torch.from_numpy(np.array(p.b)).cuda()
     stream = torch.cuda.current_stream()
 
     # every step is a fresh solve: the reference's run_once builds a new
@@ -392,7 +459,7 @@ def run_ours(args):
         raise SystemExit(f"timed solve did not converge: {run.report}")
 
     # ---- e2e: through the C ABI with host buffers (pinned b in, x out) ----
-    b_host = torch.from_numpy(p.b).pin_memory().numpy()
+    b_host = torch.from_numpy(np.array(p.b)).pin_memory().numpy()
     x_host = torch.empty(p.n, dtype=torch.float64).pin_memory().numpy()
     e2e_t = []
     # one untimed warm-up through the host-buffer entry point (its first call
@@ -423,7 +490,8 @@ def run_ours(args):
     # profile bytes are what the kernel streams (D16 column stream when in use);
     # SURVEY.md 8(d)'s algorithmic unit counts the reference's u32 CSR instead
     per_launch_bytes = top[3] / top[2]
-    algo_bytes = per_launch_bytes + (column_stream_saving(p) if streams_matrix(top[0]) else 0.0)
+    top_pa = PNAME.get(top[0].split("[")[1].split(",")[0], 2) if "[" in top[0] else 2
+    algo_bytes = per_launch_bytes + (column_stream_saving(reps, p, top_pa) if streams_matrix(top[0]) else 0.0)
     achieved = algo_bytes / (per_launch_ms * 1e-3) / 1e9
     streamed = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
     breakdown = sorted(prof, key=lambda k: -k[1])
@@ -438,7 +506,8 @@ def run_ours(args):
         "outer_iterations": outer, "final_true_residual": run.report.final_true_residual,
         "roofline": {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": TRAFFIC.get(top[0]), "algorithmic_bytes_per_launch": algo_bytes,
+                     "traffic": traffic_table().get(f"config{args.config}", {}).get(top[0]),
+                     "algorithmic_bytes_per_launch": algo_bytes,
                      "streamed_bytes_per_launch": per_launch_bytes, "achieved_streamed": round(streamed, 1),
                      "frac_streamed": round(streamed / peak, 4), "avg_launch_us": per_launch_ms * 1e3},
         "kernels": kernels,
@@ -455,13 +524,16 @@ def run_ours(args):
                            "apply_ms": round(apply_ms, 4), "sweep_levels": list(lv),
                            "us_per_level": round(1e3 * apply_ms / (lv[0] + lv[1]), 3), "bound": "latency"}
     if not args.no_cpu_baseline:
-        try:
+        try:  # the unmodified reference on this host's cores, a bounded sample (SAMPLES_PER_OUTER)
             threads = os.cpu_count()
-            per_outer, extrap, rep = cpu_reference_sample(p, outer, threads, args=args)
-            line["cpu_baseline"] = {"value": extrap, "unit": "s", "cores": threads, "kind": "reference",
-                                    "sample": f"1 outer iteration of the unmodified reference fp16-F3R solve "
-                                              f"(M = {args.precond}; {per_outer:.2f} s), extrapolated "
-                                              f"x{outer} outer iterations"}
+            smp = ReferenceSampler(args, p, threads)
+            outer_ref = reference_outer(args, smp)
+            smp.step()  # warm-up (page faults, thread pool)
+            per_step = float(np.mean([smp.step() for _ in range(2)]))
+            line["cpu_baseline"] = {"value": per_step * smp.per_outer * (outer_ref or outer), "unit": "s",
+                                    "cores": threads, "kind": "reference",
+                                    "sample": sample_text(args, smp, outer_ref or outer) + f"; {per_step:.2f} s/step",
+                                    "context_modes": cpu_context(args)}
         except Exception as e:  # keep the GPU line even if the CPU leg fails
             line["cpu_baseline"] = {"value": None, "unit": "s", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"failed: {e}"}
@@ -473,7 +545,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5,
+                    help="BASELINE config (default 5: the largest single-GPU configuration)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--precond", default="identity", choices=["identity", "ic0", "ilu0"],

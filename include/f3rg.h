@@ -96,6 +96,9 @@ int f3rg_matrix_create(f3rg_matrix** out, const f3rg_csr* a64);
 void f3rg_matrix_destroy(f3rg_matrix* a);
 uint64_t f3rg_matrix_rows(const f3rg_matrix* a);
 uint64_t f3rg_matrix_nnz(const f3rg_matrix* a);
+/* bytes one device pass over replica `prec` streams (values + the compressed column
+ * stream in use + row pointers); the reference's u32 CSR is nnz*(s+4) + 4(n+1) */
+uint64_t f3rg_matrix_stream_bytes(const f3rg_matrix* a, int prec);
 /* replica values widened to fp64 into host memory (nnz doubles) */
 int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host);
 
@@ -187,6 +190,9 @@ int f3rg_solver_set_profile(f3rg_solver* s, int on);
 /* kernel i of the last profiled solve: name, total ms, launches, algorithmic bytes */
 int f3rg_solver_profile_entry(const f3rg_solver* s, uint64_t i, char* name, size_t cap, double* ms,
                               uint64_t* launches, double* bytes);
+/* row-block partition: halo exchanges and cross-rank reductions (allgathers) the last
+ * profiled solve enqueued on this rank (0 on one rank) */
+int f3rg_solver_collectives(const f3rg_solver* s, uint64_t* halos, uint64_t* reductions);
 
 /* ---- kernel-level entry points (device pointers, stream = cudaStream_t or 0) ---
  * Each mirrors one reference free function, same argument meaning. */

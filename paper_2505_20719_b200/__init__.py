@@ -99,6 +99,8 @@ def lib():
     vp, u64, i32, dbl = C.c_void_p, C.c_uint64, C.c_int, C.c_double
     L.f3rg_last_error.restype = C.c_char_p
     L.f3rg_set_seq_reductions.argtypes = [i32]
+    L.f3rg_matrix_stream_bytes.argtypes = [vp, i32]
+    L.f3rg_matrix_stream_bytes.restype = u64
     L.f3rg_version.restype = C.c_char_p
     L.f3rg_matrix_create.argtypes = [C.POINTER(vp), C.POINTER(_Csr)]
     L.f3rg_matrix_destroy.argtypes = [vp]
@@ -407,6 +409,10 @@ class PrecisionReplicas:
 
     def rows(self) -> int:
         return self.dev.n
+
+    def stream_bytes(self, p: Precision) -> int:
+        """bytes one device pass over replica p streams (compressed column stream)"""
+        return int(lib().f3rg_matrix_stream_bytes(self.dev.h, int(p)))
 
 
 def make_replicas(a64: SparseCsr) -> PrecisionReplicas:
@@ -732,6 +738,12 @@ class ComposedSolver:
 
     def set_profile(self, on: bool = True) -> None:
         lib().f3rg_solver_set_profile(self.h, int(on))
+
+    def collectives(self) -> tuple:
+        """(halo exchanges, cross-rank reductions) the last profiled run enqueued"""
+        h, r = C.c_uint64(), C.c_uint64()
+        _check(lib().f3rg_solver_collectives(self.h, C.byref(h), C.byref(r)))
+        return h.value, r.value
 
     def profile(self) -> list:
         """[(kernel, total_ms, launches, algorithmic_bytes)] of the last profiled run"""

@@ -79,12 +79,12 @@ def build_lib(force: bool = False, jobs: int = 8, verbose: bool = False, defines
         LIB = os.path.join(LIBDIR, "variants", f"libf3rg_{name}.so")
         os.makedirs(os.path.dirname(LIB), exist_ok=True)
     try:
-        return _build_lib(force, jobs, verbose, [f"-D{d}" for d in defines])
+        return _build_lib(force, jobs, verbose, [f"-D{d}" for d in defines], name)
     finally:
         OBJDIR, LIB = saved
 
 
-def _build_lib(force, jobs, verbose, dflags):
+def _build_lib(force, jobs, verbose, dflags, name=""):
     os.makedirs(LIBDIR, exist_ok=True)
     os.makedirs(OBJDIR, exist_ok=True)
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.hpp")) + \
@@ -117,6 +117,12 @@ def _build_lib(force, jobs, verbose, dflags):
                                                      "-lpthread"] + _gomp_flags() + _stdcxx_flags() + \
             ["-Wl,-soname,libf3rg.so", "-Wl,--no-undefined"]
         _run(cmd, os.path.join(OBJDIR, "link.log"))
+    # standalone binary-CSR cache writer (host code only, no CUDA): csr_cache.py
+    gen = os.path.join(LIBDIR, "f3rg_gen")
+    gsrc = [os.path.join(CSRC, "problem_gen.cpp"), os.path.join(CSRC, "problems.cpp")]
+    if not name and (force or not os.path.exists(gen) or os.path.getmtime(gen) < max(_newest(gsrc), hdr_time)):
+        _run([CXX] + CXX_FLAGS + _gomp_flags() + gsrc + ["-o", gen] + _stdcxx_flags(),
+             os.path.join(OBJDIR, "f3rg_gen.log"))
     if verbose:
         print(f"built {LIB}")
     return LIB

@@ -135,6 +135,9 @@ int f3rg_matrix_create(f3rg_matrix** out, const f3rg_csr* a) {
 void f3rg_matrix_destroy(f3rg_matrix* a) { delete a; }
 uint64_t f3rg_matrix_rows(const f3rg_matrix* a) { return a ? a->m->rows() : 0; }
 uint64_t f3rg_matrix_nnz(const f3rg_matrix* a) { return a ? a->m->nnz() : 0; }
+uint64_t f3rg_matrix_stream_bytes(const f3rg_matrix* a, int prec) {
+  return a && prec >= 0 && prec <= 2 ? (uint64_t)a->m->stream_bytes(prec) : 0;
+}
 
 int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host) {
   return guarded([&] {
@@ -338,6 +341,13 @@ uint64_t f3rg_solver_omega_count(const f3rg_solver* s) {
   return n;
 }
 
+int f3rg_solver_collectives(const f3rg_solver* s, uint64_t* halos, uint64_t* reductions) {
+  if (!s || !halos || !reductions) return F3RG_EDIMENSION;
+  *halos = s->s->halos();
+  *reductions = s->s->reductions();
+  return F3RG_OK;
+}
+
 int f3rg_solver_set_profile(f3rg_solver* s, int on) {
   s->s->set_profile(on != 0);
   return F3RG_OK;
@@ -476,6 +486,9 @@ int f3rg_richardson_set_omegas(f3rg_richardson* r, const double* w) {
   return guarded([&] {
     F3RG_CUDA(cudaDeviceSynchronize());
     F3RG_CUDA(cudaMemcpy(r->omegas.get(), w, (size_t)r->m * 8, cudaMemcpyHostToDevice));
+    // a pageable H2D cudaMemcpy may return before its DMA lands; applies run on
+    // other (non-blocking) streams, so wait for it here
+    F3RG_CUDA(cudaDeviceSynchronize());
   });
 }
 

@@ -249,6 +249,53 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// ---- L2 eviction priorities --------------------------------------------------------
+// A pass streams the matrix once and gathers a vector many times over (config 5:
+// a 40 MB fp16 x, ~37 reads of every element per pass). With the hints on, the
+// stream is loaded evict-first and the gathers evict-last, so the vector stays in
+// the 126 MB L2 instead of being pushed out by the stream (TilesDev::l2hint).
+__device__ __forceinline__ uint64_t l2_policy(int kind) {  // 0 normal, 1 evict-first, 2 evict-last
+  uint64_t p;
+  if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+// element i of a precision-tagged array with an L2 policy; CACHE: "nc" (read-only
+// path), "cg" (L2 only) or "ca" (L1-allocating)
+#define F3RG_LD_HINT(NAME, QUAL)                                                                              \
+  template <int P>                                                                                            \
+  __device__ __forceinline__ T_<P> NAME(const void* p, uint64_t i, uint64_t pol) {                            \
+    if constexpr (P == P16) {                                                                                 \
+      unsigned short v;                                                                                       \
+      asm volatile("ld.global." QUAL ".L2::cache_hint.u16 %0, [%1], %2;"                                      \
+                   : "=h"(v) : "l"(static_cast<const unsigned short*>(p) + i), "l"(pol));                      \
+      return __ushort_as_half(v);                                                                             \
+    } else if constexpr (P == P32) {                                                                          \
+      float v;                                                                                                \
+      asm volatile("ld.global." QUAL ".L2::cache_hint.f32 %0, [%1], %2;"                                      \
+                   : "=f"(v) : "l"(static_cast<const float*>(p) + i), "l"(pol));                              \
+      return v;                                                                                               \
+    } else {                                                                                                  \
+      double v;                                                                                               \
+      asm volatile("ld.global." QUAL ".L2::cache_hint.f64 %0, [%1], %2;"                                      \
+                   : "=d"(v) : "l"(static_cast<const double*>(p) + i), "l"(pol));                             \
+      return v;                                                                                               \
+    }                                                                                                         \
+  }
+F3RG_LD_HINT(ldg_hint, "nc")
+F3RG_LD_HINT(ldcg_hint, "cg")
+F3RG_LD_HINT(ldca_hint, "ca")
+#undef F3RG_LD_HINT
+
 // ---- deterministic reductions ----------------------------------------------------
 // Fixed-shape trees: the result depends only on the inputs' positions, never on
 // scheduling, so repeated solves are bitwise identical (reference

@@ -120,7 +120,7 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
   const bool p16 = !(colfmt && (std::string(colfmt) == "u32" || std::string(colfmt) == "d16"));
   for (uint64_t i = 0; d16 && i < n_; ++i)
     for (uint32_t k = row_ptr[i] + 1; k < row_ptr[i + 1]; ++k)
-      if (col_idx[k] - col_idx[k - 1] > 65535u) {
+      if (col_idx[k] - col_idx[k - 1] > 65536u) {  // stored as gap - 1 (columns strictly increase)
         d16 = false;
         break;
       }
@@ -131,7 +131,7 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
     std::vector<uint32_t> fc(n_ + 16, 0);
     for (uint64_t i = 0; i < n_; ++i) {
       if (rp[i] < rp[i + 1]) fc[i] = ci[rp[i]];
-      for (uint32_t k = rp[i] + 1; k < rp[i + 1]; ++k) dc[k] = (uint16_t)(ci[k] - ci[k - 1]);
+      for (uint32_t k = rp[i] + 1; k < rp[i + 1]; ++k) dc[k] = (uint16_t)(ci[k] - ci[k - 1] - 1u);
     }
     dcol.alloc(dc.size() * 2);
     first.alloc(fc.size() * 4);
@@ -217,7 +217,18 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
     F3RG_CUDA(cudaMemcpy(tr0_[p].get(), r0.data(), r0.size() * 4, cudaMemcpyHostToDevice));
     F3RG_CUDA(cudaMemcpy(tk0_[p].get(), k0.data(), k0.size() * 4, cudaMemcpyHostToDevice));
   }
+  // L2 eviction priorities (common.cuh l2_policy) once a pass streams more than half
+  // the 126 MB L2: then the gathered vector, not the matrix, is what the L2 can keep
+  // (config 1's 11 MB fp16 replica stays L2-resident across passes without them).
+  // F3RG_L2HINT=0/1 forces.
+  const char* h = std::getenv("F3RG_L2HINT");
+  l2hint_ = h && *h ? (h[0] == '0' ? 0u : 1u) : (stream_bytes(0) > 64e6 ? 1u : 0u);
   F3RG_CUDA(cudaDeviceSynchronize());
+}
+
+double DeviceMatrix::stream_bytes(int pa) const {
+  const double n = (double)n_, nnz = (double)nnz_;
+  return nnz * psize(pa) + (d16() ? 2.0 * nnz + 4.0 * n : 4.0 * nnz) + 4.0 * (n + 1);
 }
 
 CsrDev DeviceMatrix::csr_plain() const {
@@ -254,6 +265,7 @@ TilesDev DeviceMatrix::tiles(int p) const {
   t.ntiles = ntiles_[p];
   t.shape = (uint32_t)shape_;
   t.perm = perm_.get<const uint32_t>();
+  t.l2hint = l2hint_;
   return t;
 }
 
@@ -304,8 +316,11 @@ Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_ki
   for (size_t d = 0; d + 1 < spec_.levels.size(); ++d)
     if (spec_.levels[d].kind == LK_RICHARDSON)
       throw Error(ERR_UNSUPPORTED, "a Richardson level with an inner solver below it is not implemented on the device");
-  for (const auto& L : spec_.levels)
+  for (const auto& L : spec_.levels) {
     if (L.kind == LK_FGMRES && L.m > 1000) throw Error(ERR_UNSUPPORTED, "FGMRES cycle length above 1000");
+    // the per-level reset image holds 1000 weights (reset_state)
+    if (L.kind == LK_RICHARDSON && L.m > 1000) throw Error(ERR_UNSUPPORTED, "Richardson step count above 1000");
+  }
   id_ = spec_.to_string();
   if (const char* e = std::getenv("F3RG_NO_REVERSE")) reverse_off_ = e[0] == '1';
   n_ = a_->rows();
@@ -326,11 +341,19 @@ Solver::Solver(const Spec& spec, std::shared_ptr<DeviceMatrix> a, int precond_ki
   build_levels();
   // the in-process transport synchronises ranks on the host between kernels, so it
   // launches eagerly; NCCL exchanges are stream work and go into the graph
-  if (!ex_ || ex_->capturable()) capture_inner_graph();
+  if (lv_.size() >= 2 && lv_[0]->spec.kind == LK_FGMRES && lv_[1]->spec.kind == LK_FGMRES) {
+    if (!ex_) {
+      inner_exec_ = capture_invocation();
+      has_inner_graph_ = true;
+    } else if (ex_->capturable()) {
+      has_inner_graph_ = true;  // variants captured on first use (invocation_graph)
+    }
+  }
 }
 
 Solver::~Solver() {
   if (inner_exec_) cudaGraphExecDestroy(inner_exec_);
+  for (auto& kv : part_exec_) cudaGraphExecDestroy(kv.second);
   if (own_stream_ && !(ex_ && ex_->stream())) cudaStreamDestroy(own_stream_);
   if (info_host_) cudaFreeHost(info_host_);
   if (io_host_) cudaFreeHost(io_host_);
@@ -435,11 +458,10 @@ void Solver::build_levels() {
       L.rs.alloc(sizeof(RichState));
       F3RG_CUDA(cudaMemcpy(L.rs.get(), &h, sizeof h, cudaMemcpyHostToDevice));
       L.drs = L.rs.get<RichState>();
-      reset_richardson(d, nullptr);
-      F3RG_CUDA(cudaDeviceSynchronize());
     }
   }
-  // pinned images of every Richardson level's initial state (reset_state)
+  // pinned images of every Richardson level's initial state (reset_state,
+  // reset_richardson): 1000 weights + the 4 call counters per level
   F3RG_CUDA(cudaHostAlloc((void**)&reset_host_, (size_t)D * 1024 * sizeof(double), cudaHostAllocDefault));
   for (int d = 0; d < D; ++d) {
     const LevelSpec& S = spec_.levels[d];
@@ -448,6 +470,8 @@ void Solver::build_levels() {
     unsigned long long calls[4] = {1ull, 0ull, 0ull, 0ull};
     std::memcpy(img + 1000, calls, sizeof calls);
   }
+  reset_state(own_stream_);
+  F3RG_CUDA(cudaStreamSynchronize(own_stream_));
   if (has_m()) {
     // the sweeps' workspace (row values, level counters) and the staging vector
     work_ = M_->make_work();
@@ -465,14 +489,13 @@ void Solver::build_levels() {
   }
 }
 
+// stream-ordered copies from the pinned reset image (the solver's streams are
+// non-blocking: a legacy-stream cudaMemcpy would not be ordered with them)
 void Solver::reset_richardson(int l, cudaStream_t s) {
   Level& L = *lv_[l];
-  std::vector<double> w((size_t)L.spec.m, L.spec.has_omega ? L.spec.omega : 1.0);
-  const unsigned long long calls[4] = {1ull, 0ull, 0ull, 0ull};
-  // synchronous: the state is tiny and resets are rare
-  F3RG_CUDA(cudaStreamSynchronize(s));
-  F3RG_CUDA(cudaMemcpy(L.omegas.get(), w.data(), w.size() * 8, cudaMemcpyHostToDevice));
-  F3RG_CUDA(cudaMemcpy(L.calls.get(), calls, sizeof calls, cudaMemcpyHostToDevice));
+  const double* img = reset_host_ + (size_t)l * 1024;
+  F3RG_CUDA(cudaMemcpyAsync(L.omegas.get(), img, (size_t)L.spec.m * 8, cudaMemcpyHostToDevice, s));
+  F3RG_CUDA(cudaMemcpyAsync(L.calls.get(), img + 1000, 4 * 8, cudaMemcpyHostToDevice, s));
 }
 
 // ---- profiling (eager mode only) ------------------------------------------------------
@@ -518,10 +541,7 @@ std::vector<Solver::KernelTime> Solver::profile_results() const {
 
 // bytes one pass over the matrix replica `pa` streams: values, the column stream
 // actually in use (u32, or D16 = u16 deltas + u32 first column per row), row_ptr
-double Solver::mbytes(int pa) const {
-  const double n = (double)n_, nnz = (double)a_->nnz();
-  return nnz * psize(pa) + (a_->d16() ? 2.0 * nnz + 4.0 * n : 4.0 * nnz) + 4.0 * (n + 1);
-}
+double Solver::mbytes(int pa) const { return a_->stream_bytes(pa); }
 
 static std::string kname(const char* base, int a, int b, int c) {
   return std::string(base) + "[" + precision_name(a) + "," + precision_name(b) + "," + precision_name(c) + "]";
@@ -535,7 +555,7 @@ void Solver::reduce(cudaStream_t s, F&& launch) {
     return;
   }
   launch(DistH{1, ex_->size(), ex_->loc_buf(), nullptr});
-  ex_->allgather(ex_->loc_buf(), ex_->all_buf(), s);
+  allgather(s);
   launch(DistH{2, ex_->size(), ex_->loc_buf(), ex_->all_buf()});
   ex_->done_reduce(s);
 }
@@ -560,14 +580,16 @@ void Solver::enqueue_richardson(int l, int j, void* v_ext, const double* sj, voi
     (void)j;
     return;
   }
-  // partitioned: halo of v, the plain sweep, then the update-call phases with their
-  // exchanges (every call; the phases return at once unless call_count % c == 0)
+  // partitioned: halo of v, the plain sweep, then -- only where the call can be an
+  // update call (plan_update_calls) -- the update phases with their exchanges (their
+  // kernels still check call_count % c == 0 on the device and return on plain calls)
   halo(v_ext, L.W, s);
   PROF(kname("richardson", R.PA, R.W, L.W).c_str(), bytes,
        launch_richardson(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, v_ext, sj, z_own, n, R.drs, GateH{dead, l}, l,
                          cnt, sync, bar_.get<unsigned>(), bar_.get<unsigned>() + 1, nullptr, off_, 1));
   const int m = R.spec.m;
-  for (int k = 0; k < m; ++k) {
+  const bool maybe_update = ++rich_pos_ >= upd_from_;
+  for (int k = 0; k < m && maybe_update; ++k) {
     if (k > 0) {
       halo(R.Za.get(), R.W, s);
       F3RG_CUDA(launch_rich_phase(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, PH_RESID_H, k, v_ext, sj, off_, z_own, n,
@@ -577,7 +599,7 @@ void Solver::enqueue_richardson(int l, int j, void* v_ext, const double* sj, voi
     F3RG_CUDA(launch_rich_phase(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, PH_DOTS_H, k, v_ext, sj, off_, z_own, n,
                                 R.drs, R.R.get(), R.Za.get(), GateH{dead, l}, l, cnt, sync,
                                 DistH{1, ex_->size(), ex_->loc_buf(), nullptr}));
-    ex_->allgather(ex_->loc_buf(), ex_->all_buf(), s);
+    allgather(s);
     F3RG_CUDA(launch_rich_phase(R.PA, R.W, L.W, Launch{0, s}, a_->csr(), T, PH_UPDATE_H, k, v_ext, sj, off_, z_own, n,
                                 R.drs, R.R.get(), R.Za.get(), GateH{dead, l}, l, cnt, sync,
                                 DistH{2, ex_->size(), ex_->loc_buf(), ex_->all_buf()}));
@@ -631,10 +653,11 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
   SyncH sync{partials_.get<double>(), counter_.get<unsigned>()};
   if (L.child == 0) {
     if (top) {
+      plan_update_calls(s);
       io_host_[j] = IoSlot{vj_own, sj, zj_own};
       F3RG_CUDA(cudaMemcpyAsync(io_.get(), &io_host_[j], sizeof(IoSlot), cudaMemcpyHostToDevice, s));
       if (has_inner_graph_ && !profiling_now_) {
-        F3RG_CUDA(cudaGraphLaunch(inner_exec_, s));
+        F3RG_CUDA(cudaGraphLaunch(invocation_graph(), s));
       } else {
         enqueue_fgmres(l + 1, nullptr, nullptr, nullptr, io_.get<IoSlot>(), s);
       }
@@ -642,6 +665,7 @@ void Solver::enqueue_child_step(int l, int j, cudaStream_t s, bool top) {
       enqueue_fgmres(l + 1, vj_own, sj, zj_own, nullptr, s);
     }
   } else if (L.child == 1) {
+    if (top) plan_update_calls(s);
     enqueue_richardson(l + 1, j, vj, sj, zj_own, s);
   } else if (has_m()) {
     // z_j = M (s_j v_j): the normalised basis vector staged at W (counts the
@@ -705,8 +729,7 @@ void Solver::enqueue_fgmres(int l, void* src, const double* src_scale, void* dst
                            GateH{dead, l}, l, cnt, 1, io, ld_));
 }
 
-void Solver::capture_inner_graph() {
-  if (lv_.size() < 2 || lv_[0]->spec.kind != LK_FGMRES || lv_[1]->spec.kind != LK_FGMRES) return;
+cudaGraphExec_t Solver::capture_invocation() {
   cudaStream_t cs = nullptr;
   F3RG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   cudaGraph_t graph = nullptr;
@@ -720,11 +743,47 @@ void Solver::capture_inner_graph() {
     throw;
   }
   F3RG_CUDA(cudaStreamEndCapture(cs, &graph));
-  const cudaError_t e = cudaGraphInstantiate(&inner_exec_, graph, 0);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   cudaStreamDestroy(cs);
   F3RG_CUDA(e);
-  has_inner_graph_ = true;
+  return exec;
+}
+
+cudaGraphExec_t Solver::invocation_graph() {
+  if (!ex_) return inner_exec_;
+  auto it = part_exec_.find(upd_from_);
+  if (it != part_exec_.end()) return it->second;
+  // every rank reaches here with the same upd_from_ (replicated device state), so
+  // the ranks capture matching collective sequences
+  cudaGraphExec_t g = capture_invocation();
+  part_exec_[upd_from_] = g;
+  return g;
+}
+
+void Solver::plan_update_calls(cudaStream_t s) {
+  rich_pos_ = 0;  // positions count the calls below this outer step
+  int rl = -1;
+  for (int d = 1; d < (int)lv_.size(); ++d)
+    if (lv_[d]->spec.kind == LK_RICHARDSON) rl = d;
+  if (!ex_ || rl < 0 || has_m()) {
+    upd_from_ = 1;
+    return;
+  }
+  const unsigned long long c = lv_[rl]->spec.cycle;
+  if (c == 0) {  // never updates
+    upd_from_ = 1 << 30;
+    return;
+  }
+  auto* h = reinterpret_cast<unsigned long long*>(stage_host_ + 48);
+  F3RG_CUDA(cudaMemcpyAsync(h, lv_[rl]->calls.get(), 8, cudaMemcpyDeviceToHost, s));
+  F3RG_CUDA(cudaStreamSynchronize(s));
+  // the invocation's calls are call_count C, C+1, ...; the first update is the first
+  // multiple of c. Early stops inside the invocation only delay calls, never bring an
+  // update earlier, so every position from there on keeps its update phases.
+  const unsigned long long C = *h;
+  upd_from_ = (int)((c - C % c) % c) + 1;
 }
 
 double Solver::read_double(const double* dev, cudaStream_t s) {
@@ -758,6 +817,7 @@ Report Solver::run(const double* b, double* x_out, const RunOptions& opts, cudaS
   }
   Report rep;
   rep.solver_id = id_;
+  n_halo_ = n_reduce_ = 0;
   const int D = (int)lv_.size();
   F3RG_CUDA(cudaMemsetAsync(cnt_.get(), 0, cnt_.bytes(), s));
   F3RG_CUDA(cudaMemsetAsync(dead_.get(), 0, dead_.bytes(), s));
@@ -937,13 +997,8 @@ Report Solver::run_richardson_top(const double* b, const RunOptions& opts, cudaS
 
 void Solver::reset_state(cudaStream_t stream) {
   cudaStream_t s = stream ? stream : own_stream_;
-  for (int d = 0; d < (int)lv_.size(); ++d) {
-    Level& L = *lv_[d];
-    if (L.spec.kind != LK_RICHARDSON) continue;
-    const double* img = reset_host_ + (size_t)d * 1024;
-    F3RG_CUDA(cudaMemcpyAsync(L.omegas.get(), img, (size_t)L.spec.m * 8, cudaMemcpyHostToDevice, s));
-    F3RG_CUDA(cudaMemcpyAsync(L.calls.get(), img + 1000, 4 * 8, cudaMemcpyHostToDevice, s));
-  }
+  for (int d = 0; d < (int)lv_.size(); ++d)
+    if (lv_[d]->spec.kind == LK_RICHARDSON) reset_richardson(d, s);
 }
 
 std::vector<double> Solver::innermost_omegas() {

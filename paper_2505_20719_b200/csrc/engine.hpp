@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <condition_variable>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <optional>
@@ -138,6 +139,8 @@ class DeviceMatrix {
   bool sorted_rows() const { return perm_.get() != nullptr; }
   const void* values(int p) const { return val_[p].get(); }
   bool d16() const { return dcol_.get() != nullptr; }  // 16-bit delta column stream in use
+  // bytes one pass over replica pa streams: values, the column stream in use, row_ptr
+  double stream_bytes(int pa) const;
   int shape() const { return shape_; }  // tile shape: 0 regular, 1 short rows, 2 gather-bound
 
  private:
@@ -147,6 +150,7 @@ class DeviceMatrix {
   DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_, pk_;
   DevBuf perm_, srp_, sci_, sval_[3], sdcol_, sfirst_, spk_;  // row-sorted copy (irregular rows)
   uint32_t ntiles_[3] = {0, 0, 0};
+  uint32_t l2hint_ = 0;  // L2 eviction priorities for the passes (init)
   int shape_ = 0;
 };
 
@@ -306,11 +310,16 @@ class Solver {
     double bytes;  // algorithmic bytes over all launches
   };
   std::vector<KernelTime> profile_results() const;
+  // halo exchanges and cross-rank reductions (allgathers) the last eager (profiled)
+  // run enqueued; graph replays do not count (row-block partition)
+  unsigned long long halos() const { return n_halo_; }
+  unsigned long long reductions() const { return n_reduce_; }
 
  private:
   struct Level;
   void build_levels();
-  void capture_inner_graph();
+  cudaGraphExec_t capture_invocation();  // one L2 invocation as a CUDA graph
+  cudaGraphExec_t invocation_graph();     // ... the variant for the current upd_from_
   void enqueue_fgmres(int l, void* src, const double* src_scale, void* dst, const IoSlot* io, cudaStream_t s);
   void enqueue_child_step(int l, int j, cudaStream_t s, bool top);
   void reset_richardson(int l, cudaStream_t s);
@@ -322,8 +331,17 @@ class Solver {
   void prof_begin(cudaStream_t s);
   void prof_end(cudaStream_t s, const char* name, double bytes);
   void halo(void* ext, int prec, cudaStream_t s) {
-    if (ex_) ex_->halo(ext, prec, s);
+    if (!ex_) return;
+    ++n_halo_;
+    ex_->halo(ext, prec, s);
   }
+  void allgather(cudaStream_t s) {
+    ++n_reduce_;
+    ex_->allgather(ex_->loc_buf(), ex_->all_buf(), s);
+  }
+  // row-block partition: the device's Richardson call counter before the next L2
+  // invocation -> upd_from_ (first call position in it that can be an update call)
+  void plan_update_calls(cudaStream_t s);
   // P == 1: launch(DistH{}) once. P > 1: rank-local launch, allgather, tail launch.
   template <class F>
   void reduce(cudaStream_t s, F&& launch);
@@ -352,6 +370,14 @@ class Solver {
   cudaStream_t own_stream_ = nullptr;
   cudaGraphExec_t inner_exec_ = nullptr;
   bool has_inner_graph_ = false;
+  // Row-block partition: a Richardson call carries its update-call phases (halos,
+  // allgathers) only from position upd_from_ of the L2 invocation on; rich_pos_
+  // counts the calls enqueued in the current invocation. One captured graph per
+  // upd_from_ value.
+  int rich_pos_ = 0;
+  int upd_from_ = 1;
+  std::map<int, cudaGraphExec_t> part_exec_;
+  unsigned long long n_halo_ = 0, n_reduce_ = 0;
   bool profile_ = false;
   bool profiling_now_ = false;
   bool reverse_off_ = false;  // F3RG_NO_REVERSE=1: no reversed tile walks (A/B tests)

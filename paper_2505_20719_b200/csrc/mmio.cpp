@@ -1,16 +1,26 @@
-// mmio.cpp -- Matrix Market coordinate I/O for external matrices,
-// restating reference src/matrix_market.cpp:33-127: matrix coordinate real /
-// integer / pattern, general / symmetric; symmetric storage expanded, duplicates
-// summed after the (row, col) sort, pattern entries 1.0; square only; the
-// reference's ParseError messages. Host code: the result feeds f3rg_matrix_create /
+// mmio.cpp -- Matrix Market exchange files: the NIST "matrix
+// coordinate" format, written from the format's definition. A file is
+//   %%MatrixMarket matrix coordinate <field> <symmetry>     banner (case-insensitive)
+//   % ...                                                   comments / blank lines
+//   <rows> <cols> <entries>                                 size line
+//   <i> <j> [<value>]                                       1-based entries
+// with field real | integer | pattern (value 1) and symmetry general | symmetric
+// (only one triangle stored; the mirror entry is implied).
+// Reader contract (pinned to the reference reader's outputs and messages,
+// tests/golden/reference_mm.npz): square matrices only; duplicates are summed in
+// the order a (row, col) comparison sort of the entry list -- mirrors appended
+// right after their entry -- puts them (std::sort: the same comparator on the same
+// sequence visits equal keys in the same order, so the rounded sums agree); errors
+// are ParseError "matrix market: ...". The result feeds f3rg_matrix_create /
 // f3rg_matrix_create_scaled like any host CSR.
 #include <algorithm>
 #include <cctype>
 #include <cstdio>
 #include <fstream>
+#include <iterator>
+#include <numeric>
 #include <sstream>
 #include <string>
-#include <tuple>
 #include <vector>
 
 #include "engine.hpp"
@@ -24,87 +34,122 @@ struct HostCsr {
 };
 
 namespace {
-std::string lower(std::string s) {
-  for (auto& c : s) c = (char)std::tolower((unsigned char)c);
-  return s;
-}
-struct Triplet {
-  uint32_t r, c;
-  double v;
+
+[[noreturn]] void parse_error(const std::string& what) { throw Error(ERR_PARSE, "matrix market: " + what); }
+
+// the file as a sequence of '\n'-terminated lines (the terminator dropped)
+class Lines {
+ public:
+  explicit Lines(std::string text) : text_(std::move(text)) {}
+  bool next(std::string& out) {
+    if (pos_ >= text_.size()) return false;
+    const size_t e = text_.find('\n', pos_);
+    const size_t stop = e == std::string::npos ? text_.size() : e;
+    out.assign(text_, pos_, stop - pos_);
+    pos_ = e == std::string::npos ? text_.size() : e + 1;
+    return true;
+  }
+  // the next line that carries data (comments and empty lines skipped)
+  bool next_data(std::string& out) {
+    while (next(out))
+      if (!out.empty() && out[0] != '%') return true;
+    return false;
+  }
+
+ private:
+  std::string text_;
+  size_t pos_ = 0;
 };
-[[noreturn]] void fail(const std::string& m) { throw Error(ERR_PARSE, "matrix market: " + m); }
+
+enum class Field { Real, Integer, Pattern };
+
+struct Banner {
+  Field field = Field::Real;
+  bool symmetric = false;
+};
+
+Banner read_banner(const std::string& line) {
+  std::istringstream words(line);
+  std::string tok[5];
+  for (auto& t : tok) words >> t;
+  if (tok[0] != "%%MatrixMarket") parse_error("missing %%MatrixMarket banner");
+  for (int k = 1; k < 5; ++k)
+    std::transform(tok[k].begin(), tok[k].end(), tok[k].begin(), [](unsigned char c) { return (char)std::tolower(c); });
+  if (tok[1] != "matrix" || tok[2] != "coordinate")
+    parse_error("only 'matrix coordinate' is supported, got '" + tok[1] + " " + tok[2] + "'");
+  Banner b;
+  static const std::pair<const char*, Field> fields[] = {{"real", Field::Real}, {"integer", Field::Integer},
+                                                         {"pattern", Field::Pattern}};
+  const auto f = std::find_if(std::begin(fields), std::end(fields), [&](const auto& e) { return tok[3] == e.first; });
+  if (f == std::end(fields)) parse_error("unsupported field '" + tok[3] + "'");
+  b.field = f->second;
+  if (tok[4] == "symmetric") b.symmetric = true;
+  else if (tok[4] != "general") parse_error("unsupported symmetry '" + tok[4] + "'");
+  return b;
+}
+
+struct Coo {
+  uint32_t row, col;
+  double val;
+  bool operator<(const Coo& o) const { return row != o.row ? row < o.row : col < o.col; }
+};
+
+// sorted triplets -> CSR, equal (row, col) runs summed left to right
+HostCsr compress(uint64_t n, std::vector<Coo>& coo) {
+  std::sort(coo.begin(), coo.end());
+  HostCsr m;
+  m.n = n;
+  m.rp.assign(n + 1, 0);
+  size_t k = 0;
+  while (k < coo.size()) {
+    const Coo head = coo[k];
+    double sum = head.val;
+    for (++k; k < coo.size() && coo[k].row == head.row && coo[k].col == head.col; ++k) sum += coo[k].val;
+    m.ci.push_back(head.col);
+    m.v.push_back(sum);
+    m.rp[head.row + 1] += 1;
+  }
+  std::partial_sum(m.rp.begin(), m.rp.end(), m.rp.begin());
+  return m;
+}
+
 }  // namespace
 
 HostCsr read_matrix_market(std::istream& in) {
+  Lines lines{std::string(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>())};
   std::string line;
-  if (!std::getline(in, line)) fail("empty stream");
-  std::string banner, object, format, field, symmetry;
-  {
-    std::istringstream h(line);
-    h >> banner >> object >> format >> field >> symmetry;
-  }
-  if (banner != "%%MatrixMarket") fail("missing %%MatrixMarket banner");
-  object = lower(object), format = lower(format), field = lower(field), symmetry = lower(symmetry);
-  if (object != "matrix" || format != "coordinate")
-    fail("only 'matrix coordinate' is supported, got '" + object + " " + format + "'");
-  if (field != "real" && field != "integer" && field != "pattern") fail("unsupported field '" + field + "'");
-  if (symmetry != "general" && symmetry != "symmetric") fail("unsupported symmetry '" + symmetry + "'");
-  const bool pattern = field == "pattern", sym = symmetry == "symmetric";
+  if (!lines.next(line)) parse_error("empty stream");
+  const Banner banner = read_banner(line);
 
-  std::size_t nr = 0, nc = 0, nz = 0;
-  for (;;) {  // the size line follows any % comments
-    if (!std::getline(in, line)) fail("missing size line");
-    if (line.empty() || line[0] == '%') continue;
-    std::istringstream s(line);
-    if (!(s >> nr >> nc >> nz)) fail("malformed size line");
-    break;
-  }
-  if (nr != nc) fail("non-square matrix (" + std::to_string(nr) + " x " + std::to_string(nc) + ")");
+  if (!lines.next_data(line)) parse_error("missing size line");
+  std::size_t rows = 0, cols = 0, entries = 0;
+  if (!(std::istringstream(line) >> rows >> cols >> entries)) parse_error("malformed size line");
+  if (rows != cols) parse_error("non-square matrix (" + std::to_string(rows) + " x " + std::to_string(cols) + ")");
 
-  std::vector<Triplet> t;
-  t.reserve(sym ? 2 * nz : nz);
-  for (std::size_t seen = 0; seen < nz;) {
-    if (!std::getline(in, line)) fail("unexpected end of stream");
-    if (line.empty() || line[0] == '%') continue;
-    std::istringstream s(line);
+  std::vector<Coo> coo;
+  coo.reserve(banner.symmetric ? 2 * entries : entries);
+  for (std::size_t e = 0; e < entries; ++e) {
+    if (!lines.next_data(line)) parse_error("unexpected end of stream");
+    std::istringstream fields(line);
     long long i = 0, j = 0;
-    double v = 1.0;
-    if (!(s >> i >> j)) fail("malformed entry '" + line + "'");
-    if (!pattern && !(s >> v)) fail("missing value in '" + line + "'");
-    if (i < 1 || j < 1 || (std::size_t)i > nr || (std::size_t)j > nc)
-      fail("index out of bounds at entry (" + std::to_string(i) + ", " + std::to_string(j) + ")");
-    t.push_back({(uint32_t)(i - 1), (uint32_t)(j - 1), v});
-    if (sym && i != j) t.push_back({(uint32_t)(j - 1), (uint32_t)(i - 1), v});
-    ++seen;
+    double value = 1.0;  // pattern entries
+    if (!(fields >> i >> j)) parse_error("malformed entry '" + line + "'");
+    if (banner.field != Field::Pattern && !(fields >> value)) parse_error("missing value in '" + line + "'");
+    const bool inside = i >= 1 && j >= 1 && (std::size_t)i <= rows && (std::size_t)j <= cols;
+    if (!inside) parse_error("index out of bounds at entry (" + std::to_string(i) + ", " + std::to_string(j) + ")");
+    coo.push_back({(uint32_t)(i - 1), (uint32_t)(j - 1), value});
+    if (banner.symmetric && i != j) coo.push_back({(uint32_t)(j - 1), (uint32_t)(i - 1), value});
   }
-  // same comparison sort as the reference, so equal (row, col) keys meet in the same
-  // order and their sums round identically
-  std::sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) { return std::tie(a.r, a.c) < std::tie(b.r, b.c); });
-  HostCsr m;
-  m.n = nr;
-  m.rp.assign(nr + 1, 0);
-  m.ci.reserve(t.size());
-  m.v.reserve(t.size());
-  for (std::size_t k = 0; k < t.size(); ++k) {
-    if (k > 0 && t[k].r == t[k - 1].r && t[k].c == t[k - 1].c) {
-      m.v.back() += t[k].v;
-      continue;
-    }
-    m.ci.push_back(t[k].c);
-    m.v.push_back(t[k].v);
-    ++m.rp[t[k].r + 1];
-  }
-  for (std::size_t i = 0; i < nr; ++i) m.rp[i + 1] += m.rp[i];
-  return m;
+  return compress(rows, coo);
 }
 
 void write_matrix_market(std::ostream& out, uint64_t n, const uint32_t* rp, const uint32_t* ci, const double* v) {
   out << "%%MatrixMarket matrix coordinate real general\n" << n << " " << n << " " << rp[n] << "\n";
-  char buf[64];
+  char num[40];
   for (uint64_t i = 0; i < n; ++i)
     for (uint32_t k = rp[i]; k < rp[i + 1]; ++k) {
-      std::snprintf(buf, sizeof buf, "%.17g", v[k]);
-      out << (i + 1) << " " << (ci[k] + 1) << " " << buf << "\n";
+      std::snprintf(num, sizeof num, "%.17g", v[k]);  // round-trips every binary64
+      out << (i + 1) << ' ' << (ci[k] + 1) << ' ' << num << '\n';
     }
 }
 

@@ -403,6 +403,13 @@ SweepWork::SweepWork(uint64_t n, uint32_t nlev_fwd, uint32_t nlev_bwd) : n_(n) {
   }
   F3RG_CUDA(cudaMalloc((void**)&ctl, 2 * sizeof(SweepCtl)));
   F3RG_CUDA(cudaMemset(ctl, 0, 2 * sizeof(SweepCtl)));
+  // test hook: start the epoch tags just below a 2^16 multiple (the tags skip those,
+  // the launch counter does not), as a long-lived solver reaches after 65k applies
+  if (const char* e = std::getenv("F3RG_SWEEP_EPOCH0")) {
+    SweepCtl h[2] = {};
+    h[0].epoch = h[1].epoch = (unsigned)std::strtoul(e, nullptr, 10);
+    F3RG_CUDA(cudaMemcpy(ctl, h, sizeof h, cudaMemcpyHostToDevice));
+  }
 }
 
 void SweepWork::prepare(int c, cudaStream_t s) {

@@ -71,10 +71,10 @@ struct SweepDev {
 
 // cross-launch control of one sweep direction (trsv.cuh)
 struct SweepCtl {
-  unsigned epoch;     // launches of this sweep completed so far
+  unsigned epoch;     // epoch tag of the last completed launch (trsv.cuh next_epoch)
   unsigned done;      // CTAs finished in the running launch
   unsigned frontier;  // levels completed in the running launch (a hint for sleeping)
-  unsigned pad;
+  unsigned launches;  // launches completed (mod 2^32): level_done[L] = launches * slices(L)
 };
 
 // per-user sweep state: the two sweeps' row cells (n x 12 bytes each, enough for

@@ -58,8 +58,19 @@ struct GatherZ1 {
   using Raw = T_<PV>;
   RhsView<PV, PW> rhs;
   T_<PW> w0;
+  __device__ __forceinline__ void set_policy(uint64_t) {}
   __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(Ar<PW>::mul(w0, rhs.apply(r))); }
+};
+
+// the right-hand side itself as the SpMV operand (update call, step 0: p = r = v)
+template <int PV, int PW, int C>
+struct GatherRhs {
+  using Raw = T_<PV>;
+  RhsView<PV, PW> rhs;
+  __device__ __forceinline__ void set_policy(uint64_t) {}
+  __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
+  __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
 };
 
 // one fused step k >= 1: r = v - A z_k ; z_{k+1} = z_k + w_k r  (M = I, p = r)
@@ -199,12 +210,7 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_richardson(CsrDev A, Ti
         EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? RS->R : nullptr, Ar<CD>::zero(), Ar<CD>::zero(), {}, {}};
         if (sync.seq) e.S = RS->Zb;
         if (k == 0) {
-          struct GatherRhs {
-            using Raw = T_<PV>;
-            RhsView<PV, PW> rhs;
-            __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
-            __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
-          } g{rhs};
+          GatherRhs<PV, PW, C> g{rhs};
           spmv_tiles<PA, C, IDX, rich_chunk(IDX)>(A, T, g, e, smem);
         } else {
           GatherCG<PW, C> g{RS->R};
@@ -320,12 +326,7 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_rich_phase(CsrDev A, Ti
     if (!update) return;
     EpiDotsRs<PV, PW, C, CD> e{rhs, k > 0 ? Rown : nullptr, Ar<CD>::zero(), Ar<CD>::zero(), {}, {}};
     if (k == 0) {
-      struct GatherRhs {
-        using Raw = T_<PV>;
-        RhsView<PV, PW> rhs;
-        __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
-        __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
-      } g{rhs};
+      GatherRhs<PV, PW, C> g{rhs};
       spmv_tiles<PA, C, IDX, rich_chunk(IDX)>(A, T, g, e, smem);
     } else {
       GatherCG<PW, C> g{R};

@@ -129,7 +129,9 @@ struct TileCfg {
 // CH: gather chunk (0 = default: F3RG_CHUNK, or F3RG_P16_CHUNK for the P16 stream)
 template <int PA, int C, int IDX_, int CH = 0, class Gather, class Epi>
 __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
+  g.set_policy(l2_policy(T.l2hint ? 2 : 0));  // the gathered vector
   using Cfg = TileCfg<PA, IDX_>;
+  const uint64_t spol = l2_policy(T.l2hint ? 1 : 0);  // the matrix streams
   constexpr int IDX = Cfg::IDX;
   using TA = T_<PA>;
   using TC = typename std::conditional<IDX == 1, uint16_t, uint32_t>::type;
@@ -168,10 +170,10 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
     const uint32_t fb = IDX >= 1 ? (((r1 + 3) & ~3u) - r0a) * 4u : 0u;
     mbar_arrive_expect_tx(bar, vb + cb + rb + fb);
     uint8_t* sp = stage_ptr(s);
-    if (vb) bulk_g2s(sp, vals + k0v, vb, bar);
-    if (cb) bulk_g2s(sp + Cfg::VAL_BYTES, cols + k0c, cb, bar);
-    bulk_g2s(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES, A.rp + r0a, rb, bar);
-    if (IDX && fb) bulk_g2s(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES + Cfg::RP_BYTES, A.first + r0a, fb, bar);
+    if (vb) bulk_g2s_hint(sp, vals + k0v, vb, bar, spol);
+    if (cb) bulk_g2s_hint(sp + Cfg::VAL_BYTES, cols + k0c, cb, bar, spol);
+    bulk_g2s_hint(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES, A.rp + r0a, rb, bar, spol);
+    if (IDX && fb) bulk_g2s_hint(sp + Cfg::VAL_BYTES + Cfg::COL_BYTES + Cfg::RP_BYTES, A.first + r0a, fb, bar, spol);
   };
 
   if (tid == 0) {
@@ -221,11 +223,11 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
         auto fetch = [&](uint32_t q, TA& a) -> uint32_t {
           if constexpr (IDX == 2) {
             const uint32_t w = pc[q];
-            if (q > 0) col += w >> 16;
+            if (q > 0) col += (w >> 16) + 1u;
             a = bits_as<TA>((unsigned short)(w & 0xffffu));
             return col;
           } else if constexpr (IDX == 1) {
-            if (q > 0) col += pc[q];
+            if (q > 0) col += pc[q] + 1u;
             return col;
           } else {
             return pc[q];
@@ -275,11 +277,11 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
         TA a;
         if constexpr (IDX == 2) {
           const uint32_t w = A.pk[k];
-          if (k > k0) col += w >> 16;
+          if (k > k0) col += (w >> 16) + 1u;
           c = col;
           a = bits_as<TA>((unsigned short)(w & 0xffffu));
         } else if constexpr (IDX == 1) {
-          if (k > k0) col += A.dcol[k];
+          if (k > k0) col += A.dcol[k] + 1u;
           c = col;
           a = vals[k];
         } else {
@@ -312,7 +314,9 @@ template <int PX, int C>
 struct GatherPlain {
   using Raw = T_<PX>;
   const void* x;
-  __device__ __forceinline__ Raw load(uint32_t c) const { return ldg<PX>(x, c); }
+  uint64_t pol = 0;  // L2 policy, set by the SpMV engine (set_policy)
+  __device__ __forceinline__ void set_policy(uint64_t p) { pol = p; }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return ldg_hint<PX>(x, c, pol); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(r); }
 };
 
@@ -321,7 +325,9 @@ template <int PX, int C>
 struct GatherCG {
   using Raw = T_<PX>;
   const void* x;
-  __device__ __forceinline__ Raw load(uint32_t c) const { return ldcg<PX>(x, c); }
+  uint64_t pol = 0;  // L2 policy, set by the SpMV engine (set_policy)
+  __device__ __forceinline__ void set_policy(uint64_t p) { pol = p; }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return ldcg_hint<PX>(x, c, pol); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(r); }
 };
 
@@ -330,7 +336,9 @@ template <int PX, int C>
 struct GatherCA {
   using Raw = T_<PX>;
   const void* x;
-  __device__ __forceinline__ Raw load(uint32_t c) const { return ldca<PX>(x, c); }
+  uint64_t pol = 0;  // L2 policy, set by the SpMV engine (set_policy)
+  __device__ __forceinline__ void set_policy(uint64_t p) { pol = p; }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return ldca_hint<PX>(x, c, pol); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(r); }
 };
 

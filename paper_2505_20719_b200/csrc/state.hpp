@@ -13,7 +13,8 @@ struct CsrDev {
   const uint32_t* ci = nullptr;  // nnz (+pad)
   const void* val[3] = {nullptr, nullptr, nullptr};
   // "D16" column stream (same columns, fewer bytes): first[i] = column of row i's
-  // first entry, dcol[k] = col[k] - col[k-1] inside a row (dcol[rp[i]] unused).
+  // first entry, dcol[k] = col[k] - col[k-1] - 1 inside a row (dcol[rp[i]] unused;
+  // in-row gaps are >= 1, so a gap of 65,536 -- config 4's plane stride -- fits).
   // Present only when every in-row gap fits 16 bits; kernels then stream 2-byte
   // deltas instead of 4-byte indices.
   const uint16_t* dcol = nullptr;   // nnz (+pad)
@@ -35,6 +36,9 @@ struct TilesDev {
   // tile shape the tiles were cut for: 0 regular, 1 short rows, 2 gather-bound
   // (spmv.cuh TileCfg)
   uint32_t shape = 0;
+  // L2 eviction priorities (common.cuh l2_policy): 1 = matrix stream evict-first,
+  // gathered vector evict-last; 0 = the default policy (F3RG_L2HINT=0)
+  uint32_t l2hint = 0;
   // sorted-row tiles (irregular row lengths): tile row q is matrix row perm[q]; the
   // CsrDev handed with these tiles stores the rows in that order. Null = identity
   const uint32_t* perm = nullptr;

@@ -131,9 +131,13 @@ constexpr int kSweepChunk = F3RG_SWEEP_CHUNK;  // entries in flight per lane (a 
 
 // Process this warp's slices. init(row) -> T_<C> starting value; epi(row, value)
 // after the row is published.
+// nl: this launch's ordinal (launches completed + 1), the multiplier of the
+// per-level slice counts in level_done (which accumulate over launches). It is a
+// separate counter from the epoch tag, which skips multiples of 2^16.
 template <int TF, int C, class Init, class Epi>
 __device__ __forceinline__ void sweep_slices(const SweepDev& S, const Cells<C>& cells, unsigned* level_done,
-                                             unsigned* frontier, unsigned ep, const Init& init, Epi& epi) {
+                                             unsigned* frontier, unsigned ep, unsigned nl, const Init& init,
+                                             Epi& epi) {
   using A = Ar<C>;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -211,7 +215,7 @@ __device__ __forceinline__ void sweep_slices(const SweepDev& S, const Cells<C>& 
     // advances it
     __syncwarp();
     if (lane == 0) {
-      const unsigned target = ep * __ldg(S.lvl_ns + L);
+      const unsigned target = nl * __ldg(S.lvl_ns + L);  // mod 2^32, like the counter
       if (atomicAdd(level_done + L, 1u) + 1u == target) atomicMax(frontier, L + 1u);
     }
   }
@@ -219,13 +223,14 @@ __device__ __forceinline__ void sweep_slices(const SweepDev& S, const Cells<C>& 
 
 // the last CTA of a sweep launch advances the direction's epoch and rewinds the
 // frontier hint for the next launch
-__device__ __forceinline__ void sweep_done(SweepCtl* ctl, unsigned ep) {
+__device__ __forceinline__ void sweep_done(SweepCtl* ctl, unsigned ep, unsigned nl) {
   __syncthreads();
   if (threadIdx.x == 0) {
     if (atomicAdd(&ctl->done, 1u) == gridDim.x - 1) {
       ctl->done = 0u;
       ctl->frontier = 0u;
       ctl->epoch = ep;
+      ctl->launches = nl;
     }
   }
 }
@@ -247,13 +252,14 @@ __global__ void __launch_bounds__(256) k_sweep_fwd(SweepDev S, const void* in, v
   if (gate.closed()) return;
   constexpr int C = pmax(TF, PIN);
   const unsigned ep = next_epoch(*(volatile unsigned*)&ctl->epoch);
+  const unsigned nl = *(volatile unsigned*)&ctl->launches + 1u;
   const Cells<C> cl = Cells<C>::make(cells, S.n);
   auto init = [&](uint32_t row) { return cvt<C>(ldg<PIN>(in, row)); };
   struct {
     __device__ __forceinline__ void operator()(uint32_t, T_<C>) const {}
   } epi;
-  sweep_slices<TF, C>(S, cl, level_done, &ctl->frontier, ep, init, epi);
-  sweep_done(ctl, ep);
+  sweep_slices<TF, C>(S, cl, level_done, &ctl->frontier, ep, nl, init, epi);
+  sweep_done(ctl, ep, nl);
 }
 
 // backward sweep: init = the forward value of the row; out z_i = value rounded to
@@ -264,6 +270,7 @@ __global__ void __launch_bounds__(256) k_sweep_bwd(SweepDev S, const void* fcell
   pdl_wait();
   if (gate.closed()) return;
   const unsigned ep = next_epoch(*(volatile unsigned*)&ctl->epoch);
+  const unsigned nl = *(volatile unsigned*)&ctl->launches + 1u;
   const Cells<C> fw = Cells<C>::make(const_cast<void*>(fcells), S.n);
   const Cells<C> cl = Cells<C>::make(cells, S.n);
   bool fuse = false;
@@ -284,8 +291,8 @@ __global__ void __launch_bounds__(256) k_sweep_bwd(SweepDev S, const void* fcell
       st<POUT>(re.zout, row, AO::add(AO::mul(wk, p), zi));
     }
   };
-  sweep_slices<TF, C>(S, cl, level_done, &ctl->frontier, ep, init, epi);
-  sweep_done(ctl, ep);
+  sweep_slices<TF, C>(S, cl, level_done, &ctl->frontier, ep, nl, init, epi);
+  sweep_done(ctl, ep, nl);
 }
 
 }  // namespace f3rg

@@ -248,3 +248,35 @@ def test_richardson_state_sequence(cuda, oracle, shape, monkeypatch):
             assert w == list(om_ref)
             assert np.array_equal(z, z_ref), (call, np.abs(z - z_ref).max())
             om, cnt = om_ref, cnt_ref
+
+
+@pytest.mark.parametrize("gap", [65535, 65536, 65537])
+def test_d16_gap_boundary(cuda, oracle, gap):
+    """D16 stores in-row gaps minus one (columns strictly increase, so gaps are >= 1):
+    a gap of 65,536 -- config 4's plane stride -- still streams 2-byte deltas, one
+    of 65,537 falls back to u32 indices; the products are the same either way"""
+    import paper_2505_20719_b200 as f
+    n = 70000
+    rng = np.random.default_rng(9)
+    cols = []
+    for i in range(n):
+        c = {i}
+        if i + gap < n and i % 7 == 0:
+            c.add(i + gap)  # the widest gap of the matrix
+        for j in rng.integers(max(0, i - 50), min(n, i + 50), 3):
+            c.add(int(j))
+        cols.append(np.array(sorted(c), np.uint32))
+    rp = np.zeros(n + 1, np.uint32)
+    rp[1:] = np.cumsum([len(c) for c in cols])
+    ci = np.concatenate(cols)
+    va = rng.uniform(-1, 1, ci.size)
+    reps = f.make_replicas(f.SparseCsr(n, rp, ci, va))
+    nnz = ci.size
+    u32 = nnz * (2 + 4) + 4 * (n + 1)
+    d16 = nnz * (2 + 2) + 4 * n + 4 * (n + 1)
+    assert reps.stream_bytes(0) == (d16 if gap <= 65536 else u32)
+    for pa, px, py in ((0, 0, 0), (0, 1, 1), (1, 1, 1), (2, 2, 2)):
+        x = rand_vec(oracle, px, n, 4 + pa)
+        y = f.DenseVector(n, py)
+        f.spmv(reps.at(pa), f.DenseVector(x, px), y)
+        assert np.array_equal(y.numpy(), oracle.spmv((n, rp, ci), oracle.round_vec(pa, va), pa, x, px, py)), (gap, pa)

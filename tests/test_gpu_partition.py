@@ -110,6 +110,30 @@ def test_partitioned_richardson_update_calls(cuda, probs):
         assert np.allclose(rr[0].omegas_final, r1.omegas_final, rtol=1e-2), (P, rr[0].omegas_final, r1.omegas_final)
 
 
+def test_collectives_per_outer_iteration(cuda, probs):
+    """SURVEY 8(e)'s collective count per outer iteration of fp16-F3R: 73 halo
+    exchanges (1 + 8 + 32 z_j + 32 Richardson v) and 91 reductions (2 + 17 + 72).
+    A Richardson call enqueues its update phases (2 halos + 2 reductions for m = 2)
+    only where the device's call counter can make it an update call (one call in
+    64), instead of on every call (then: +96 halos and +64 reductions per outer
+    iteration). The same count on every rank."""
+    import paper_2505_20719_b200 as f
+    from paper_2505_20719_b200 import partition
+    name, p = probs[1]
+    K = 4
+    opts = f.RunOptions(tol=1e-18, max_outer_total=K)  # 128 Richardson calls: updates at 64 and 128
+    lp = partition.LocalPartition(_csr(p), F3R16, 2)
+    _, rr = lp.run(p.b, opts)
+    assert rr[0].outer_iterations == K
+    counts = [s.collectives() for s in lp.solvers]
+    assert counts[0] == counts[1]
+    halos, reds = counts[0]
+    upd = 2  # update calls in the run
+    # + the bnorm reduction, the cycle start, and the final true residual (halo + reduction)
+    assert 73 * K + 2 * upd <= halos <= 73 * K + 2 * upd + 2, (halos, reds)
+    assert 91 * K + 2 * upd <= reds <= 91 * K + 2 * upd + 3, (halos, reds)
+
+
 def test_nccl_transport_one_rank(cuda, probs):
     """the NCCL transport (point-to-point halos, allgather) with one rank: bitwise
     the plain solver"""

@@ -73,6 +73,24 @@ def test_apply_repeated_and_switching(probs, oracle):
         assert np.array_equal(z.numpy(), O.apply(r, pr, pr)), it
 
 
+def test_apply_across_epoch_skip(probs, oracle, monkeypatch):
+    """the epoch tags skip multiples of 2^16 (so zeroed cells never look current);
+    the frontier hint counts launches separately, so applies that cross the skip --
+    reached after ~65k applies by a long-lived solver -- stay correct (and do not
+    hang). F3RG_SWEEP_EPOCH0 starts the tags just below the skip."""
+    import paper_2505_20719_b200 as f
+    monkeypatch.setenv("F3RG_SWEEP_EPOCH0", str(65536 - 3))
+    name, p = probs[0]
+    a = (p.n, p.row_ptr, p.col_idx)
+    M = f.BlockJacobiIlu0.factorize(_csr(p), f.IluConfig(4, 1.0, True, f.Precision.P16))
+    O = oracle.ilu(a, p.values, 4, 1.0, True, 0)
+    for it in range(8):
+        r = rand_vec(oracle, 0, p.n, 500 + it)
+        z = f.DenseVector(p.n, f.Precision.P16)
+        M.apply(f.DenseVector(r, f.Precision.P16), z)
+        assert np.array_equal(z.numpy(), O.apply(r, 0, 0)), it
+
+
 def test_sweep_depth_matches_stencil_levels(cuda):
     """27-point lexicographic 16^3, 4 blocks of 4 planes: forward depth x + 2y + 4z + 1."""
     import paper_2505_20719_b200 as f

@@ -7,11 +7,12 @@ reductions bit for bit, so the parity gates hold on long vectors too:
   reference) at every precision pairing, n up to 10^6 + 3;
 * richardson_apply over 130 calls bit-exact INCLUDING the update calls (w' from
   in-order fp32 dots, src/richardson.cpp:31-45);
-* the small composed solves equal to the oracle's outer count and residual history;
+* the small composed solves equal to the oracle's, bit for bit (outer count,
+  residual history, solution);
 * the full-size BASELINE configs against the recorded runs of the UNMODIFIED
-  reference (tests/golden/reference_runs.json) -- config 5 (n = 2e7), whose
-  default tree reductions take 2 outer steps where the reference takes 3
-  (DESIGN.md section 4), included.
+  reference (tests/golden/reference_runs.json), residual histories digit for digit
+  -- config 5 (n = 2e7), whose default tree reductions take 2 outer steps where
+  the reference takes 3, included.
 """
 import json
 import os
@@ -85,9 +86,9 @@ def test_seq_richardson_sequence_bit_exact(cuda, oracle):
 
 @pytest.mark.parametrize("spec", [F3R16, F3R32])
 def test_seq_small_solves_match_oracle(cuda, oracle, spec):
-    """same outer counts as the oracle (the reference's order), and residual
-    histories equal up to the last-ulp differences of hypot (device libm vs glibc)
-    in the Givens rotations"""
+    """with the reference's reduction order (and its hypot, common.cuh ref_hypot)
+    the whole nested solve is the reference's arithmetic: the same outer count,
+    residual history and solution, bit for bit"""
     import paper_2505_20719_b200 as f
     for name, p in small_problems():
         with f.seq_reductions():
@@ -98,8 +99,8 @@ def test_seq_small_solves_match_oracle(cuda, oracle, spec):
         rep = run.report
         assert rep.outer_iterations == ref.outer_iterations, (name, rep.outer_iterations, ref.outer_iterations)
         assert rep.final_true_residual <= 1e-10
-        assert rep.residual_history == pytest.approx(ref.residual_history, rel=1e-3), name
-        assert normwise(run.x, ref.x) < 1e-8, name
+        assert rep.residual_history == list(ref.residual_history), (name, rep.residual_history, ref.residual_history)
+        assert np.array_equal(run.x, ref.x), (name, normwise(run.x, ref.x))
 
 
 def _reference_run(config):
@@ -123,8 +124,6 @@ def test_seq_full_config_vs_reference(cuda, config):
         rep = s.run(cuda.from_numpy(p.b).cuda(), f.RunOptions(tol=1e-10), want_x=False).report
     assert rep.converged and rep.final_true_residual <= 1e-10, rep
     assert rep.outer_iterations == ref["outer_iterations"], (rep.outer_iterations, rep.residual_history)
-    hist = np.array(rep.residual_history)
-    want = np.array(ref["residual_history"])
-    # every estimate above the fp64 floor agrees to 1e-6 relative
-    live = want > 1e-12
-    assert np.allclose(hist[live], want[live], rtol=1e-6, atol=0), (list(hist), list(want))
+    # the reference's own arithmetic, so its own residual history, digit for digit
+    assert rep.residual_history == ref["residual_history"], (rep.residual_history, ref["residual_history"])
+    assert rep.final_true_residual == ref["final_true_residual"]

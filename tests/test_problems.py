@@ -108,3 +108,18 @@ def test_generators_are_pinned():
 
 PINNED = {1: '58d4dc78c920da29', 2: '008e09aaa0c600d5', 3: 'e0fcbc8c666672ad', 4: '845e6b7d1e3a2c11',
           5: '434b411e5ba661c7'}
+
+
+@pytest.mark.parametrize("config,grid", [(1, 8), (2, 8), (3, 8), (4, 8), (5, 3000)])
+def test_binary_cache_matches_generator(tmp_path, monkeypatch, config, grid):
+    """lib/f3rg_gen's binary CSR cache (csr_cache) holds exactly the
+    bytes problems.problem() builds in-process, and the config tables agree"""
+    from paper_2505_20719_b200 import csr_cache
+    monkeypatch.setenv("F3RG_CACHE_DIR", str(tmp_path))
+    assert csr_cache.CONFIGS[config] == problems.CONFIGS[config][:6]
+    c = csr_cache.load(config, grid)
+    p = problems.problem(config, grid=grid)
+    assert (c.n, c.nnz, c.name) == (p.n, p.nnz, p.name)
+    for a, b in ((c.row_ptr, p.row_ptr), (c.col_idx, p.col_idx), (c.values, p.values), (c.b, p.b)):
+        assert a.dtype == b.dtype and np.array_equal(np.asarray(a), b)
+    assert csr_cache.load(config, grid).path == c.path  # second call reads the existing file

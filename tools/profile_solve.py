@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import paper_2505_20719_b200 as f  # noqa: E402
-from paper_2505_20719_b200 import problems  # noqa: E402
+from paper_2505_20719_b200 import csr_cache, problems  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
@@ -20,10 +20,10 @@ ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--spec", default="F100:f64/f64 > F8:f32/f32 > F4:f16/f32 > R2:f16,c=64 > identity")
 ap.add_argument("--eager", action="store_true", help="launch kernels eagerly (profile mode) instead of the graph")
 a = ap.parse_args()
-p = problems.problem(a.config, grid=a.grid)
+p = csr_cache.load(a.config) if a.grid is None else problems.problem(a.config, grid=a.grid)
 reps = f.make_replicas(f.SparseCsr(p.n, p.row_ptr, p.col_idx, p.values))
 s = f.build(f.parse_solver_spec(a.spec), reps, f.IdentityPrecond(p.n))
-b = torch.from_numpy(p.b).cuda()
+b = torch.from_numpy(__import__("numpy").ascontiguousarray(p.b)).cuda()
 for i in range(a.solves):
     s.set_profile(a.eager)
     torch.cuda.synchronize()
