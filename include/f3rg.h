@@ -99,6 +99,10 @@ uint64_t f3rg_matrix_nnz(const f3rg_matrix* a);
 /* bytes one device pass over replica `prec` streams (values + the compressed column
  * stream in use + row pointers); the reference's u32 CSR is nnz*(s+4) + 4(n+1) */
 uint64_t f3rg_matrix_stream_bytes(const f3rg_matrix* a, int prec);
+/* SpMV engine the matrix was laid out for: 0 row tiles (regular), 1 row tiles (short
+ * rows), 2 row tiles over the row-sorted copy (gather-bound), 3 windowed SELL
+ * (gather-bound, square, one rank); F3RG_SHAPE / F3RG_SORT_ROWS / F3RG_WSELL force */
+int f3rg_matrix_engine(const f3rg_matrix* a);
 /* replica values widened to fp64 into host memory (nnz doubles) */
 int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host);
 

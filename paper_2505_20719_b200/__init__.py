@@ -109,6 +109,8 @@ def lib():
     L.f3rg_matrix_nnz.restype = u64
     L.f3rg_matrix_nnz.argtypes = [vp]
     L.f3rg_matrix_values.argtypes = [vp, i32, vp]
+    L.f3rg_matrix_engine.argtypes = [vp]
+    L.f3rg_matrix_engine.restype = i32
     L.f3rg_spec_canonical.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
     L.f3rg_solver_create.argtypes = [C.POINTER(vp), vp, C.c_char_p, i32]
     L.f3rg_solver_destroy.argtypes = [vp]
@@ -413,6 +415,11 @@ class PrecisionReplicas:
     def stream_bytes(self, p: Precision) -> int:
         """bytes one device pass over replica p streams (compressed column stream)"""
         return int(lib().f3rg_matrix_stream_bytes(self.dev.h, int(p)))
+
+    def engine(self) -> int:
+        """SpMV engine of the device layout: 0/1 row tiles, 2 row tiles over the
+        row-sorted copy, 3 windowed SELL (f3rg_matrix_engine)"""
+        return int(lib().f3rg_matrix_engine(self.dev.h))
 
 
 def make_replicas(a64: SparseCsr) -> PrecisionReplicas:

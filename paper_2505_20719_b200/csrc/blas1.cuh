@@ -114,7 +114,7 @@ static __global__ void __launch_bounds__(256) k_pack16(const __half* v, const ui
 
 // plain y = A x (any precision triple), for the kernel-level entry point
 template <int PA, int PX, int PY, int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_spmv(CsrDev A, TilesDev T, const void* x, void* y) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int C = pmax(PA, PX);

@@ -139,6 +139,8 @@ uint64_t f3rg_matrix_stream_bytes(const f3rg_matrix* a, int prec) {
   return a && prec >= 0 && prec <= 2 ? (uint64_t)a->m->stream_bytes(prec) : 0;
 }
 
+int f3rg_matrix_engine(const f3rg_matrix* a) { return a ? a->m->shape() : -1; }
+
 int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host) {
   return guarded([&] {
     check_prec(prec);

@@ -36,10 +36,11 @@ constexpr int kThreads = 256;
 // touching anything another kernel wrote. F3RG_PDL=0 turns it off (A/B runs).
 bool pdl_enabled();
 template <class... KArgs, class... Args>
-inline cudaError_t launch_k(void (*kern)(KArgs...), int grid, int smem, cudaStream_t s, Args&&... args) {
+inline cudaError_t launch_kt(void (*kern)(KArgs...), int grid, int threads, int smem, cudaStream_t s,
+                             Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -48,6 +49,10 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), int grid, int smem, cudaStre
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <class... KArgs, class... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), int grid, int smem, cudaStream_t s, Args&&... args) {
+  return launch_kt(kern, grid, kThreads, smem, s, std::forward<Args>(args)...);
 }
 // one-thread scalar kernel (state updates between batched kernels)
 template <class... KArgs, class... Args>
@@ -67,10 +72,10 @@ inline cudaError_t launch_k1(void (*kern)(KArgs...), cudaStream_t s, Args&&... a
 // occupancy-derived persistent grid for a tile kernel instantiation (cached per
 // instantiation by the caller through a function-local static)
 template <class K>
-inline int occupancy_blocks(K kernel, int smem) {
+inline int occupancy_blocks(K kernel, int smem, int threads = kThreads) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem);
   return nb < 1 ? 1 : nb;
 }
 

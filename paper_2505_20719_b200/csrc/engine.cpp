@@ -174,6 +174,18 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
   }
   // irregular rows are gather-bound rows (config 5): half-size tiles leave L1 room
   if (sort_rows && !forced_shape && shape_ == 0) shape_ = 2;
+  // ... and go to the windowed SELL engine (wsell.cuh) when the matrix is square and
+  // on one rank (the engine's band of x is indexed by row); F3RG_WSELL=0/1 forces
+  {
+    const char* wse = std::getenv("F3RG_WSELL");
+    const bool square = ncols == 0 || ncols == n_;
+    const bool want = wse && *wse ? wse[0] != '0' : (sort_rows && !forced_shape);
+    if (want && square && n_ > 0 && nnz_ > 0 && n_ < (1ull << 31)) {
+      build_wsell(row_ptr);
+      shape_ = 3;
+      sort_rows = false;
+    }
+  }
   const uint32_t* trp = row_ptr;  // row pointers the tiles are cut from
   std::vector<uint32_t> srp;
   if (sort_rows) {
@@ -226,8 +238,84 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
   F3RG_CUDA(cudaDeviceSynchronize());
 }
 
+// Windowed SELL layout (wsell.cuh): rows sorted by length inside windows of
+// kWsSortRows, 64 slices of 32 rows per window, each slice chunk-major and as wide
+// as its longest row rounded up to 4; the windows are split over one CTA per SM by
+// stored entries. The columns and the three value replicas are moved into the
+// layout on the device, bit for bit.
+void DeviceMatrix::build_wsell(const uint32_t* rp) {
+  constexpr uint64_t SW = kWsSortRows, NS = kWsSortRows / 32;
+  const uint64_t nwin = (n_ + SW - 1) / SW, nsl = nwin * NS;
+  auto len = [&](uint32_t i) { return rp[i + 1] - rp[i]; };
+  std::vector<uint32_t> order(nwin * SW, kWsPadIdx), width(nsl, 0);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t w = 0; w < (int64_t)nwin; ++w) {
+    uint32_t* o = &order[(uint64_t)w * SW];
+    const uint64_t r0 = (uint64_t)w * SW, r1 = std::min<uint64_t>(n_, r0 + SW);
+    for (uint64_t i = r0; i < r1; ++i) o[i - r0] = (uint32_t)i;
+    std::stable_sort(o, o + (r1 - r0), [&](uint32_t a, uint32_t b) { return len(a) > len(b); });
+    for (uint64_t j = 0; j < NS; ++j) {
+      uint32_t k = 0;
+      for (uint64_t l = 0; l < 32; ++l) {
+        const uint32_t r = o[j * 32 + l];
+        if (r != kWsPadIdx) k = std::max(k, len(r));
+      }
+      width[(uint64_t)w * NS + j] = (k + 3u) & ~3u;
+    }
+  }
+  std::vector<uint32_t> soff(nsl + 1, 0);
+  uint64_t acc = 0;
+  for (uint64_t s = 0; s < nsl; ++s) {
+    soff[s] = (uint32_t)acc;
+    acc += (uint64_t)width[s] * 32u;
+    if (acc >= 0xffffffffull) throw Error(ERR_UNSUPPORTED, "windowed SELL layout exceeds 2^32 entries");
+  }
+  soff[nsl] = (uint32_t)acc;
+  ws_E_ = acc;
+  std::vector<uint32_t> src(ws_E_ + 16, kWsPadIdx);
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t s = 0; s < (int64_t)nsl; ++s)
+    for (uint32_t l = 0; l < 32; ++l) {
+      const uint32_t r = order[(uint64_t)s * 32 + l];
+      if (r == kWsPadIdx) continue;
+      const uint32_t L = len(r);
+      for (uint32_t k = 0; k < L; ++k) src[soff[s] + (k >> 2) * 128u + l * 4u + (k & 3u)] = rp[r] + k;
+    }
+  // CTA split: sort windows, balanced by stored entries
+  ws_G_ = (uint32_t)sm_count();
+  std::vector<uint32_t> cwin(ws_G_ + 1, 0);
+  uint64_t w = 0;
+  for (uint32_t c = 1; c < ws_G_; ++c) {
+    const uint64_t target = (ws_E_ * c + ws_G_ - 1) / ws_G_;
+    while (w < nwin && soff[w * NS] < target) ++w;
+    cwin[c] = (uint32_t)w;
+  }
+  cwin[ws_G_] = (uint32_t)nwin;
+  auto up = [&](DevBuf& b, const std::vector<uint32_t>& v) {
+    b.alloc(v.size() * 4 + 16);
+    F3RG_CUDA(cudaMemcpy(b.get(), v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+  };
+  up(ws_soff_, soff);
+  up(ws_row_, order);
+  up(ws_cwin_, cwin);
+  DevBuf dsrc;
+  up(dsrc, src);
+  ws_col_.alloc(ws_E_ * 4 + 64);
+  F3RG_CUDA(launch_ws_scatter(Launch{}, 4, dsrc.get<uint32_t>(), ci_.get(), ws_col_.get(), ws_E_, true));
+  for (int p = 0; p < 3; ++p) {
+    ws_val_[p].alloc(ws_E_ * psize(p) + 64);
+    F3RG_CUDA(launch_ws_scatter(Launch{}, (int)psize(p), dsrc.get<uint32_t>(), val_[p].get(), ws_val_[p].get(),
+                                ws_E_, false));
+  }
+  F3RG_CUDA(cudaDeviceSynchronize());
+}
+
 double DeviceMatrix::stream_bytes(int pa) const {
   const double n = (double)n_, nnz = (double)nnz_;
+  if (ws_E_) {  // windowed SELL: chunk-major columns + values (padding included), slice rows and offsets
+    const double E = (double)ws_E_, nsl = (double)((n_ + kWsSortRows - 1) / kWsSortRows) * (kWsSortRows / 32);
+    return E * (psize(pa) + 4.0) + nsl * 32.0 * 4.0 + (nsl + 1.0) * 4.0;
+  }
   return nnz * psize(pa) + (d16() ? 2.0 * nnz + 4.0 * n : 4.0 * nnz) + 4.0 * (n + 1);
 }
 
@@ -266,6 +354,14 @@ TilesDev DeviceMatrix::tiles(int p) const {
   t.shape = (uint32_t)shape_;
   t.perm = perm_.get<const uint32_t>();
   t.l2hint = l2hint_;
+  if (ws_E_) {
+    t.ws_soff = ws_soff_.get<const uint32_t>();
+    t.ws_row = ws_row_.get<const uint32_t>();
+    t.ws_col = ws_col_.get<const uint32_t>();
+    t.ws_val = ws_val_[p].get();
+    t.ws_cwin = ws_cwin_.get<const uint32_t>();
+    t.ws_G = ws_G_;
+  }
   return t;
 }
 

@@ -141,7 +141,8 @@ class DeviceMatrix {
   bool d16() const { return dcol_.get() != nullptr; }  // 16-bit delta column stream in use
   // bytes one pass over replica pa streams: values, the column stream in use, row_ptr
   double stream_bytes(int pa) const;
-  int shape() const { return shape_; }  // tile shape: 0 regular, 1 short rows, 2 gather-bound
+  int shape() const { return shape_; }  // 0 regular, 1 short rows, 2 gather-bound, 3 windowed SELL
+  uint64_t ws_entries() const { return ws_E_; }  // stored entries of the windowed layout (0: none)
 
  private:
   void init(const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, uint64_t ncols,
@@ -149,6 +150,10 @@ class DeviceMatrix {
   uint64_t n_ = 0, nnz_ = 0;
   DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_, pk_;
   DevBuf perm_, srp_, sci_, sval_[3], sdcol_, sfirst_, spk_;  // row-sorted copy (irregular rows)
+  DevBuf ws_soff_, ws_row_, ws_col_, ws_val_[3], ws_cwin_;  // windowed SELL layout (shape 3)
+  uint64_t ws_E_ = 0;
+  uint32_t ws_G_ = 0;
+  void build_wsell(const uint32_t* row_ptr);
   uint32_t ntiles_[3] = {0, 0, 0};
   uint32_t l2hint_ = 0;  // L2 eviction priorities for the passes (init)
   int shape_ = 0;

@@ -65,11 +65,11 @@ struct EpiBiT {
 // ---- CG ---------------------------------------------------------------------------
 // q = A p, pq = (p, q); alpha = rz / pq, or stop on pq <= 0 (src/cg.cpp:49-52)
 template <int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_cg_spmv(CsrDev A, TilesDev T, const double* p, double* q,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_cg_spmv(CsrDev A, TilesDev T, const double* p, double* q,
                                                                KState* S, Sync sync) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[tile_scratch(IDX)];
   __shared__ double tot[1];
   if (S->stop) return;
   GatherPlain<P64, P64> g{p};
@@ -191,11 +191,11 @@ __global__ void __launch_bounds__(256) k_bi_p(double* p, const double* v, const 
 
 // phat = M p = p; v = A phat; (rhat, v); alpha = rho / (rhat, v) (src/cg.cpp:120-129)
 template <int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_bi_v(CsrDev A, TilesDev T, const double* p, double* v,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_bi_v(CsrDev A, TilesDev T, const double* p, double* v,
                                                             const double* rhat, KState* S, Sync sync) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[tile_scratch(IDX)];
   __shared__ double tot[1];
   if (S->stop) return;
   GatherPlain<P64, P64> g{p};
@@ -225,11 +225,11 @@ __global__ void __launch_bounds__(256) k_bi_s(double* s, const double* r, const 
 // shat = M s = s; t = A shat; omega = (t, s) / (t, t), or the t = 0 cases
 // (src/cg.cpp:131-147)
 template <int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_bi_t(CsrDev A, TilesDev T, const double* s,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_bi_t(CsrDev A, TilesDev T, const double* s,
                                                             const double* shat, double* t, KState* S, Sync sync) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64 * 3];
+  __shared__ double scratch[tile_scratch(IDX) * 3];
   __shared__ double tot[3];
   if (S->stop) return;
   GatherPlain<P64, P64> g{shat};

@@ -146,6 +146,10 @@ cudaError_t launch_dot(int px, int py, int floor_p, Launch l, const void* x, con
 cudaError_t launch_norm2(int px, Launch l, const void* x, uint64_t n, double* out, SyncH sync, DistH dist = {});
 cudaError_t launch_permute_rows(Launch l, int esize, const uint32_t* rp_old, const uint32_t* rp_new,
                                 const uint32_t* perm, const void* src, void* dst, uint64_t n);
+// windowed SELL layout: out[e] = in[src[e]] (esize bytes, bit copy), or the pad
+// (all ones if pad_ones, else zero) where src[e] == 0xffffffff
+cudaError_t launch_ws_scatter(Launch l, int esize, const uint32_t* src, const void* in, void* out, uint64_t cnt,
+                              bool pad_ones);
 cudaError_t launch_pack16(Launch l, const void* val16, const uint16_t* dcol, uint32_t* out, uint64_t nnz);
 // dst[i] = src[idx[i]], i < cnt, at precision p (halo pack / gather)
 cudaError_t launch_gather(int p, Launch l, const void* src, const uint32_t* idx, uint64_t cnt, void* dst);

@@ -7,7 +7,9 @@ namespace f3rg {
 
 template <class F>
 static void with_idx64(const CsrDev& A, const TilesDev& T, F&& go) {
-  if (T.shape == 1) {
+  if (T.shape == 3) {
+    go(PC<16>{});
+  } else if (T.shape == 1) {
     if (A.dcol) go(PC<5>{});
     else go(PC<4>{});
   } else if (T.shape == 2) {
@@ -26,6 +28,11 @@ static int tile_grid(int occ, uint32_t ntiles) {
   if (g > (long)ntiles) g = ntiles;
   return g < 1 ? 1 : (int)g;
 }
+// the windowed engine runs exactly the CTA count its windows were split over
+template <int IDX>
+static int krylov_grid(int occ, const TilesDev& T) {
+  return idx_wsell(IDX) ? (int)T.ws_G : tile_grid(occ, T.ntiles);
+}
 
 cudaError_t launch_cg_spmv(Launch l, const CsrDev& A, const TilesDev& T, const double* p, double* q, KState* S,
                            SyncH sync) {
@@ -34,8 +41,8 @@ cudaError_t launch_cg_spmv(Launch l, const CsrDev& A, const TilesDev& T, const d
     constexpr int IDX = decltype(I)::value;
     constexpr int SM = TileCfg<P64, IDX>::SMEM_BYTES;
     auto kern = k_cg_spmv<IDX>;
-    static const int occ = occupancy_blocks(kern, SM);  // also sets the dynamic smem limit
-    err = launch_k(kern, tile_grid(occ, T.ntiles), SM, l.stream, A, T, p, q, S, to_sync(sync));
+    static const int occ = occupancy_blocks(kern, SM, tile_threads(IDX));  // also sets the dynamic smem limit
+    err = launch_kt(kern, krylov_grid<IDX>(occ, T), tile_threads(IDX), SM, l.stream, A, T, p, q, S, to_sync(sync));
   });
   return err;
 }
@@ -70,8 +77,8 @@ cudaError_t launch_bi_v(Launch l, const CsrDev& A, const TilesDev& T, const doub
     constexpr int IDX = decltype(I)::value;
     constexpr int SM = TileCfg<P64, IDX>::SMEM_BYTES;
     auto kern = k_bi_v<IDX>;
-    static const int occ = occupancy_blocks(kern, SM);  // also sets the dynamic smem limit
-    err = launch_k(kern, tile_grid(occ, T.ntiles), SM, l.stream, A, T, p, v, rhat, S, to_sync(sync));
+    static const int occ = occupancy_blocks(kern, SM, tile_threads(IDX));  // also sets the dynamic smem limit
+    err = launch_kt(kern, krylov_grid<IDX>(occ, T), tile_threads(IDX), SM, l.stream, A, T, p, v, rhat, S, to_sync(sync));
   });
   return err;
 }
@@ -87,8 +94,8 @@ cudaError_t launch_bi_t(Launch l, const CsrDev& A, const TilesDev& T, const doub
     constexpr int IDX = decltype(I)::value;
     constexpr int SM = TileCfg<P64, IDX>::SMEM_BYTES;
     auto kern = k_bi_t<IDX>;
-    static const int occ = occupancy_blocks(kern, SM);  // also sets the dynamic smem limit
-    err = launch_k(kern, tile_grid(occ, T.ntiles), SM, l.stream, A, T, s, shat, t, S, to_sync(sync));
+    static const int occ = occupancy_blocks(kern, SM, tile_threads(IDX));  // also sets the dynamic smem limit
+    err = launch_kt(kern, krylov_grid<IDX>(occ, T), tile_threads(IDX), SM, l.stream, A, T, s, shat, t, S, to_sync(sync));
   });
   return err;
 }

@@ -78,4 +78,32 @@ cudaError_t launch_permute_rows(Launch l, int esize, const uint32_t* rp_old, con
   return cudaGetLastError();
 }
 
+// Windowed SELL layout (wsell.cuh, engine.cpp build_wsell): entry e of the layout is
+// CSR entry src[e] (kWsPad: a padding slot). Columns get kWsPad, values +0 there
+// (never read: the engine skips padded columns); everything else is copied bit for bit.
+template <class E>
+__global__ void __launch_bounds__(256) k_ws_scatter(const uint32_t* src, const E* in, E* out, uint64_t cnt, E pad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += stride) {
+    const uint32_t k = src[e];
+    out[e] = k == 0xffffffffu ? pad : in[k];
+  }
+}
+
+cudaError_t launch_ws_scatter(Launch l, int esize, const uint32_t* src, const void* in, void* out, uint64_t cnt,
+                              bool pad_ones) {
+  const int g = l.grid ? l.grid : stream_grid();
+  switch (esize) {
+    case 2: k_ws_scatter<<<g, kThreads, 0, l.stream>>>(src, static_cast<const uint16_t*>(in),
+                                                        static_cast<uint16_t*>(out), cnt, (uint16_t)0); break;
+    case 4: k_ws_scatter<<<g, kThreads, 0, l.stream>>>(src, static_cast<const uint32_t*>(in),
+                                                        static_cast<uint32_t*>(out), cnt,
+                                                        pad_ones ? 0xffffffffu : 0u); break;
+    case 8: k_ws_scatter<<<g, kThreads, 0, l.stream>>>(src, static_cast<const unsigned long long*>(in),
+                                                        static_cast<unsigned long long*>(out), cnt, 0ull); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace f3rg

@@ -15,6 +15,8 @@ namespace f3rg {
 
 // column stream of a launch: P16 (packed fp16 value + delta) for the fp16 replica
 // when present, else D16, else u32; plus the matrix's tile shape (IDX bit 2)
+// shape 3: the windowed SELL engine (wsell.cuh), whose own layout replaces the
+// column streams
 template <int PA, int SH, class F>
 inline void dispatch_col(const CsrDev& A, F&& go) {
   if constexpr (PA == P16) {
@@ -25,17 +27,33 @@ inline void dispatch_col(const CsrDev& A, F&& go) {
 }
 template <int PA, class F>
 inline void dispatch_idx(const CsrDev& A, const TilesDev& T, F&& go) {
-  if (T.shape == 1) dispatch_col<PA, 4>(A, go);
+  if (T.shape == 3) go(std::integral_constant<int, 16>{});
+  else if (T.shape == 1) dispatch_col<PA, 4>(A, go);
   else if (T.shape == 2) dispatch_col<PA, 8>(A, go);
   else dispatch_col<PA, 0>(A, go);
 }
 
 template <class K>
-inline int tile_kernel_grid(K kern, int smem, uint32_t ntiles, bool cap_by_tiles) {
-  const int occ = occupancy_blocks(kern, smem);
+inline int tile_kernel_grid(K kern, int smem, uint32_t ntiles, bool cap_by_tiles, int threads = kThreads) {
+  const int occ = occupancy_blocks(kern, smem, threads);
   long g = (long)occ * sm_count();
   if (cap_by_tiles && g > (long)ntiles) g = ntiles;
   return g < 1 ? 1 : (int)g;
+}
+
+// grid of one tile-kernel launch: the occupancy-derived persistent grid (capped by
+// the tile count, or the caller's override), or, for the windowed engine, exactly
+// the CTA count its window split was made for
+template <int IDX, class K>
+inline int tile_launch_grid(K kern, int smem, const TilesDev& T, int override_grid) {
+  static const int g0 = tile_kernel_grid(kern, smem, T.ntiles, false, tile_threads(IDX));
+  if constexpr (idx_wsell(IDX)) {
+    (void)override_grid;
+    return (int)T.ws_G;
+  } else {
+    int g = override_grid ? override_grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+    return g < 1 ? 1 : g;
+  }
 }
 
 template <int PA>
@@ -52,12 +70,10 @@ cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const 
         constexpr int PZ = decltype(Z)::value;
         if constexpr (PZ <= PW) {
           auto kern = k_spmv_dots<PA, PZ, PW, IDX>;
-          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
           if (dist.mode == 2) g = 1;
-          if (g < 1) g = 1;
           if (grid_out) *grid_out = g;
-          launch_k(kern, g, SM, l.stream, A, T, z, V, ld, j, L, to_gate(gate), to_sync(sync), dots, defer,
+          launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, z, V, ld, j, L, to_gate(gate), to_sync(sync), dots, defer,
                                               to_dist(dist));
           err = cudaGetLastError();
         }
@@ -81,11 +97,9 @@ cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const T
         constexpr int PW = decltype(W)::value;
         if constexpr (PW >= PX) {
           auto kern = k_residual<PA, PX, PW, IDX>;
-          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
           if (dist.mode == 2) g = 1;
-          if (g < 1) g = 1;
-          launch_k(kern, g, SM, l.stream, A, T, x, b, r, L, out_norm, to_sync(sync), to_dist(dist));
+          launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, x, b, r, L, out_norm, to_sync(sync), to_dist(dist));
           err = cudaGetLastError();
         }
       });
@@ -104,9 +118,8 @@ cudaError_t launch_spmv_t(int px, int py, Launch l, const CsrDev& A, const Tiles
     with_p(px, [&](auto X) {
       with_p(py, [&](auto Y) {
         auto kern = k_spmv<PA, decltype(X)::value, decltype(Y)::value, IDX>;
-        static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-        const int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
-        launch_k(kern, g, SM, l.stream, A, T, x, y);
+        const int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
+        launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, x, y);
         err = cudaGetLastError();
       });
     });
@@ -131,11 +144,11 @@ cudaError_t launch_richardson_t(int pw, int pv, Launch l, const CsrDev& A, const
         constexpr int PW = decltype(W)::value;
         if constexpr (PW <= PV) {
           auto kern = k_richardson<PA, PW, PV, IDX>;
-          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-          const int g = l.grid ? l.grid : g0;
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false, tile_threads(IDX));
+          const int g = idx_wsell(IDX) ? (int)T.ws_G : l.grid ? l.grid : g0;
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3(g);
-          cfg.blockDim = dim3(kThreads);
+          cfg.blockDim = dim3(tile_threads(IDX));
           cfg.dynamicSmemBytes = SM;
           cfg.stream = l.stream;
           cudaLaunchAttribute attr[1];
@@ -169,11 +182,9 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
         constexpr int PW = decltype(W)::value;
         if constexpr (PW <= PV) {
           auto kern = k_rich_phase<PA, PW, PV, IDX>;
-          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
           if (phase == PH_BOOK) g = 1;
-          if (g < 1) g = 1;
-          launch_k(kern, g, SM, l.stream, A, T, phase, k, v, v_scale, off, out, n, RS, R, Za, to_gate(gate), level,
+          launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, phase, k, v, v_scale, off, out, n, RS, R, Za, to_gate(gate), level,
                                               cnt, to_sync(sync), to_dist(dist));
           err = cudaGetLastError();
         }
@@ -198,11 +209,9 @@ cudaError_t launch_richm_phase_t(int pw, int pv, Launch l, const CsrDev& A, cons
         constexpr int PW = decltype(W)::value;
         if constexpr (PW <= PV) {
           auto kern = k_richm_phase<PA, PW, PV, IDX>;
-          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false);
-          int g = l.grid ? l.grid : (g0 > (int)T.ntiles ? (int)T.ntiles : g0);
+          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
           if (phase == RM_BOOK) g = 1;
-          if (g < 1) g = 1;
-          launch_k(kern, g, SM, l.stream, A, T, phase, k, v, v_scale, out, n, RS, R, P, Za, to_gate(gate), level, cnt,
+          launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, phase, k, v, v_scale, out, n, RS, R, P, Za, to_gate(gate), level, cnt,
                    to_sync(sync));
           err = cudaGetLastError();
         }

@@ -273,12 +273,12 @@ __device__ __forceinline__ void spmv_dots_body(const CsrDev& A, const TilesDev& 
 // partials are written (to `dots`); the following k_cgs reduces them.
 // V: slot 0 of the basis (owned rows); ld: slot stride; z: the SpMV input (ext layout)
 template <int PA, int PZ, int PW, int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t ld, int j,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_spmv_dots(CsrDev A, TilesDev T, const void* z, void* V, uint64_t ld, int j,
                                                    LevelState* L, Gate gate, Sync sync, double* dots, int defer,
                                                    Dist dist) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[tile_scratch(IDX)];
   __shared__ double res[8];
   if (gate.closed()) return;
   if (dist.mode == 2) {
@@ -708,11 +708,11 @@ struct EpiResidual {
 // also written to *out_norm.
 // x: ext layout (gathered); b, r: owned rows
 template <int PA, int PX, int PW, int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_residual(CsrDev A, TilesDev T, const void* x, const double* b, void* r,
                                                   LevelState* L, double* out_norm, Sync sync, Dist dist) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[tile_scratch(IDX)];
   __shared__ double tot[1];
   if (dist.mode != 2) {
     constexpr int C = pmax(PA, PX);

@@ -61,6 +61,10 @@ struct GatherZ1 {
   __device__ __forceinline__ void set_policy(uint64_t) {}
   __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(Ar<PW>::mul(w0, rhs.apply(r))); }
+  // windowed engine: the ring holds z1 itself (wsell.cuh WsRing)
+  using RingT = T_<PW>;
+  __device__ __forceinline__ RingT ring_put(Raw r) const { return Ar<PW>::mul(w0, rhs.apply(r)); }
+  __device__ __forceinline__ T_<C> ring_get(RingT z) const { return cvt<C>(z); }
 };
 
 // the right-hand side itself as the SpMV operand (update call, step 0: p = r = v)
@@ -71,6 +75,9 @@ struct GatherRhs {
   __device__ __forceinline__ void set_policy(uint64_t) {}
   __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
+  using RingT = T_<PW>;
+  __device__ __forceinline__ RingT ring_put(Raw r) const { return rhs.apply(r); }
+  __device__ __forceinline__ T_<C> ring_get(RingT z) const { return cvt<C>(z); }
 };
 
 // one fused step k >= 1: r = v - A z_k ; z_{k+1} = z_k + w_k r  (M = I, p = r)
@@ -135,13 +142,13 @@ struct EpiResid {
 // calls and the per-call bookkeeping run as k_rich_phase launches with the
 // cross-rank exchanges between them
 template <int PA, int PW, int PV, int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_richardson(CsrDev A, TilesDev T, const void* v, const double* v_scale,
                                                     void* out, uint64_t n, RichState* RS, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, unsigned* bar_count,
                                                     unsigned* bar_gen, const IoSlot* io, uint64_t voff, int flags) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[tile_scratch(IDX)];
   __shared__ double red[2];
   if (gate.closed()) return;
   if (io) {
@@ -299,13 +306,13 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_richardson(CsrDev A, Ti
 enum { PH_RESID = 0, PH_DOTS = 1, PH_UPDATE = 2, PH_BOOK = 3 };
 
 template <int PA, int PW, int PV, int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_rich_phase(CsrDev A, TilesDev T, int phase, int k, const void* v,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_rich_phase(CsrDev A, TilesDev T, int phase, int k, const void* v,
                                                     const double* v_scale, uint64_t off, void* out, uint64_t n,
                                                     RichState* RS, void* R, void* Za, Gate gate, int level,
                                                     unsigned long long* cnt, Sync sync, Dist dist) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[tile_scratch(IDX)];
   __shared__ double tot[2];
   if (gate.closed()) return;
   constexpr int C = pmax(PA, PW);
@@ -399,14 +406,14 @@ __global__ void __launch_bounds__(256, tile_minb(IDX)) k_rich_phase(CsrDev A, Ti
 enum { RM_START = 0, RM_RESID = 1, RM_DOTS = 2, RM_UPDATE = 3, RM_BOOK = 4 };
 
 template <int PA, int PW, int PV, int IDX>
-__global__ void __launch_bounds__(256, tile_minb(IDX)) k_richm_phase(CsrDev A, TilesDev T, int phase, int k,
+__global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_richm_phase(CsrDev A, TilesDev T, int phase, int k,
                                                                      const void* v, const double* v_scale,
                                                                      void* out, uint64_t n, RichState* RS, void* R,
                                                                      void* P, void* Za, Gate gate, int level,
                                                                      unsigned long long* cnt, Sync sync) {
   pdl_wait();
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ double scratch[64];
+  __shared__ double scratch[tile_scratch(IDX)];
   __shared__ double tot[2];
   if (gate.closed()) return;
   constexpr int C = pmax(PA, PW);

@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "state.hpp"
+#include "wsell.cuh"
 
 #ifndef F3RG_TILE_MINB  // tile kernels: min CTAs per SM (register budget)
 #define F3RG_TILE_MINB 3
@@ -90,11 +91,16 @@
 namespace f3rg {
 
 // IDX of the tiled kernels: bits 0-1 = column stream (0 u32, 1 D16, 2 P16),
-// bit 2 = short-row shape, bit 3 = gather-bound shape
+// bit 2 = short-row shape, bit 3 = gather-bound shape, bit 4 = the windowed SELL
+// engine (wsell.cuh: one 1024-thread CTA per SM, its own layout)
 constexpr int idx_col(int idx) { return idx & 3; }
 constexpr bool idx_short(int idx) { return (idx & 4) != 0; }
 constexpr bool idx_gather(int idx) { return (idx & 8) != 0; }
-constexpr int tile_minb(int idx) { return idx_short(idx) ? F3RG_SHORT_MINB : F3RG_TILE_MINB; }
+constexpr bool idx_wsell(int idx) { return (idx & 16) != 0; }
+constexpr int tile_minb(int idx) { return idx_wsell(idx) ? 1 : idx_short(idx) ? F3RG_SHORT_MINB : F3RG_TILE_MINB; }
+constexpr int tile_threads(int idx) { return idx_wsell(idx) ? kWsThreads : 256; }
+// block_sum scratch of a tile kernel: 8 values per warp
+constexpr int tile_scratch(int idx) { return tile_threads(idx) / 32 * 8; }
 
 template <int PA, int IDX_ = 0>
 struct TileCfg {
@@ -120,7 +126,7 @@ struct TileCfg {
   static constexpr int RP_BYTES = (NT + 12) * 4;
   static constexpr int FIRST_BYTES = IDX >= 1 ? (NT + 12) * 4 : 0;
   static constexpr int STAGE_BYTES = VAL_BYTES + COL_BYTES + RP_BYTES + FIRST_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 64;
+  static constexpr int SMEM_BYTES = idx_wsell(IDX_) ? kWsSmem : STAGES * STAGE_BYTES + 64;
 };
 
 // Streams all tiles owned by this CTA (tile t = blockIdx.x + i*gridDim.x) through
@@ -128,7 +134,7 @@ struct TileCfg {
 // C = promote(PA, gather precision).
 // CH: gather chunk (0 = default: F3RG_CHUNK, or F3RG_P16_CHUNK for the P16 stream)
 template <int PA, int C, int IDX_, int CH = 0, class Gather, class Epi>
-__device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
+__device__ __forceinline__ void spmv_row_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
   g.set_policy(l2_policy(T.l2hint ? 2 : 0));  // the gathered vector
   using Cfg = TileCfg<PA, IDX_>;
   const uint64_t spol = l2_policy(T.l2hint ? 1 : 0);  // the matrix streams
@@ -304,6 +310,14 @@ __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, G
   if (tid == 0)
     for (int s = 0; s < ST; ++s) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
   pdl_trigger();
+}
+
+// The SpMV engine of a tile kernel: the row tiles above, or the windowed SELL
+// engine (IDX bit 4, gather-bound matrices) -- same per-row sums either way.
+template <int PA, int C, int IDX_, int CH = 0, class Gather, class Epi>
+__device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
+  if constexpr (idx_wsell(IDX_)) wsell_pass<PA, C>(A, T, g, e, smem);
+  else spmv_row_tiles<PA, C, IDX_, CH>(A, T, g, e, smem);
 }
 
 // ---- gathers ----------------------------------------------------------------------

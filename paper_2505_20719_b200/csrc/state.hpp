@@ -25,6 +25,10 @@ struct CsrDev {
   const uint32_t* pk = nullptr;     // nnz (+pad)
 };
 
+// windowed SELL layout constants (wsell.cuh; built by engine.cpp build_wsell)
+constexpr uint32_t kWsSortRows = 2048;      // rows per sort window
+constexpr uint32_t kWsPadIdx = 0xffffffffu;  // padding slot / padding lane
+
 struct TilesDev {
   const uint32_t* r0 = nullptr;  // ntiles+1 row starts
   const uint32_t* k0 = nullptr;  // ntiles+1 nnz starts (= rp[r0])
@@ -42,6 +46,15 @@ struct TilesDev {
   // sorted-row tiles (irregular row lengths): tile row q is matrix row perm[q]; the
   // CsrDev handed with these tiles stores the rows in that order. Null = identity
   const uint32_t* perm = nullptr;
+  // windowed SELL layout (shape 3, wsell.cuh): slice entry offsets (slices+1), slice
+  // lane -> matrix row (slices*32), chunk-major columns and values at this replica's
+  // precision, and the split of the sort windows over ws_G CTAs (ws_G+1)
+  const uint32_t* ws_soff = nullptr;
+  const uint32_t* ws_row = nullptr;
+  const uint32_t* ws_col = nullptr;
+  const void* ws_val = nullptr;
+  const uint32_t* ws_cwin = nullptr;
+  uint32_t ws_G = 0;
 };
 
 // Device-resident state of one FGMRES level. H is column-major: column j holds

@@ -1,0 +1,278 @@
+// wsell.cuh -- windowed SELL-32 SpMV engine for gather-bound matrices (config 5:
+// n = 2e7 unstructured rows whose columns scatter +-15,000 around the diagonal plus
+// 5 % uniform long-range entries).
+//
+// Why: with one thread per row and the gathered vector read through L1 (the tile
+// engine, spmv.cuh), every entry of such a matrix is its own 128-byte line request;
+// the L1 tag stage serves about one line per clock per SM, which is exactly the
+// 2 ms the config-5 fp16 pass took (4.1 M lines per SM at 1.965 GHz). Here the
+// gathered vector lives in shared memory instead: each persistent CTA (one per SM,
+// 1024 threads) owns a contiguous run of rows and keeps the band of x those rows
+// can touch in a 128 KB ring, slid forward window by window with plain loads issued
+// one window ahead. Gathers inside the band are shared-memory loads; the rest (the
+// long-range 5 %) go to L2 with an evict-last policy.
+//
+// Layout (host: engine.cpp build_wsell; device arrays in TilesDev ws_*):
+//  * sort windows of kWsSort = 2048 consecutive rows; inside a window the rows are
+//    ordered by length (descending, stable) and cut into 64 slices of 32 rows;
+//  * a slice stores its entries chunk-major: chunk q (entries 4q..4q+3 of every
+//    lane's row) is 32 lanes x 4 entries, so lane l reads one 16-byte column quad
+//    and one 8/16/32-byte value quad per chunk, fully coalesced across the warp;
+//    a slice is as wide as its longest row rounded up to 4; missing entries carry
+//    the column kWsPad and are skipped (never added as zeros: -0 + +0 = +0);
+//  * ws_row maps slice lane -> matrix row; ws_cwin splits the windows over the
+//    CTAs by stored entries.
+// Each row is still summed by one thread in stored column order at
+// C = promote(TA, TX), each product and sum rounded to C (src/csr.cpp:23-37), so
+// results are bit-identical to the tile engine and to the reference.
+//
+// Per kernel window of TW rows (TW = a multiple of kWsSort, set by the ring element
+// size): warps claim slices in descending-length order (longest processing time
+// first, so the window's tail is one short slice), write each row's sum into a
+// shared-memory buffer at the row's position, then, after one CTA barrier, the
+// epilogue runs over the window's rows in natural order (coalesced row-local
+// operands). Ring invariant for the window at rows [B, B+TW): the ring holds
+// x[B-W, B+2TW+W) (RN = 2TW + 2W elements): the gathers' band [B-W, B+TW+W) plus
+// the top block of the next window's band; the block after that is loaded into
+// registers at the window's start and stored after its barrier into the slots the
+// window just freed.
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "state.hpp"
+
+namespace f3rg {
+
+constexpr int kWsThreads = 1024;
+constexpr int kWsSort = (int)kWsSortRows;   // rows per sort window (layout unit)
+constexpr int kWsSlices = kWsSort / 32;     // slices per sort window
+constexpr int kWsRingBytes = 128 * 1024;    // the x band
+constexpr int kWsYBytes = 64 * 1024;        // two row-sum buffers
+constexpr int kWsSmem = kWsRingBytes + kWsYBytes + 64;
+constexpr uint32_t kWsPad = kWsPadIdx;
+#ifndef F3RG_WS_U  // column/value quads per lane per pipeline step
+#define F3RG_WS_U 2
+#endif
+
+// What the ring stores for a gather: its raw load, or (gathers with a per-element
+// transform, e.g. Richardson's z1 = w0 * v) the transformed value, so the transform
+// runs once per ring element instead of once per gathered entry.
+template <class G, class = void>
+struct WsRing {
+  using R = typename G::Raw;
+  __device__ __forceinline__ static R put(const G&, typename G::Raw r) { return r; }
+  __device__ __forceinline__ static auto get(const G& g, R r) { return g.value(r); }
+};
+template <class G>
+struct WsRing<G, std::void_t<typename G::RingT>> {
+  using R = typename G::RingT;
+  __device__ __forceinline__ static R put(const G& g, typename G::Raw r) { return g.ring_put(r); }
+  __device__ __forceinline__ static auto get(const G& g, R r) { return g.ring_get(r); }
+};
+
+// streamed loads: read once, do not allocate in L1, L2 policy from the caller
+__device__ __forceinline__ uint4 ws_ld16(const void* p, uint64_t pol) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint2 ws_ld8(const void* p, uint64_t pol) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+// one lane's 4 values of a chunk
+template <int PA>
+struct WsVals;
+template <>
+struct WsVals<P16> {
+  uint2 q;
+  __device__ __forceinline__ void load(const void* base, uint64_t quad, uint64_t pol) {
+    q = ws_ld8(static_cast<const uint2*>(base) + quad, pol);
+  }
+  __device__ __forceinline__ void zero() { q = make_uint2(0u, 0u); }
+  __device__ __forceinline__ __half at(int e) const {
+    const uint32_t w = e < 2 ? q.x : q.y;
+    return __ushort_as_half((unsigned short)((e & 1) ? (w >> 16) : (w & 0xffffu)));
+  }
+};
+template <>
+struct WsVals<P32> {
+  uint4 q;
+  __device__ __forceinline__ void load(const void* base, uint64_t quad, uint64_t pol) {
+    q = ws_ld16(static_cast<const uint4*>(base) + quad, pol);
+  }
+  __device__ __forceinline__ void zero() { q = make_uint4(0u, 0u, 0u, 0u); }
+  __device__ __forceinline__ float at(int e) const {
+    return __uint_as_float(e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w);
+  }
+};
+template <>
+struct WsVals<P64> {
+  uint4 a, b;
+  __device__ __forceinline__ void load(const void* base, uint64_t quad, uint64_t pol) {
+    a = ws_ld16(static_cast<const uint4*>(base) + 2 * quad, pol);
+    b = ws_ld16(static_cast<const uint4*>(base) + 2 * quad + 1, pol);
+  }
+  __device__ __forceinline__ void zero() { a = b = make_uint4(0u, 0u, 0u, 0u); }
+  __device__ __forceinline__ double at(int e) const {
+    const uint4& h = e < 2 ? a : b;
+    return (e & 1) ? __hiloint2double((int)h.w, (int)h.z) : __hiloint2double((int)h.y, (int)h.x);
+  }
+};
+__device__ __forceinline__ uint32_t quad_at(const uint4& q, int e) {
+  return e == 0 ? q.x : e == 1 ? q.y : e == 2 ? q.z : q.w;
+}
+
+// Streams this CTA's windows; calls e.prefetch(i); e.row(i, acc) for every row i in
+// natural order, acc at C. Launch: gridDim.x == T.ws_G, blockDim.x == kWsThreads,
+// kWsSmem bytes of dynamic shared memory. Square matrices on one rank only (x has
+// n elements).
+template <int PA, int C, class G, class Epi>
+__device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G& g, Epi& e, uint8_t* smem) {
+  using RT = WsRing<G>;
+  using R = typename RT::R;
+  using Raw = typename G::Raw;
+  using TA = T_<PA>;
+  constexpr int RS = (int)sizeof(R);
+  constexpr int RN = kWsRingBytes / RS;  // ring elements (power of two)
+  constexpr int CS = (int)sizeof(T_<C>);
+  // rows per kernel window: as many as the ring keeps a wide band for, and the two
+  // row-sum buffers fit
+  constexpr int TW = (16384 / RS < 32768 / CS) ? 16384 / RS : 32768 / CS;
+  constexpr int KW = TW / kWsSort;  // sort windows per kernel window
+  constexpr int W = (RN - 2 * TW) / 2;
+  constexpr int PF = TW / kWsThreads;  // ring elements each thread carries one window ahead
+  constexpr uint32_t SPAN = (uint32_t)(TW + 2 * W);
+  constexpr int U = PA == P64 ? 1 : F3RG_WS_U;
+  static_assert(TW % kWsSort == 0 && W > 0 && PF >= 1 && (RN & (RN - 1)) == 0, "window geometry");
+  static_assert(2 * TW * CS <= kWsYBytes, "row-sum buffers");
+
+  R* ring = reinterpret_cast<R*>(smem);
+  T_<C>* ybuf = reinterpret_cast<T_<C>*>(smem + kWsRingBytes);
+  unsigned* claim = reinterpret_cast<unsigned*>(smem + kWsRingBytes + kWsYBytes);
+  g.set_policy(l2_policy(T.l2hint ? 2 : 0));             // far gathers: keep x in L2
+  const uint64_t spol = l2_policy(T.l2hint ? 1 : 0);     // the matrix stream
+  const int64_t n = (int64_t)A.n;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+  const uint32_t sw0 = T.ws_cwin[blockIdx.x], sw1 = T.ws_cwin[blockIdx.x + 1];
+  const TA* __restrict__ vals = static_cast<const TA*>(T.ws_val);
+  (void)vals;
+
+  __syncthreads();  // a previous pass in the same kernel is done with the ring
+  if (tid < 2) claim[tid] = 0u;
+  if (sw0 < sw1) {  // ring for the first window: x[B0-W, B0+2TW+W)
+    const int64_t B0 = (int64_t)sw0 * kWsSort;
+    int64_t i0 = B0 - W;
+    if (i0 < 0) i0 = 0;
+    int64_t i1 = B0 + 2 * TW + W;
+    if (i1 > n) i1 = n;
+    for (int64_t i = i0 + tid; i < i1; i += kWsThreads) ring[i & (RN - 1)] = RT::put(g, g.load((uint32_t)i));
+  }
+  __syncthreads();
+
+  uint32_t it = 0;
+  for (uint32_t sw = sw0; sw < sw1; sw += KW, ++it) {
+    const int64_t B = (int64_t)sw * kWsSort;
+    const uint32_t kw = (sw1 - sw) < (uint32_t)KW ? (sw1 - sw) : (uint32_t)KW;
+    // the ring block two windows ahead, into registers now, into the ring after the barrier
+    const int64_t pb = B + 2 * TW + W;
+    Raw pf[PF];
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int64_t i = pb + (int64_t)q * kWsThreads + tid;
+      if (i < n) pf[q] = g.load((uint32_t)i);
+    }
+    const uint32_t lo = (uint32_t)(int32_t)(B - W);  // band [B-W, B+TW+W), wraps below 0
+    T_<C>* yb = ybuf + (it & 1u) * TW;
+    const uint32_t nsl = kw * (uint32_t)kWsSlices;
+    unsigned* cl = &claim[it & 1u];
+    for (;;) {
+      uint32_t j = 0;
+      if (lane == 0) j = atomicAdd(cl, 1u);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      if (j >= nsl) break;
+      // claim order: slice rank j / kw of sort window j % kw -- descending length
+      const uint32_t s = (sw + j % kw) * (uint32_t)kWsSlices + j / kw;
+      const uint32_t e0 = __ldg(T.ws_soff + s), e1 = __ldg(T.ws_soff + s + 1);
+      const uint32_t row = __ldg(T.ws_row + (size_t)s * 32 + lane);
+      const uint32_t nq = (e1 - e0) >> 7;  // chunks: 32 lanes x 4 entries
+      const uint64_t qb = (uint64_t)(e0 >> 2) + lane;  // this lane's quad of chunk 0
+      T_<C> acc = Ar<C>::zero();
+      uint4 cc[U], cn[U];
+      WsVals<PA> vc[U], vn[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if ((uint32_t)u < nq) {
+          cc[u] = ws_ld16(reinterpret_cast<const uint4*>(T.ws_col) + qb + (uint64_t)u * 32, spol);
+          vc[u].load(T.ws_val, qb + (uint64_t)u * 32, spol);
+        } else {
+          cc[u] = make_uint4(kWsPad, kWsPad, kWsPad, kWsPad);
+          vc[u].zero();
+        }
+      }
+      for (uint32_t q0 = 0; q0 < nq; q0 += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {  // next step's stream, in flight during this one
+          const uint32_t q = q0 + U + u;
+          if (q < nq) {
+            cn[u] = ws_ld16(reinterpret_cast<const uint4*>(T.ws_col) + qb + (uint64_t)q * 32, spol);
+            vn[u].load(T.ws_val, qb + (uint64_t)q * 32, spol);
+          } else {
+            cn[u] = make_uint4(kWsPad, kWsPad, kWsPad, kWsPad);
+            vn[u].zero();
+          }
+        }
+        R xr[4 * U];
+        Raw xf[4 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t c = quad_at(cc[u], k);
+            const bool in = c - lo < SPAN;
+            xr[4 * u + k] = in ? ring[c & (uint32_t)(RN - 1)] : R{};
+            xf[4 * u + k] = (!in && c != kWsPad) ? g.load(c) : Raw{};
+          }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t c = quad_at(cc[u], k);
+            if (c != kWsPad) {
+              const bool in = c - lo < SPAN;
+              const T_<C> xv = in ? RT::get(g, xr[4 * u + k]) : RT::get(g, RT::put(g, xf[4 * u + k]));
+              acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vc[u].at(k)), xv));
+            }
+          }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          cc[u] = cn[u];
+          vc[u] = vn[u];
+        }
+      }
+      if (row != kWsPad) yb[(uint32_t)((int64_t)row - B)] = acc;
+    }
+    __syncthreads();  // every row sum of the window is in yb; the band's bottom block is free
+    if (tid == 0) claim[it & 1u] = 0u;  // reused two windows on, after the next barrier
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const int64_t i = pb + (int64_t)q * kWsThreads + tid;
+      if (i < n) ring[i & (RN - 1)] = RT::put(g, pf[q]);
+    }
+    int64_t rend = B + (int64_t)kw * kWsSort;
+    if (rend > n) rend = n;
+    for (int64_t i = B + tid; i < rend; i += kWsThreads) {
+      e.prefetch((uint32_t)i);
+      e.row((uint32_t)i, yb[(uint32_t)(i - B)]);
+    }
+  }
+  pdl_trigger();
+}
+
+}  // namespace f3rg
