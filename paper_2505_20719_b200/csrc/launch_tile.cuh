@@ -44,9 +44,12 @@ inline int tile_kernel_grid(K kern, int smem, uint32_t ntiles, bool cap_by_tiles
 // grid of one tile-kernel launch: the occupancy-derived persistent grid (capped by
 // the tile count, or the caller's override), or, for the windowed engine, exactly
 // the CTA count its window split was made for
-template <int IDX, class K>
-inline int tile_launch_grid(K kern, int smem, const TilesDev& T, int override_grid) {
-  static const int g0 = tile_kernel_grid(kern, smem, T.ntiles, false, tile_threads(IDX));
+// (g0: the caller's per-instantiation cached tile_kernel_grid -- it must be a static
+// local of the generic lambda that names the kernel, NOT of a helper templated on
+// the kernel's pointer type: kernels of one signature would share it and all but
+// the first would miss their cudaFuncSetAttribute)
+template <int IDX>
+inline int tile_launch_grid(int g0, const TilesDev& T, int override_grid) {
   if constexpr (idx_wsell(IDX)) {
     (void)override_grid;
     return (int)T.ws_G;
@@ -70,7 +73,8 @@ cudaError_t launch_spmv_dots_t(int pz, int pw, Launch l, const CsrDev& A, const 
         constexpr int PZ = decltype(Z)::value;
         if constexpr (PZ <= PW) {
           auto kern = k_spmv_dots<PA, PZ, PW, IDX>;
-          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false, tile_threads(IDX));
+          int g = tile_launch_grid<IDX>(g0, T, l.grid);
           if (dist.mode == 2) g = 1;
           if (grid_out) *grid_out = g;
           launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, z, V, ld, j, L, to_gate(gate), to_sync(sync), dots, defer,
@@ -97,7 +101,8 @@ cudaError_t launch_residual_t(int px, int pw, Launch l, const CsrDev& A, const T
         constexpr int PW = decltype(W)::value;
         if constexpr (PW >= PX) {
           auto kern = k_residual<PA, PX, PW, IDX>;
-          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false, tile_threads(IDX));
+          int g = tile_launch_grid<IDX>(g0, T, l.grid);
           if (dist.mode == 2) g = 1;
           launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, x, b, r, L, out_norm, to_sync(sync), to_dist(dist));
           err = cudaGetLastError();
@@ -118,7 +123,8 @@ cudaError_t launch_spmv_t(int px, int py, Launch l, const CsrDev& A, const Tiles
     with_p(px, [&](auto X) {
       with_p(py, [&](auto Y) {
         auto kern = k_spmv<PA, decltype(X)::value, decltype(Y)::value, IDX>;
-        const int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
+        static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false, tile_threads(IDX));
+        const int g = tile_launch_grid<IDX>(g0, T, l.grid);
         launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, x, y);
         err = cudaGetLastError();
       });
@@ -182,7 +188,8 @@ cudaError_t launch_rich_phase_t(int pw, int pv, Launch l, const CsrDev& A, const
         constexpr int PW = decltype(W)::value;
         if constexpr (PW <= PV) {
           auto kern = k_rich_phase<PA, PW, PV, IDX>;
-          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false, tile_threads(IDX));
+          int g = tile_launch_grid<IDX>(g0, T, l.grid);
           if (phase == PH_BOOK) g = 1;
           launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, phase, k, v, v_scale, off, out, n, RS, R, Za, to_gate(gate), level,
                                               cnt, to_sync(sync), to_dist(dist));
@@ -209,7 +216,8 @@ cudaError_t launch_richm_phase_t(int pw, int pv, Launch l, const CsrDev& A, cons
         constexpr int PW = decltype(W)::value;
         if constexpr (PW <= PV) {
           auto kern = k_richm_phase<PA, PW, PV, IDX>;
-          int g = tile_launch_grid<IDX>(kern, SM, T, l.grid);
+          static const int g0 = tile_kernel_grid(kern, SM, T.ntiles, false, tile_threads(IDX));
+          int g = tile_launch_grid<IDX>(g0, T, l.grid);
           if (phase == RM_BOOK) g = 1;
           launch_kt(kern, g, tile_threads(IDX), SM, l.stream, A, T, phase, k, v, v_scale, out, n, RS, R, P, Za, to_gate(gate), level, cnt,
                    to_sync(sync));
