@@ -29,6 +29,9 @@ namespace f3rg {
 #ifndef F3RG_RICH_CHUNK
 #define F3RG_RICH_CHUNK 9
 #endif
+#ifndef F3RG_WSELL_Z1  // windowed engine: materialise z1 before the plain Richardson pass (A/B: 0)
+#define F3RG_WSELL_Z1 1
+#endif
 constexpr int rich_chunk(int idx) { return idx == 2 ? F3RG_RICH_CHUNK : 0; }  // short shape: its own chunk
 
 // Right-hand side of the call: v_i = demote(s * parent_v_i) (s optional). v is in
@@ -58,8 +61,10 @@ struct GatherZ1 {
   using Raw = T_<PV>;
   RhsView<PV, PW> rhs;
   T_<PW> w0;
+  uint64_t pol = 0;  // L2 policy of the windowed engine's ring fills / far gathers (0: plain loads)
   __device__ __forceinline__ void set_policy(uint64_t) {}
-  __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
+  __device__ __forceinline__ void set_ring_policy(uint64_t p) { pol = p; }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return pol ? ldg_hint<PV>(rhs.v, c, pol) : rhs.raw(c); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(Ar<PW>::mul(w0, rhs.apply(r))); }
   // windowed engine: the ring holds z1 itself (wsell.cuh WsRing)
   using RingT = T_<PW>;
@@ -72,8 +77,10 @@ template <int PV, int PW, int C>
 struct GatherRhs {
   using Raw = T_<PV>;
   RhsView<PV, PW> rhs;
+  uint64_t pol = 0;
   __device__ __forceinline__ void set_policy(uint64_t) {}
-  __device__ __forceinline__ Raw load(uint32_t c) const { return rhs.raw(c); }
+  __device__ __forceinline__ void set_ring_policy(uint64_t p) { pol = p; }
+  __device__ __forceinline__ Raw load(uint32_t c) const { return pol ? ldg_hint<PV>(rhs.v, c, pol) : rhs.raw(c); }
   __device__ __forceinline__ T_<C> value(Raw r) const { return cvt<C>(rhs.apply(r)); }
   using RingT = T_<PW>;
   __device__ __forceinline__ RingT ring_put(Raw r) const { return rhs.apply(r); }
@@ -173,12 +180,14 @@ __global__ void __launch_bounds__(tile_threads(IDX), tile_minb(IDX)) k_richardso
       for (uint64_t i = gtid; i < n; i += gstride) st<PW>(out, i, AW::add(AW::mul(w0, rhs.row(i)), AW::zero()));
     } else {
       // step 1 with z1 on the fly, then steps 2..m-1 ping-ponging through scratch.
-      // Gather-bound matrices (config 5, IDX bit 3), m = 2 on one rank: z1 is
-      // materialised at the storage precision first, so the scattered gathers read
-      // 2-byte z1 through L1 instead of the wider v (same z1 bits; the +0 is
-      // immaterial as an SpMV operand, see GatherZ1)
+      // Gather-bound matrices (config 5: the gather-bound tile shape, IDX bit 3, and
+      // the windowed engine, bit 4), m = 2 on one rank: z1 is materialised at the
+      // storage precision first, so the scattered gathers read 2-byte z1 (through L1,
+      // or as the windowed engine's ring element with no per-entry transform left)
+      // instead of the wider v (same z1 bits; the +0 is immaterial as an SpMV
+      // operand, see GatherZ1)
       bool done = false;
-      if constexpr (idx_gather(IDX)) {
+      if constexpr (idx_gather(IDX) || (idx_wsell(IDX) && F3RG_WSELL_Z1)) {
         if (m == 2 && !(flags & 1) && voff == 0) {
           for (uint64_t i = gtid; i < n; i += gstride)
             st<PW>(RS->Za, i, AW::add(AW::mul(w0, rhs.row(i)), AW::zero()));

@@ -39,6 +39,7 @@
 #pragma once
 
 #include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 #include "state.hpp"
@@ -70,6 +71,18 @@ struct WsRing<G, std::void_t<typename G::RingT>> {
   using R = typename G::RingT;
   __device__ __forceinline__ static R put(const G& g, typename G::Raw r) { return g.ring_put(r); }
   __device__ __forceinline__ static auto get(const G& g, R r) { return g.ring_get(r); }
+};
+
+// L2 policy of the engine's vector loads (ring fills, far gathers): the gather's own
+// set_policy, or set_ring_policy where the tile engine's gathers take none
+// (Richardson's GatherZ1 / GatherRhs read the parent's v)
+template <class G, class = void>
+struct WsPolicy {
+  __device__ __forceinline__ static void set(G& g, uint64_t p) { g.set_policy(p); }
+};
+template <class G>
+struct WsPolicy<G, std::void_t<decltype(std::declval<G&>().set_ring_policy(0ull))>> {
+  __device__ __forceinline__ static void set(G& g, uint64_t p) { g.set_ring_policy(p); }
 };
 
 // streamed loads: read once, do not allocate in L1, L2 policy from the caller
@@ -156,7 +169,7 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
   R* ring = reinterpret_cast<R*>(smem);
   T_<C>* ybuf = reinterpret_cast<T_<C>*>(smem + kWsRingBytes);
   unsigned* claim = reinterpret_cast<unsigned*>(smem + kWsRingBytes + kWsYBytes);
-  g.set_policy(l2_policy(T.l2hint ? 2 : 0));             // far gathers: keep x in L2
+  WsPolicy<G>::set(g, l2_policy(T.l2hint ? 2 : 0));       // ring fills and far gathers: keep x in L2
   const uint64_t spol = l2_policy(T.l2hint ? 1 : 0);     // the matrix stream
   const int64_t n = (int64_t)A.n;
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
