@@ -300,8 +300,12 @@ void DeviceMatrix::build_wsell(const uint32_t* rp) {
   up(ws_cwin_, cwin);
   DevBuf dsrc;
   up(dsrc, src);
-  ws_col_.alloc(ws_E_ * 4 + 64);
-  F3RG_CUDA(launch_ws_scatter(Launch{}, 4, dsrc.get<uint32_t>(), ci_.get(), ws_col_.get(), ws_E_, true));
+  for (int c = 0; c < 3; ++c) {  // the column stream, encoded per ring class (wsell.cuh)
+    ws_enc_[c].alloc(ws_E_ * 4 + 64);
+    F3RG_CUDA(cudaMemset(ws_enc_[c].get(), 0, ws_E_ * 4 + 64));
+    F3RG_CUDA(launch_ws_encode(Launch{}, dsrc.get<uint32_t>(), ci_.get<uint32_t>(), ws_soff_.get<uint32_t>(),
+                               ws_cwin_.get<uint32_t>(), ws_G_, nsl, n_, c, ws_enc_[c].get<uint32_t>()));
+  }
   for (int p = 0; p < 3; ++p) {
     ws_val_[p].alloc(ws_E_ * psize(p) + 64);
     F3RG_CUDA(launch_ws_scatter(Launch{}, (int)psize(p), dsrc.get<uint32_t>(), val_[p].get(), ws_val_[p].get(),
@@ -357,7 +361,7 @@ TilesDev DeviceMatrix::tiles(int p) const {
   if (ws_E_) {
     t.ws_soff = ws_soff_.get<const uint32_t>();
     t.ws_row = ws_row_.get<const uint32_t>();
-    t.ws_col = ws_col_.get<const uint32_t>();
+    for (int c = 0; c < 3; ++c) t.ws_enc[c] = ws_enc_[c].get<const uint32_t>();
     t.ws_val = ws_val_[p].get();
     t.ws_cwin = ws_cwin_.get<const uint32_t>();
     t.ws_G = ws_G_;

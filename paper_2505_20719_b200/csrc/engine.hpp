@@ -150,7 +150,7 @@ class DeviceMatrix {
   uint64_t n_ = 0, nnz_ = 0;
   DevBuf rp_, ci_, val_[3], tr0_[3], tk0_[3], dcol_, first_, pk_;
   DevBuf perm_, srp_, sci_, sval_[3], sdcol_, sfirst_, spk_;  // row-sorted copy (irregular rows)
-  DevBuf ws_soff_, ws_row_, ws_col_, ws_val_[3], ws_cwin_;  // windowed SELL layout (shape 3)
+  DevBuf ws_soff_, ws_row_, ws_enc_[3], ws_val_[3], ws_cwin_;  // windowed SELL layout (shape 3)
   uint64_t ws_E_ = 0;
   uint32_t ws_G_ = 0;
   void build_wsell(const uint32_t* row_ptr);

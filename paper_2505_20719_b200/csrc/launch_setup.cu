@@ -106,4 +106,49 @@ cudaError_t launch_ws_scatter(Launch l, int esize, const uint32_t* src, const vo
   return cudaGetLastError();
 }
 
+// Encoded column stream of the windowed engine for one ring class (wsell.cuh): one
+// warp per 32-row slice. The slice's kernel window follows from its sort window and
+// the CTA that owns it (cwin: G + 1 sort-window boundaries): the CTA's windows start
+// at its first sort window and hold KW sort windows each. An entry whose column lies
+// in the window's band [B - W, B + TW + W) (clipped to [0, n)) becomes the byte
+// offset of its ring slot, (column mod RN) * RS; padding becomes zoff; any other
+// entry keeps its column with kWsFarBit set.
+__global__ void __launch_bounds__(256) k_ws_encode(const uint32_t* __restrict__ src, const uint32_t* __restrict__ ci,
+                                                   const uint32_t* __restrict__ soff, const uint32_t* __restrict__ cwin,
+                                                   uint32_t G, uint64_t nsl, uint64_t n, int cl, uint32_t zoff,
+                                                   uint32_t* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t RN = ws_rn(cl), TW = ws_tw(cl), W = ws_w(cl);
+  const uint32_t KW = (uint32_t)(TW / (int64_t)kWsSortRows), RS = 2u << cl;
+  for (uint64_t s = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); s < nsl; s += nwarps) {
+    const uint32_t sw = (uint32_t)(s / (kWsSortRows / 32));
+    uint32_t lo_g = 0, hi_g = G;  // the CTA g with cwin[g] <= sw < cwin[g + 1]
+    while (hi_g - lo_g > 1) {
+      const uint32_t mid = (lo_g + hi_g) >> 1;
+      if (cwin[mid] <= sw) lo_g = mid;
+      else hi_g = mid;
+    }
+    const uint32_t sw0 = cwin[lo_g];
+    const int64_t B = (int64_t)(sw0 + (sw - sw0) / KW * KW) * (int64_t)kWsSortRows;
+    const int64_t lo = B - W < 0 ? 0 : B - W, hi = B + TW + W > (int64_t)n ? (int64_t)n : B + TW + W;
+    for (uint32_t e = soff[s] + lane; e < soff[s + 1]; e += 32u) {
+      const uint32_t k = src[e];
+      uint32_t v = zoff;
+      if (k != kWsPadIdx) {
+        const uint32_t c = ci[k];
+        v = ((int64_t)c >= lo && (int64_t)c < hi) ? (uint32_t)((int64_t)c & (RN - 1)) * RS : (kWsFarBit | c);
+      }
+      out[e] = v;
+    }
+  }
+}
+
+cudaError_t launch_ws_encode(Launch l, const uint32_t* src, const uint32_t* ci, const uint32_t* soff,
+                             const uint32_t* cwin, uint32_t G, uint64_t nsl, uint64_t n, int cl, uint32_t* out) {
+  const int g = l.grid ? l.grid : stream_grid();
+  k_ws_encode<<<g, kThreads, 0, l.stream>>>(src, ci, soff, cwin, G, nsl, n, cl, kWsZeroOffset, out);
+  return cudaGetLastError();
+}
+
 }  // namespace f3rg

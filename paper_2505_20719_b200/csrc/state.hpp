@@ -28,6 +28,17 @@ struct CsrDev {
 // windowed SELL layout constants (wsell.cuh; built by engine.cpp build_wsell)
 constexpr uint32_t kWsSortRows = 2048;      // rows per sort window
 constexpr uint32_t kWsPadIdx = 0xffffffffu;  // padding slot / padding lane
+// Ring class cl = 0 / 1 / 2: gathers whose ring element has 2 / 4 / 8 bytes. The ring
+// is 128 KB: RN elements; a kernel window has TW rows; the band half-width is
+// W = (RN - 2 TW) / 2 (the ring holds x[B - W, B + 2 TW + W) while the window at row
+// B runs).
+constexpr int ws_rn(int cl) { return 65536 >> cl; }
+constexpr int ws_tw(int cl) { return 8192 >> cl; }
+constexpr int ws_w(int cl) { return (ws_rn(cl) - 2 * ws_tw(cl)) / 2; }  // 24576, 12288, 6144 rows
+// encoded column stream (per ring class): byte offset of the ring slot (in band),
+// kWsZeroOffset (padding), or kWsFarBit | column (anything else)
+constexpr uint32_t kWsZeroOffset = 128u * 1024u + 64u * 1024u + 32u;
+constexpr uint32_t kWsFarBit = 0x80000000u;
 
 struct TilesDev {
   const uint32_t* r0 = nullptr;  // ntiles+1 row starts
@@ -47,11 +58,11 @@ struct TilesDev {
   // CsrDev handed with these tiles stores the rows in that order. Null = identity
   const uint32_t* perm = nullptr;
   // windowed SELL layout (shape 3, wsell.cuh): slice entry offsets (slices+1), slice
-  // lane -> matrix row (slices*32), chunk-major columns and values at this replica's
-  // precision, and the split of the sort windows over ws_G CTAs (ws_G+1)
+  // lane -> matrix row (slices*32), chunk-major encoded columns (per ring class) and
+  // values at this replica's precision, and the split of the sort windows over ws_G CTAs (ws_G+1)
   const uint32_t* ws_soff = nullptr;
   const uint32_t* ws_row = nullptr;
-  const uint32_t* ws_col = nullptr;
+  const uint32_t* ws_enc[3] = {nullptr, nullptr, nullptr};  // encoded columns per ring class
   const void* ws_val = nullptr;
   const uint32_t* ws_cwin = nullptr;
   uint32_t ws_G = 0;

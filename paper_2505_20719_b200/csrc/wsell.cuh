@@ -53,6 +53,8 @@ constexpr int kWsRingBytes = 128 * 1024;    // the x band
 constexpr int kWsYBytes = 64 * 1024;        // two row-sum buffers
 constexpr int kWsSmem = kWsRingBytes + kWsYBytes + 64;
 constexpr uint32_t kWsPad = kWsPadIdx;
+constexpr uint32_t kWsZeroOff = kWsZeroOffset;  // byte offset of the zero slot (after the claim counters)
+static_assert(kWsZeroOffset == kWsRingBytes + kWsYBytes + 32, "zero slot offset (state.hpp)");
 #ifndef F3RG_WS_U  // column/value quads per lane per pipeline step
 #define F3RG_WS_U 2
 #endif
@@ -155,16 +157,24 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
   constexpr int RS = (int)sizeof(R);
   constexpr int RN = kWsRingBytes / RS;  // ring elements (power of two)
   constexpr int CS = (int)sizeof(T_<C>);
-  // rows per kernel window: as many as the ring keeps a wide band for, and the two
-  // row-sum buffers fit
-  constexpr int TW = (16384 / RS < 32768 / CS) ? 16384 / RS : 32768 / CS;
+  constexpr int CL = RS == 2 ? 0 : RS == 4 ? 1 : 2;  // ring class (state.hpp): fixes the window geometry
+  static_assert(RN == ws_rn(CL), "ring size");
+  constexpr int TW = ws_tw(CL);     // rows per kernel window
   constexpr int KW = TW / kWsSort;  // sort windows per kernel window
-  constexpr int W = (RN - 2 * TW) / 2;
+  constexpr int W = ws_w(CL);
   constexpr int PF = TW / kWsThreads;  // ring elements each thread carries one window ahead
-  constexpr uint32_t SPAN = (uint32_t)(TW + 2 * W);
   constexpr int U = PA == P64 ? 1 : F3RG_WS_U;
+  // two row-sum buffers (the next window's sums land while this one's epilogue runs),
+  // or one and a second barrier per window when the accumulator is too wide for two
+  constexpr bool YDBL = 2 * TW * CS <= kWsYBytes;
   static_assert(TW % kWsSort == 0 && W > 0 && PF >= 1 && (RN & (RN - 1)) == 0, "window geometry");
-  static_assert(2 * TW * CS <= kWsYBytes, "row-sum buffers");
+  static_assert(TW * CS <= kWsYBytes, "row-sum buffer");
+  // the column stream of this ring class, encoded on the host side of the layout
+  // (launch_setup.cu k_ws_encode): an entry inside its window's band is the byte
+  // offset of its ring slot, a padding entry the offset of a slot that holds zero
+  // (its value is +0 too; a row accumulator is never -0, so the +-0 product leaves
+  // it unchanged), any other ("far") entry its column with bit 31 set
+  const uint32_t* __restrict__ enc = T.ws_enc[CL];
 
   R* ring = reinterpret_cast<R*>(smem);
   T_<C>* ybuf = reinterpret_cast<T_<C>*>(smem + kWsRingBytes);
@@ -179,6 +189,7 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
 
   __syncthreads();  // a previous pass in the same kernel is done with the ring
   if (tid < 2) claim[tid] = 0u;
+  if (tid < 2) reinterpret_cast<uint32_t*>(smem + kWsZeroOff)[tid] = 0u;  // the zero slot
   if (sw0 < sw1) {  // ring for the first window: x[B0-W, B0+2TW+W)
     const int64_t B0 = (int64_t)sw0 * kWsSort;
     int64_t i0 = B0 - W;
@@ -201,8 +212,7 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
       const int64_t i = pb + (int64_t)q * kWsThreads + tid;
       if (i < n) pf[q] = g.load((uint32_t)i);
     }
-    const uint32_t lo = (uint32_t)(int32_t)(B - W);  // band [B-W, B+TW+W), wraps below 0
-    T_<C>* yb = ybuf + (it & 1u) * TW;
+    T_<C>* yb = ybuf + (YDBL ? (it & 1u) * TW : 0u);
     const uint32_t nsl = kw * (uint32_t)kWsSlices;
     unsigned* cl = &claim[it & 1u];
     for (;;) {
@@ -222,10 +232,10 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if ((uint32_t)u < nq) {
-          cc[u] = ws_ld16(reinterpret_cast<const uint4*>(T.ws_col) + qb + (uint64_t)u * 32, spol);
+          cc[u] = ws_ld16(reinterpret_cast<const uint4*>(enc) + qb + (uint64_t)u * 32, spol);
           vc[u].load(T.ws_val, qb + (uint64_t)u * 32, spol);
         } else {
-          cc[u] = make_uint4(kWsPad, kWsPad, kWsPad, kWsPad);
+          cc[u] = make_uint4(kWsZeroOff, kWsZeroOff, kWsZeroOff, kWsZeroOff);
           vc[u].zero();
         }
       }
@@ -234,10 +244,10 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
         for (int u = 0; u < U; ++u) {  // next step's stream, in flight during this one
           const uint32_t q = q0 + U + u;
           if (q < nq) {
-            cn[u] = ws_ld16(reinterpret_cast<const uint4*>(T.ws_col) + qb + (uint64_t)q * 32, spol);
+            cn[u] = ws_ld16(reinterpret_cast<const uint4*>(enc) + qb + (uint64_t)q * 32, spol);
             vn[u].load(T.ws_val, qb + (uint64_t)q * 32, spol);
           } else {
-            cn[u] = make_uint4(kWsPad, kWsPad, kWsPad, kWsPad);
+            cn[u] = make_uint4(kWsZeroOff, kWsZeroOff, kWsZeroOff, kWsZeroOff);
             vn[u].zero();
           }
         }
@@ -248,20 +258,17 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t c = quad_at(cc[u], k);
-            const bool in = c - lo < SPAN;
-            xr[4 * u + k] = in ? ring[c & (uint32_t)(RN - 1)] : R{};
-            xf[4 * u + k] = (!in && c != kWsPad) ? g.load(c) : Raw{};
+            const bool in = (int32_t)c >= 0;
+            xr[4 * u + k] = in ? *reinterpret_cast<const R*>(smem + c) : R{};
+            xf[4 * u + k] = !in ? g.load(c & 0x7fffffffu) : Raw{};
           }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint32_t c = quad_at(cc[u], k);
-            if (c != kWsPad) {
-              const bool in = c - lo < SPAN;
-              const T_<C> xv = in ? RT::get(g, xr[4 * u + k]) : RT::get(g, RT::put(g, xf[4 * u + k]));
-              acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vc[u].at(k)), xv));
-            }
+            const bool in = (int32_t)quad_at(cc[u], k) >= 0;
+            const T_<C> xv = in ? RT::get(g, xr[4 * u + k]) : RT::get(g, RT::put(g, xf[4 * u + k]));
+            acc = Ar<C>::add(acc, Ar<C>::mul(cvt<C>(vc[u].at(k)), xv));
           }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -284,6 +291,7 @@ __device__ __forceinline__ void wsell_pass(const CsrDev& A, const TilesDev& T, G
       e.prefetch((uint32_t)i);
       e.row((uint32_t)i, yb[(uint32_t)(i - B)]);
     }
+    if constexpr (!YDBL) __syncthreads();  // the one row-sum buffer is free again
   }
   pdl_trigger();
 }
