@@ -17,8 +17,10 @@
 #include <cstddef>
 #include <cstdlib>
 #include <cstring>
+#include <stdexcept>
 
 #include "launch.hpp"
+#include "wsell_pk_layout.hpp"
 
 namespace f3rg {
 
@@ -180,8 +182,9 @@ void DeviceMatrix::init(const uint32_t* row_ptr, const uint32_t* col_idx, const 
     const char* wse = std::getenv("F3RG_WSELL");
     const bool square = ncols == 0 || ncols == n_;
     const bool want = wse && *wse ? wse[0] != '0' : (sort_rows && !forced_shape);
-    if (want && square && n_ > 0 && nnz_ > 0 && n_ < (1ull << 31)) {
+    if (want && square && n_ > 0 && nnz_ > 0 && n_ < (1ull << 30)) {
       build_wsell(row_ptr);
+      build_wsell_pk(row_ptr, col_idx);
       shape_ = 3;
       sort_rows = false;
     }
@@ -314,8 +317,41 @@ void DeviceMatrix::build_wsell(const uint32_t* rp) {
   F3RG_CUDA(cudaDeviceSynchronize());
 }
 
+// Packed windowed layout (wsell_pk.cuh): built on the host (wsell_pk_layout.hpp), the fp16
+// values packed in on the device from the fp16 replica, bit for bit.
+void DeviceMatrix::build_wsell_pk(const uint32_t* rp, const uint32_t* ci) {
+  PkLayoutHost L;
+  try {
+    pk_build_layout(n_, rp, ci, (uint32_t)sm_count(), L);
+  } catch (const std::length_error& e) {
+    throw Error(ERR_UNSUPPORTED, e.what());
+  }
+  pk_E_ = L.E;
+  pk_far_ = L.far;
+  auto up = [&](DevBuf& b, const void* v, size_t bytes) {
+    b.alloc(bytes + 64);
+    F3RG_CUDA(cudaMemset(b.get(), 0, bytes + 64));
+    if (bytes) F3RG_CUDA(cudaMemcpy(b.get(), v, bytes, cudaMemcpyHostToDevice));
+  };
+  up(pk_soff_, L.soff.data(), L.soff.size() * 4);
+  up(pk_row_, L.row.data(), L.row.size() * 4);
+  up(pk_cwin_, L.cwin.data(), L.cwin.size() * 4);
+  DevBuf dsrc, dcode;
+  up(dsrc, L.src.data(), L.src.size() * 4);
+  up(dcode, L.code.data(), L.code.size() * 2);
+  pk_words_.alloc(pk_E_ * 4 + 256);
+  F3RG_CUDA(cudaMemset(pk_words_.get(), 0, pk_E_ * 4 + 256));
+  F3RG_CUDA(launch_pk_pack(Launch{}, dsrc.get<uint32_t>(), dcode.get<uint16_t>(), val_[0].get(),
+                           pk_words_.get<uint32_t>(), pk_E_));
+  F3RG_CUDA(cudaDeviceSynchronize());
+}
+
 double DeviceMatrix::stream_bytes(int pa) const {
   const double n = (double)n_, nnz = (double)nnz_;
+  if (pk_E_ && pa == 0) {  // fp16 replica on the packed windowed layout: one 4-byte word per slot + slice tables
+    const double nsl = (double)((n_ + kWsSortRows - 1) / kWsSortRows) * (kWsSortRows / 32);
+    return (double)pk_E_ * 4.0 + nsl * 32.0 * 4.0 + (nsl + 1.0) * 4.0;
+  }
   if (ws_E_) {  // windowed SELL: chunk-major columns + values (padding included), slice rows and offsets
     const double E = (double)ws_E_, nsl = (double)((n_ + kWsSortRows - 1) / kWsSortRows) * (kWsSortRows / 32);
     return E * (psize(pa) + 4.0) + nsl * 32.0 * 4.0 + (nsl + 1.0) * 4.0;
@@ -365,6 +401,12 @@ TilesDev DeviceMatrix::tiles(int p) const {
     t.ws_val = ws_val_[p].get();
     t.ws_cwin = ws_cwin_.get<const uint32_t>();
     t.ws_G = ws_G_;
+    if (pk_E_ && p == 0) {
+      t.pk_soff = pk_soff_.get<const uint32_t>();
+      t.pk_row = pk_row_.get<const uint32_t>();
+      t.pk_words = pk_words_.get<const uint32_t>();
+      t.pk_cwin = pk_cwin_.get<const uint32_t>();
+    }
   }
   return t;
 }

@@ -142,7 +142,8 @@ class DeviceMatrix {
   // bytes one pass over replica pa streams: values, the column stream in use, row_ptr
   double stream_bytes(int pa) const;
   int shape() const { return shape_; }  // 0 regular, 1 short rows, 2 gather-bound, 3 windowed SELL
-  uint64_t ws_entries() const { return ws_E_; }  // stored entries of the windowed layout (0: none)
+  uint64_t ws_entries() const { return ws_E_; }
+  uint64_t pk_slots() const { return pk_E_; }  // slots of the packed layout (0: none)  // stored entries of the windowed layout (0: none)
 
  private:
   void init(const uint32_t* row_ptr, const uint32_t* col_idx, const double* values, uint64_t ncols,
@@ -154,6 +155,10 @@ class DeviceMatrix {
   uint64_t ws_E_ = 0;
   uint32_t ws_G_ = 0;
   void build_wsell(const uint32_t* row_ptr);
+  // packed layout of the fp16 replica for the 2-byte-ring passes (wsell_pk_layout.hpp)
+  DevBuf pk_soff_, pk_row_, pk_words_, pk_cwin_;
+  uint64_t pk_E_ = 0, pk_far_ = 0;
+  void build_wsell_pk(const uint32_t* row_ptr, const uint32_t* col_idx);
   uint32_t ntiles_[3] = {0, 0, 0};
   uint32_t l2hint_ = 0;  // L2 eviction priorities for the passes (init)
   int shape_ = 0;

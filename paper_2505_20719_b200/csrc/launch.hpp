@@ -153,6 +153,9 @@ cudaError_t launch_ws_scatter(Launch l, int esize, const uint32_t* src, const vo
 // windowed SELL layout: the encoded column stream of ring class cl (launch_setup.cu k_ws_encode)
 cudaError_t launch_ws_encode(Launch l, const uint32_t* src, const uint32_t* ci, const uint32_t* soff,
                              const uint32_t* cwin, uint32_t G, uint64_t nsl, uint64_t n, int cl, uint32_t* out);
+// packed windowed layout: out[e] = code[e] | fp16 bits of val16[src[e]] << 16 (+0 where src[e] == 0xffffffff)
+cudaError_t launch_pk_pack(Launch l, const uint32_t* src, const uint16_t* code, const void* val16, uint32_t* out,
+                           uint64_t cnt);
 cudaError_t launch_pack16(Launch l, const void* val16, const uint16_t* dcol, uint32_t* out, uint64_t nnz);
 // dst[i] = src[idx[i]], i < cnt, at precision p (halo pack / gather)
 cudaError_t launch_gather(int p, Launch l, const void* src, const uint32_t* idx, uint64_t cnt, void* dst);

@@ -151,4 +151,23 @@ cudaError_t launch_ws_encode(Launch l, const uint32_t* src, const uint32_t* ci, 
   return cudaGetLastError();
 }
 
+// Packed windowed layout (wsell_pk_layout.hpp): word = slot code | fp16 value bits << 16; a slot
+// without an entry of its own (padding, the escape half of a far pair) carries +0
+__global__ void __launch_bounds__(256) k_pk_pack(const uint32_t* __restrict__ src, const uint16_t* __restrict__ code,
+                                                 const uint16_t* __restrict__ val16, uint32_t* __restrict__ out,
+                                                 uint64_t cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += stride) {
+    const uint32_t k = src[e];
+    out[e] = (uint32_t)code[e] | (k == kWsPadIdx ? 0u : (uint32_t)val16[k] << 16);
+  }
+}
+
+cudaError_t launch_pk_pack(Launch l, const uint32_t* src, const uint16_t* code, const void* val16, uint32_t* out,
+                           uint64_t cnt) {
+  const int g = l.grid ? l.grid : stream_grid();
+  k_pk_pack<<<g, kThreads, 0, l.stream>>>(src, code, static_cast<const uint16_t*>(val16), out, cnt);
+  return cudaGetLastError();
+}
+
 }  // namespace f3rg

@@ -32,6 +32,7 @@
 #include "common.cuh"
 #include "state.hpp"
 #include "wsell.cuh"
+#include "wsell_pk.cuh"
 
 #ifndef F3RG_TILE_MINB  // tile kernels: min CTAs per SM (register budget)
 #define F3RG_TILE_MINB 3
@@ -316,8 +317,13 @@ __device__ __forceinline__ void spmv_row_tiles(const CsrDev& A, const TilesDev& 
 // engine (IDX bit 4, gather-bound matrices) -- same per-row sums either way.
 template <int PA, int C, int IDX_, int CH = 0, class Gather, class Epi>
 __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
-  if constexpr (idx_wsell(IDX_)) wsell_pass<PA, C>(A, T, g, e, smem);
-  else spmv_row_tiles<PA, C, IDX_, CH>(A, T, g, e, smem);
+  if constexpr (idx_wsell(IDX_)) {
+    // fp16 matrix and a 2-byte ring (Richardson on z1, the L3 spmv_dots, the fp16 SpMV): the packed stream
+    if constexpr (PA == P16 && sizeof(typename WsRing<Gather>::R) == 2) wsell_pass_pk<C>(A, T, g, e, smem);
+    else wsell_pass<PA, C>(A, T, g, e, smem);
+  } else {
+    spmv_row_tiles<PA, C, IDX_, CH>(A, T, g, e, smem);
+  }
 }
 
 // ---- gathers ----------------------------------------------------------------------

@@ -40,6 +40,14 @@ constexpr int ws_w(int cl) { return (ws_rn(cl) - 2 * ws_tw(cl)) / 2; }  // 24576
 constexpr uint32_t kWsZeroOffset = 128u * 1024u + 64u * 1024u + 32u;
 constexpr uint32_t kWsFarBit = 0x80000000u;
 
+// Packed windowed layout (wsell_pk.cuh / wsell_pk_layout.hpp): fp16 matrix, 2-byte ring.
+// Window geometry on a global grid of kPkTW rows; ring of kPkRing slots (slot = row mod
+// kPkRing, the last one reserved: it holds zero), band half-width kPkW = (kPkRing - 2 kPkTW) / 2.
+// A slot's 16-bit code: < kPkLimit a ring slot, kPkPad the zero slot, >= kPkEsc the
+// high part of a far column (the low 16 bits are the next slot's code).
+constexpr int kPkTW = 8192, kPkRing = 49152, kPkW = (kPkRing - 2 * kPkTW) / 2;
+constexpr uint32_t kPkLimit = kPkRing - 1, kPkPad = kPkRing - 1, kPkEsc = kPkRing;
+
 struct TilesDev {
   const uint32_t* r0 = nullptr;  // ntiles+1 row starts
   const uint32_t* k0 = nullptr;  // ntiles+1 nnz starts (= rp[r0])
@@ -66,6 +74,12 @@ struct TilesDev {
   const void* ws_val = nullptr;
   const uint32_t* ws_cwin = nullptr;
   uint32_t ws_G = 0;
+  // packed layout of the fp16 replica for 2-byte rings (null: none): slice slot offsets,
+  // slice lane -> row, the packed words (code | fp16 value << 16), the CTA split
+  const uint32_t* pk_soff = nullptr;
+  const uint32_t* pk_row = nullptr;
+  const uint32_t* pk_words = nullptr;
+  const uint32_t* pk_cwin = nullptr;
 };
 
 // Device-resident state of one FGMRES level. H is column-major: column j holds

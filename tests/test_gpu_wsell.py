@@ -21,7 +21,7 @@ TRIPLES = [(pa, px, py) for pa in (0, 1, 2) for px in (0, 1, 2) for py in (0, 1,
 SOME = [(0, 0, 0), (0, 1, 1), (0, 0, 1), (1, 1, 1), (2, 1, 2), (2, 2, 2), (0, 2, 0)]
 # band half-widths W of the three ring widths (wsell.cuh: RN = 128 KB / element size,
 # TW rows per window, W = (RN - 2 TW) / 2) for 2-, 4- and 8-byte ring elements
-BANDS = (24576, 12288, 6144)
+BANDS = (24576, 12288, 6144, 16384)  # + the packed fp16 stream's band (wsell_pk.cuh: 49,152-slot ring, 8192-row windows)
 
 
 def _reps(f, n, rp, ci, va, monkeypatch, on="1"):
