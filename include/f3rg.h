@@ -103,6 +103,13 @@ uint64_t f3rg_matrix_stream_bytes(const f3rg_matrix* a, int prec);
  * rows), 2 row tiles over the row-sorted copy (gather-bound), 3 windowed SELL
  * (gather-bound, square, one rank); F3RG_SHAPE / F3RG_SORT_ROWS / F3RG_WSELL force */
 int f3rg_matrix_engine(const f3rg_matrix* a);
+/* Host-side self-check of the packed windowed SELL layout (csrc/wsell_pk_layout.hpp) the fp16
+ * passes of engine 3 stream: builds the layout of the CSR pattern for `ctas` CTAs (no GPU needed)
+ * and decodes every row back -- slot codes, escape pairs of far columns, padding -- against the
+ * CSR row, in order. stats (4 values, may be null): slots, far entries, slices, padding slots.
+ * Returns 0, or F3RG_EDIMENSION with the first mismatch in f3rg_last_error(). */
+int f3rg_wsell_pk_selfcheck(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, uint32_t ctas,
+                            uint64_t* stats);
 /* replica values widened to fp64 into host memory (nnz doubles) */
 int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host);
 

@@ -111,6 +111,8 @@ def lib():
     L.f3rg_matrix_values.argtypes = [vp, i32, vp]
     L.f3rg_matrix_engine.argtypes = [vp]
     L.f3rg_matrix_engine.restype = i32
+    L.f3rg_wsell_pk_selfcheck.argtypes = [u64, vp, vp, C.c_uint32, vp]
+    L.f3rg_wsell_pk_selfcheck.restype = i32
     L.f3rg_spec_canonical.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
     L.f3rg_solver_create.argtypes = [C.POINTER(vp), vp, C.c_char_p, i32]
     L.f3rg_solver_destroy.argtypes = [vp]
@@ -450,6 +452,17 @@ def diagonal_scale(a: SparseCsr, b) -> ScaledSystem:
     vals = np.zeros(a.nnz())
     _check(lib().f3rg_matrix_values(h, 2, vals.ctypes.data))
     return ScaledSystem(PrecisionReplicas(SparseCsr(a.n, a.row_ptr, a.col_idx, vals), _dev=dev), bs, d)
+
+
+def wsell_pk_selfcheck(n: int, row_ptr, col_idx, ctas: int = 148) -> dict:
+    """Builds the packed windowed SELL layout (csrc/wsell_pk_layout.hpp) of a CSR pattern on
+    the host and decodes every row back against the CSR (no GPU needed); raises
+    DimensionError on the first mismatch. Returns the layout's slot / far / slice / padding counts."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.uint32)
+    ci = np.ascontiguousarray(col_idx, dtype=np.uint32)
+    stats = np.zeros(4, dtype=np.uint64)
+    _check(lib().f3rg_wsell_pk_selfcheck(int(n), rp.ctypes.data, ci.ctypes.data, int(ctas), stats.ctypes.data))
+    return {"slots": int(stats[0]), "far": int(stats[1]), "slices": int(stats[2]), "padding": int(stats[3])}
 
 
 def read_matrix_market(path: str) -> SparseCsr:

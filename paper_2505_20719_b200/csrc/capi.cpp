@@ -10,6 +10,7 @@
 
 #include "../../include/f3rg.h"
 #include "engine.hpp"
+#include "wsell_pk_layout.hpp"
 #include "launch.hpp"
 
 using namespace f3rg;
@@ -140,6 +141,70 @@ uint64_t f3rg_matrix_stream_bytes(const f3rg_matrix* a, int prec) {
 }
 
 int f3rg_matrix_engine(const f3rg_matrix* a) { return a ? a->m->shape() : -1; }
+
+int f3rg_wsell_pk_selfcheck(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, uint32_t ctas,
+                            uint64_t* stats) {
+  return guarded([&] {
+    PkLayoutHost L;
+    try {
+      pk_build_layout(n, row_ptr, col_idx, ctas, L);
+    } catch (const std::length_error& e) {
+      throw Error(ERR_UNSUPPORTED, e.what());
+    }
+    const uint64_t nsl = L.soff.size() - 1;
+    uint64_t pads = 0, far = 0, rows_seen = 0;
+    auto fail = [&](uint64_t r, const char* what) {
+      throw Error(ERR_DIMENSION, "packed layout: row " + std::to_string(r) + ": " + what);
+    };
+    if (L.cwin.size() != (size_t)ctas + 1 || L.cwin.front() != 0 ||
+        (uint64_t)L.cwin.back() * kWsSortRows < n)
+      fail(0, "CTA split does not cover the rows");
+    for (uint64_t s = 0; s < nsl; ++s) {
+      const uint32_t width = (L.soff[s + 1] - L.soff[s]) / 32u;
+      if ((L.soff[s] & 127u) || (width & 3u)) fail(0, "slice offset / width not chunk aligned");
+      for (uint32_t l = 0; l < 32; ++l) {
+        const uint32_t r = L.row[s * 32 + l];
+        auto at = [&](uint32_t pos) { return (uint64_t)L.soff[s] + (uint64_t)(pos >> 2) * 128u + l * 4u + (pos & 3u); };
+        if (r == kWsPadIdx) {
+          for (uint32_t pos = 0; pos < width; ++pos)
+            if (L.code[at(pos)] != kPkPad || L.src[at(pos)] != kWsPadIdx) fail(s, "a lane without a row holds an entry");
+          continue;
+        }
+        if (r / kWsSortRows != s / (kWsSortRows / 32)) fail(r, "row outside its sort window");
+        ++rows_seen;
+        const int64_t B = (int64_t)(r / (uint64_t)kPkTW) * kPkTW;
+        const int64_t lo = std::max<int64_t>(0, B - kPkW), hi = std::min<int64_t>((int64_t)n, B + kPkTW + kPkW);
+        uint32_t k = row_ptr[r], pos = 0;
+        while (pos < width) {
+          const uint32_t code = L.code[at(pos)], src = L.src[at(pos)];
+          if (code >= kPkEsc) {  // escape pair: this slot carries no value, the next one the low half and the entry
+            if ((pos & 3u) == 3u) fail(r, "escape pair split over two quads");
+            if (src != kWsPadIdx) fail(r, "escape slot carries a value");
+            if (k >= row_ptr[r + 1]) fail(r, "more entries than the CSR row");
+            const uint32_t c = ((code - kPkEsc) << 16) | L.code[at(pos + 1)];
+            if (c != col_idx[k] || L.src[at(pos + 1)] != k) fail(r, "far column / entry mismatch");
+            const bool inband = (int64_t)c >= lo && (int64_t)c < hi && c % (uint32_t)kPkRing < kPkLimit;
+            if (inband) fail(r, "band entry stored as far");
+            ++far, ++k, pos += 2;
+          } else if (src == kWsPadIdx) {
+            if (code != kPkPad) fail(r, "padding slot with a ring code");
+            ++pads, ++pos;
+          } else {
+            if (k >= row_ptr[r + 1] || src != k) fail(r, "entry out of order");
+            const uint32_t c = col_idx[k];
+            if (code != c % (uint32_t)kPkRing || code >= kPkLimit || (int64_t)c < lo || (int64_t)c >= hi)
+              fail(r, "ring slot does not match the column / band");
+            ++k, ++pos;
+          }
+        }
+        if (k != row_ptr[r + 1]) fail(r, "row not fully stored");
+      }
+    }
+    if (rows_seen != n) fail(0, "not every row is stored exactly once");
+    if (far != L.far) fail(0, "far count mismatch");
+    if (stats) stats[0] = L.E, stats[1] = far, stats[2] = nsl, stats[3] = pads;
+  });
+}
 
 int f3rg_matrix_values(const f3rg_matrix* a, int prec, double* out_host) {
   return guarded([&] {

@@ -52,7 +52,7 @@ inline void pk_build_layout(uint64_t n, const uint32_t* rp, const uint32_t* ci, 
   const uint64_t nwin = (n + SW - 1) / SW, nsl = nwin * NS;
   L.G = G;
   // walks row r's entries and calls slot(pos, code, src) for every slot it takes; returns the slot count
-  auto walk = [&](uint32_t r, auto&& slot) {
+  auto walk = [&](uint32_t r, auto&& slot, uint32_t* nfar = nullptr) {
     const int64_t B = (int64_t)(r / (uint64_t)TW) * TW;
     const int64_t lo = std::max<int64_t>(0, B - W), hi = std::min<int64_t>((int64_t)n, B + TW + W);
     uint32_t pos = 0;
@@ -65,6 +65,7 @@ inline void pk_build_layout(uint64_t n, const uint32_t* rp, const uint32_t* ci, 
         if ((pos & 3u) == 3u) slot(pos++, (uint16_t)kPkPad, kWsPadIdx);  // keep the pair inside one quad
         slot(pos++, (uint16_t)(kPkEsc + (c >> 16)), kWsPadIdx);
         slot(pos++, (uint16_t)(c & 0xffffu), k);
+        if (nfar) ++*nfar;
       }
     }
     return pos;
@@ -74,7 +75,7 @@ inline void pk_build_layout(uint64_t n, const uint32_t* rp, const uint32_t* ci, 
 #pragma omp parallel for schedule(dynamic, 4096) reduction(+ : far)
   for (int64_t r = 0; r < (int64_t)n; ++r) {
     uint32_t esc = 0;
-    xlen[r] = walk((uint32_t)r, [&](uint32_t, uint16_t code, uint32_t) { esc += code >= kPkEsc ? 1u : 0u; });
+    xlen[r] = walk((uint32_t)r, [](uint32_t, uint16_t, uint32_t) {}, &esc);
     far += esc;
   }
   L.far = far;
