@@ -10,7 +10,10 @@
 // 1024 threads) owns a contiguous run of rows and keeps the band of x those rows
 // can touch in a 128 KB ring, slid forward window by window with plain loads issued
 // one window ahead. Gathers inside the band are shared-memory loads; the rest (the
-// long-range 5 %) go to L2 with an evict-last policy.
+// long-range 5 %) go to L2 with an evict-last policy. Which of the two an entry is
+// gets decided once, when the matrix is uploaded (the encoded column stream below).
+// The fp16-matrix passes with 2-byte operands run the same engine over a packed
+// 4-byte stream: wsell_pk.cuh.
 //
 // Layout (host: engine.cpp build_wsell; device arrays in TilesDev ws_*):
 //  * sort windows of kWsSort = 2048 consecutive rows; inside a window the rows are
@@ -18,8 +21,12 @@
 //  * a slice stores its entries chunk-major: chunk q (entries 4q..4q+3 of every
 //    lane's row) is 32 lanes x 4 entries, so lane l reads one 16-byte column quad
 //    and one 8/16/32-byte value quad per chunk, fully coalesced across the warp;
-//    a slice is as wide as its longest row rounded up to 4; missing entries carry
-//    the column kWsPad and are skipped (never added as zeros: -0 + +0 = +0);
+//    a slice is as wide as its longest row rounded up to 4;
+//  * per ring width (state.hpp ws_rn/ws_tw/ws_w) the columns are ENCODED on the
+//    device at upload (launch_setup.cu k_ws_encode): the byte offset of the ring slot
+//    for an entry inside its window's band, the offset of a slot that holds zero for
+//    padding (the padded value is +0 too, and a row accumulator is never -0, so the
+//    +-0 product leaves it unchanged), the column with bit 31 set for the rest;
 //  * ws_row maps slice lane -> matrix row; ws_cwin splits the windows over the
 //    CTAs by stored entries.
 // Each row is still summed by one thread in stored column order at
