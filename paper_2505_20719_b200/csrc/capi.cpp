@@ -145,9 +145,12 @@ int f3rg_matrix_engine(const f3rg_matrix* a) { return a ? a->m->shape() : -1; }
 int f3rg_wsell_pk_selfcheck(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx, uint32_t ctas,
                             uint64_t* stats) {
   return guarded([&] {
+   for (int cl = 1; cl >= 0; --cl) {  // both geometries; the statistics are the packed fp16 stream's (class 0)
+    const int64_t kPkTW = pk_tw(cl), kPkW = pk_w(cl), kPkRing = pk_ring(cl);
+    const uint32_t kPkLimit = pk_pad(cl), kPkPad = pk_pad(cl), kPkEsc = pk_esc(cl);
     PkLayoutHost L;
     try {
-      pk_build_layout(n, row_ptr, col_idx, ctas, L);
+      pk_build_layout(n, row_ptr, col_idx, ctas, L, cl);
     } catch (const std::length_error& e) {
       throw Error(ERR_UNSUPPORTED, e.what());
     }
@@ -203,6 +206,7 @@ int f3rg_wsell_pk_selfcheck(uint64_t n, const uint32_t* row_ptr, const uint32_t*
     if (rows_seen != n) fail(0, "not every row is stored exactly once");
     if (far != L.far) fail(0, "far count mismatch");
     if (stats) stats[0] = L.E, stats[1] = far, stats[2] = nsl, stats[3] = pads;
+   }
   });
 }
 

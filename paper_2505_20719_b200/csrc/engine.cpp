@@ -344,6 +344,27 @@ void DeviceMatrix::build_wsell_pk(const uint32_t* rp, const uint32_t* ci) {
   F3RG_CUDA(launch_pk_pack(Launch{}, dsrc.get<uint32_t>(), dcode.get<uint16_t>(), val_[0].get(),
                            pk_words_.get<uint32_t>(), pk_E_));
   F3RG_CUDA(cudaDeviceSynchronize());
+  // class 1 (4-byte rings: the L2 and L1 spmv_dots): the code stream as built, the fp32 and
+  // fp64 values scattered into the same slots on the device (padding / escape slots: +0)
+  PkLayoutHost L1;
+  try {
+    pk_build_layout(n_, rp, ci, (uint32_t)sm_count(), L1, 1);
+  } catch (const std::length_error& e) {
+    throw Error(ERR_UNSUPPORTED, e.what());
+  }
+  pk1_E_ = L1.E;
+  up(pk1_soff_, L1.soff.data(), L1.soff.size() * 4);
+  up(pk1_row_, L1.row.data(), L1.row.size() * 4);
+  up(pk1_cwin_, L1.cwin.data(), L1.cwin.size() * 4);
+  up(pk1_code_, L1.code.data(), L1.code.size() * 2);
+  DevBuf dsrc1;
+  up(dsrc1, L1.src.data(), L1.src.size() * 4);
+  for (int p = 1; p < 3; ++p) {
+    pk1_val_[p].alloc(pk1_E_ * psize(p) + 256);
+    F3RG_CUDA(launch_ws_scatter(Launch{}, (int)psize(p), dsrc1.get<uint32_t>(), val_[p].get(), pk1_val_[p].get(),
+                                pk1_E_, false));
+  }
+  F3RG_CUDA(cudaDeviceSynchronize());
 }
 
 double DeviceMatrix::stream_bytes(int pa) const {
@@ -351,6 +372,10 @@ double DeviceMatrix::stream_bytes(int pa) const {
   if (pk_E_ && pa == 0) {  // fp16 replica on the packed windowed layout: one 4-byte word per slot + slice tables
     const double nsl = (double)((n_ + kWsSortRows - 1) / kWsSortRows) * (kWsSortRows / 32);
     return (double)pk_E_ * 4.0 + nsl * 32.0 * 4.0 + (nsl + 1.0) * 4.0;
+  }
+  if (pk1_E_ && pa == 1) {  // fp32 replica on the class-1 code + value streams
+    const double nsl = (double)((n_ + kWsSortRows - 1) / kWsSortRows) * (kWsSortRows / 32);
+    return (double)pk1_E_ * 6.0 + nsl * 32.0 * 4.0 + (nsl + 1.0) * 4.0;
   }
   if (ws_E_) {  // windowed SELL: chunk-major columns + values (padding included), slice rows and offsets
     const double E = (double)ws_E_, nsl = (double)((n_ + kWsSortRows - 1) / kWsSortRows) * (kWsSortRows / 32);
@@ -406,6 +431,13 @@ TilesDev DeviceMatrix::tiles(int p) const {
       t.pk_row = pk_row_.get<const uint32_t>();
       t.pk_words = pk_words_.get<const uint32_t>();
       t.pk_cwin = pk_cwin_.get<const uint32_t>();
+    }
+    if (pk1_E_ && p >= 1) {
+      t.pk1_soff = pk1_soff_.get<const uint32_t>();
+      t.pk1_row = pk1_row_.get<const uint32_t>();
+      t.pk1_cwin = pk1_cwin_.get<const uint32_t>();
+      t.pk1_code = pk1_code_.get<const uint16_t>();
+      t.pk1_val = pk1_val_[p].get();
     }
   }
   return t;

@@ -47,6 +47,15 @@ constexpr uint32_t kWsFarBit = 0x80000000u;
 // high part of a far column (the low 16 bits are the next slot's code).
 constexpr int kPkTW = 8192, kPkRing = 49152, kPkW = (kPkRing - 2 * kPkTW) / 2;
 constexpr uint32_t kPkLimit = kPkRing - 1, kPkPad = kPkRing - 1, kPkEsc = kPkRing;
+// The same slot codes for 4-byte rings (class 1: fp32 / fp64 matrix, fp32 operand -- the L2
+// and L1 spmv_dots): 32,768 slots, 4096-row windows, band half-width 12,288; there the
+// codes and the values are two streams (2 + 4 or 8 bytes per slot). Class 0 is the packed
+// fp16 stream above.
+constexpr int pk_ring(int cl) { return cl == 0 ? kPkRing : 32768; }
+constexpr int pk_tw(int cl) { return cl == 0 ? kPkTW : 4096; }
+constexpr int pk_w(int cl) { return (pk_ring(cl) - 2 * pk_tw(cl)) / 2; }
+constexpr uint32_t pk_pad(int cl) { return (uint32_t)pk_ring(cl) - 1u; }  // = the first unusable slot
+constexpr uint32_t pk_esc(int cl) { return (uint32_t)pk_ring(cl); }
 
 struct TilesDev {
   const uint32_t* r0 = nullptr;  // ntiles+1 row starts
@@ -80,6 +89,13 @@ struct TilesDev {
   const uint32_t* pk_row = nullptr;
   const uint32_t* pk_words = nullptr;
   const uint32_t* pk_cwin = nullptr;
+  // the class-1 layout (4-byte rings) of the fp32 / fp64 replica: slice tables, the 16-bit
+  // code stream and the value stream at this replica's precision (null: none)
+  const uint32_t* pk1_soff = nullptr;
+  const uint32_t* pk1_row = nullptr;
+  const uint32_t* pk1_cwin = nullptr;
+  const uint16_t* pk1_code = nullptr;
+  const void* pk1_val = nullptr;
 };
 
 // Device-resident state of one FGMRES level. H is column-major: column j holds

@@ -45,9 +45,11 @@ struct PkLayoutHost {
 };
 
 // rp/ci: the matrix's CSR (n rows, square, n < 2^30); G: CTAs (one per SM)
-inline void pk_build_layout(uint64_t n, const uint32_t* rp, const uint32_t* ci, uint32_t G, PkLayoutHost& L) {
+// cl: ring class of the geometry (state.hpp pk_ring / pk_tw / pk_w): 0 the packed fp16 stream's, 1 the 4-byte rings'
+inline void pk_build_layout(uint64_t n, const uint32_t* rp, const uint32_t* ci, uint32_t G, PkLayoutHost& L, int cl = 0) {
   constexpr uint64_t SW = kWsSortRows, NS = kWsSortRows / 32;
-  constexpr int64_t TW = kPkTW, W = kPkW, RN = kPkRing;
+  const int64_t TW = pk_tw(cl), W = pk_w(cl), RN = pk_ring(cl);
+  const uint32_t kPkLimit = pk_pad(cl), kPkPad = pk_pad(cl), kPkEsc = pk_esc(cl);  // this class's codes
   if (n >= (1ull << 30)) throw std::length_error("packed windowed layout needs n < 2^30");
   const uint64_t nwin = (n + SW - 1) / SW, nsl = nwin * NS;
   L.G = G;

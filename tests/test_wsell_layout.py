@@ -2,7 +2,8 @@
 CPU through the C ABI (f3rg_wsell_pk_selfcheck): every row's slot sequence -- ring-slot
 codes, escape pairs of far columns, padding -- must decode back to the CSR row in stored
 order (the order the reference sums in, src/csr.cpp:23-37), far pairs must not straddle a
-quad, and band / far classification must follow the window geometry of state.hpp.
+quad, and band / far classification must follow the window geometry of state.hpp. The check
+runs for both geometries: the packed fp16 stream's (2-byte rings) and the 4-byte rings'.
 """
 import numpy as np
 import pytest
@@ -45,7 +46,9 @@ def test_band_edges_and_reserved_slot():
     rows = []
     for i in range(n):
         B = i // TW * TW
-        cand = {i, B - W, B - W - 1, B + TW + W - 1, B + TW + W, RING - 1, 2 * RING - 1, (i + 7) % n}
+        B1 = i // 4096 * 4096  # the 4-byte rings' geometry (class 1): 32,768 slots, 4096-row windows, W = 12,288
+        cand = {i, B - W, B - W - 1, B + TW + W - 1, B + TW + W, RING - 1, 2 * RING - 1, (i + 7) % n,
+                B1 - 12288, B1 - 12289, B1 + 4096 + 12288 - 1, B1 + 4096 + 12288, 32767, 65535}
         rows.append(sorted(c for c in cand if 0 <= c < n))
     rp, ci = _csr_from_rows(n, rows)
     st = f.wsell_pk_selfcheck(n, rp, ci, 5)
