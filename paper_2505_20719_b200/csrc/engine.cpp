@@ -344,8 +344,9 @@ void DeviceMatrix::build_wsell_pk(const uint32_t* rp, const uint32_t* ci) {
   F3RG_CUDA(launch_pk_pack(Launch{}, dsrc.get<uint32_t>(), dcode.get<uint16_t>(), val_[0].get(),
                            pk_words_.get<uint32_t>(), pk_E_));
   F3RG_CUDA(cudaDeviceSynchronize());
-  // class 1 (4-byte rings: the L2 and L1 spmv_dots): the code stream as built, the fp32 and
-  // fp64 values scattered into the same slots on the device (padding / escape slots: +0)
+  // class 1 (4-byte rings: the L2 and L1 spmv_dots, an fp16 matrix times an fp32 vector): the code
+  // stream as built, every replica's values scattered into the same slots on the device
+  // (padding / escape slots: +0)
   PkLayoutHost L1;
   try {
     pk_build_layout(n_, rp, ci, (uint32_t)sm_count(), L1, 1);
@@ -359,7 +360,7 @@ void DeviceMatrix::build_wsell_pk(const uint32_t* rp, const uint32_t* ci) {
   up(pk1_code_, L1.code.data(), L1.code.size() * 2);
   DevBuf dsrc1;
   up(dsrc1, L1.src.data(), L1.src.size() * 4);
-  for (int p = 1; p < 3; ++p) {
+  for (int p = 0; p < 3; ++p) {
     pk1_val_[p].alloc(pk1_E_ * psize(p) + 256);
     F3RG_CUDA(launch_ws_scatter(Launch{}, (int)psize(p), dsrc1.get<uint32_t>(), val_[p].get(), pk1_val_[p].get(),
                                 pk1_E_, false));
@@ -432,7 +433,7 @@ TilesDev DeviceMatrix::tiles(int p) const {
       t.pk_words = pk_words_.get<const uint32_t>();
       t.pk_cwin = pk_cwin_.get<const uint32_t>();
     }
-    if (pk1_E_ && p >= 1) {
+    if (pk1_E_) {
       t.pk1_soff = pk1_soff_.get<const uint32_t>();
       t.pk1_row = pk1_row_.get<const uint32_t>();
       t.pk1_cwin = pk1_cwin_.get<const uint32_t>();

@@ -158,7 +158,7 @@ class DeviceMatrix {
   // packed layout of the fp16 replica for the 2-byte-ring passes (wsell_pk_layout.hpp)
   DevBuf pk_soff_, pk_row_, pk_words_, pk_cwin_;
   uint64_t pk_E_ = 0, pk_far_ = 0;
-  // ... and the class-1 layout (4-byte rings) of the fp32 / fp64 replicas: codes + values
+  // ... and the class-1 layout (4-byte rings) of all three replicas: codes + values
   DevBuf pk1_soff_, pk1_row_, pk1_cwin_, pk1_code_, pk1_val_[3];
   uint64_t pk1_E_ = 0;
   void build_wsell_pk(const uint32_t* row_ptr, const uint32_t* col_idx);

@@ -319,9 +319,9 @@ template <int PA, int C, int IDX_, int CH = 0, class Gather, class Epi>
 __device__ __forceinline__ void spmv_tiles(const CsrDev& A, const TilesDev& T, Gather& g, Epi& e, uint8_t* smem) {
   if constexpr (idx_wsell(IDX_)) {
     // fp16 matrix and a 2-byte ring (Richardson on z1, the L3 spmv_dots, the fp16 SpMV): the packed stream
-    // ... and an fp32 / fp64 matrix with a 4-byte ring (the L2 and L1 spmv_dots): code + value streams
+    // ... and any matrix with a 4-byte ring (the L2 and L1 spmv_dots, fp16 A times fp32 x): code + value streams
     constexpr int RSZ = (int)sizeof(typename WsRing<Gather>::R);
-    if constexpr ((PA == P16 && RSZ == 2) || (PA != P16 && RSZ == 4)) wsell_pass_pk<PA, C>(A, T, g, e, smem);
+    if constexpr ((PA == P16 && RSZ == 2) || RSZ == 4) wsell_pass_pk<PA, C>(A, T, g, e, smem);
     else wsell_pass<PA, C>(A, T, g, e, smem);
   } else {
     spmv_row_tiles<PA, C, IDX_, CH>(A, T, g, e, smem);

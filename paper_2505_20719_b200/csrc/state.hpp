@@ -47,9 +47,9 @@ constexpr uint32_t kWsFarBit = 0x80000000u;
 // high part of a far column (the low 16 bits are the next slot's code).
 constexpr int kPkTW = 8192, kPkRing = 49152, kPkW = (kPkRing - 2 * kPkTW) / 2;
 constexpr uint32_t kPkLimit = kPkRing - 1, kPkPad = kPkRing - 1, kPkEsc = kPkRing;
-// The same slot codes for 4-byte rings (class 1: fp32 / fp64 matrix, fp32 operand -- the L2
-// and L1 spmv_dots): 32,768 slots, 4096-row windows, band half-width 12,288; there the
-// codes and the values are two streams (2 + 4 or 8 bytes per slot). Class 0 is the packed
+// The same slot codes for 4-byte rings (class 1: any replica, fp32 operand -- the L2
+// and L1 spmv_dots, fp16 A times fp32 x): 32,768 slots, 4096-row windows, band half-width 12,288; there the
+// codes and the values are two streams (2 + 2, 4 or 8 bytes per slot). Class 0 is the packed
 // fp16 stream above.
 constexpr int pk_ring(int cl) { return cl == 0 ? kPkRing : 32768; }
 constexpr int pk_tw(int cl) { return cl == 0 ? kPkTW : 4096; }
@@ -89,7 +89,7 @@ struct TilesDev {
   const uint32_t* pk_row = nullptr;
   const uint32_t* pk_words = nullptr;
   const uint32_t* pk_cwin = nullptr;
-  // the class-1 layout (4-byte rings) of the fp32 / fp64 replica: slice tables, the 16-bit
+  // the class-1 layout (4-byte rings) of this replica: slice tables, the 16-bit
   // code stream and the value stream at this replica's precision (null: none)
   const uint32_t* pk1_soff = nullptr;
   const uint32_t* pk1_row = nullptr;

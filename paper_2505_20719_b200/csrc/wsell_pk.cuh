@@ -11,9 +11,9 @@
 // to an accumulator that is never -0, so the results are bit-identical to wsell.cuh,
 // to the row tiles and to the reference (src/csr.cpp:23-37).
 //
-// The same pass serves the 4-byte rings of the fp32 / fp64 matrix (class 1, state.hpp pk_*:
-// the L2 and L1 spmv_dots) with the codes and the values as two streams of 2 and 4 / 8
-// bytes per slot.
+// The same pass serves every 4-byte ring (class 1, state.hpp pk_*: the L2 and L1 spmv_dots,
+// and the fp16 matrix times an fp32 vector) with the codes and the values as two streams of
+// 2 and 2 / 4 / 8 bytes per slot.
 //
 // Kernel windows lie on a global grid of kPkTW rows; a CTA owns whole sort windows and
 // may start and end inside a window. Ring invariant for the window at rows
